@@ -1,0 +1,413 @@
+"""RAGBoost context-index ORACLE — plain, slow, obviously correct CPU code.
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this
+module.  The product path (``paper_2511_03475_b200``) never imports it, and it
+shares no code with that path (no kernels, headers, helpers or constants).
+
+Every function cites the passage of /root/reference/PAPER.md (``PAPER:n`` =
+line n; section / equation named) it follows.  Where the paper is silent or
+ambiguous the reading is the one of SURVEY.md §8(c) (``X#``), all listed in
+DESIGN.md "Readings".
+
+Pins (tests/test_oracle_*.py): paper worked examples (PAPER:337, 344-348,
+378-382, 429-433, 454-462, 508-513), closed forms (identity, disjoint,
+footrule permutation, one shared doc), invariants, brute force against an
+independent K×K implementation (oracle/c), scipy complete linkage on tie-free
+matrices, greedy vs. NN-chain.
+"""
+from __future__ import annotations
+
+from fractions import Fraction
+
+import numpy as np
+
+PAD_ID = 0xFFFFFFFF
+
+
+class OracleError(ValueError):
+    pass
+
+
+# --------------------------------------------------------------------------- O1
+def validate(ids, lens=None):
+    """O1 / a1: K ∈ [1,255], 1 ≤ len_i ≤ K, DocId ≠ 0xFFFFFFFF, no duplicate DocId
+    within a context ("docs contains no duplicate DocId"; X5).  Returns the
+    contexts as Python lists of ints in retrieval order."""
+    ids = np.asarray(ids)
+    if ids.ndim != 2:
+        raise OracleError("ids must be [N, K]")
+    N, K = ids.shape
+    if N < 1 or not (1 <= K <= 255):
+        raise OracleError("bad N/K")
+    out = []
+    for i in range(N):
+        L = K if lens is None else int(lens[i])
+        if not (1 <= L <= K):
+            raise OracleError(f"len out of range at row {i}")
+        row = [int(x) for x in ids[i, :L]]
+        if any(x == PAD_ID for x in row):
+            raise OracleError(f"reserved DocId at row {i}")
+        if len(set(row)) != len(row):
+            raise OracleError(f"duplicate DocId in context {i}")
+        out.append(row)
+    return out
+
+
+# ------------------------------------------------------------------------ O2/O3
+def overlap(ci, cj):
+    """O2: S_ij (shared docs) and the positional sum Σ_{k∈S_ij} |p_i(k) − p_j(k)|
+    of Eq. 1, positions 0-based (X2).  A dict of positions, no
+    sorting tricks."""
+    pos_i = {doc: p for p, doc in enumerate(ci)}
+    pos_j = {doc: p for p, doc in enumerate(cj)}
+    s = 0
+    D = 0
+    for doc, pi in pos_i.items():
+        if doc in pos_j:
+            s += 1
+            D += abs(pi - pos_j[doc])
+    return s, D
+
+
+def distance_exact(ci, cj, alpha: Fraction) -> Fraction:
+    """Eq. 1 as an exact rational:
+    d_ij = 1 − |S_ij| / max(|C_i|,|C_j|) + α · Σ|p_i(k) − p_j(k)| / |S_ij|,
+    with the positional term 0 when S_ij = ∅ (X3)."""
+    s, D = overlap(ci, cj)
+    m = max(len(ci), len(cj))
+    if s == 0:
+        return Fraction(1)
+    return 1 - Fraction(s, m) + alpha * Fraction(D, s)
+
+
+def rn32(q: Fraction) -> np.float32:
+    """Correctly rounded (round-to-nearest-even) binary32 value of a non-negative
+    rational (X6: d := RN32 of the exact Eq. 1 value).  Picks among the float32
+    neighbours of the double approximation by exact rational distance."""
+    if q < 0:
+        raise OracleError("negative distance")
+    c0 = np.float32(float(q))
+    cands = {c0, np.nextafter(c0, np.float32(np.inf)), np.nextafter(c0, np.float32(0))}
+    best = None
+    for c in cands:
+        err = abs(Fraction(float(c)) - q)
+        key = (err, int(np.array(c, dtype=np.float32).view(np.uint32)) & 1)
+        if best is None or key < best[0]:
+            best = (key, c)
+    return np.float32(best[1])
+
+
+def distance(ci, cj, alpha: Fraction) -> np.float32:
+    """O3: canonical fp32 Eq. 1 distance = RN32(exact rational) (X6)."""
+    return rn32(distance_exact(ci, cj, alpha))
+
+
+def alpha_fraction(alpha, max_den: int = 1000) -> Fraction:
+    """X1: α is carried as an exact rational with denominator ≤ 1000
+    ("α ∈ [0.001, 0.01]")."""
+    return Fraction(alpha).limit_denominator(max_den)
+
+
+def pairwise(ctxs, alpha: Fraction):
+    """A2 ("compute pairwise distances between all contexts"): full
+    N×N matrices of s (uint8), D (uint16) and fp32 d.  O(N²·K) Python — small N."""
+    N = len(ctxs)
+    S = np.zeros((N, N), dtype=np.uint8)
+    Dm = np.zeros((N, N), dtype=np.uint16)
+    d = np.zeros((N, N), dtype=np.float32)
+    for i in range(N):
+        for j in range(i, N):
+            s, D = overlap(ctxs[i], ctxs[j])
+            v = distance(ctxs[i], ctxs[j], alpha)
+            S[i, j] = S[j, i] = s
+            Dm[i, j] = Dm[j, i] = D
+            d[i, j] = d[j, i] = v
+    return S, Dm, d
+
+
+# --------------------------------------------------------------------------- O4
+def row_nn(d: np.ndarray):
+    """O4: nn_i = argmin_{j≠i} (d_ij, j) (north_star "row-wise min/argmin").
+    N == 1 → (-1, +inf)."""
+    N = d.shape[0]
+    idx = np.full(N, -1, dtype=np.int32)
+    val = np.full(N, np.inf, dtype=np.float32)
+    for i in range(N):
+        best = None
+        for j in range(N):
+            if j == i:
+                continue
+            key = (d[i, j], j)
+            if best is None or key < best:
+                best = key
+        if best is not None:
+            val[i], idx[i] = best
+    return idx, val
+
+
+# --------------------------------------------------------------------------- O5
+def linkage_greedy(d: np.ndarray):
+    """O5 ("iteratively merge the closest pair"): greedy complete
+    linkage (X7) with the tie key (D(A,B), min rep, max rep), rep = smallest leaf
+    index of a cluster (X8).  D(A∪B, C) = max(D(A,C), D(B,C)) is the maximum over
+    member pairs.  Brute force: every step scans every active pair.  Returns rows
+    (rep_a < rep_b, h, size) in merge order."""
+    N = d.shape[0]
+    size = {i: 1 for i in range(N)}
+    dist = {}
+    for i in range(N):
+        for j in range(i + 1, N):
+            dist[(i, j)] = d[i, j]
+    Z = []
+    while len(size) > 1:
+        best = None
+        act = sorted(size)
+        for x in range(len(act)):
+            for y in range(x + 1, len(act)):
+                a, b = act[x], act[y]
+                key = (dist[(a, b)], a, b)
+                if best is None or key < best:
+                    best = key
+        h, a, b = best
+        Z.append((a, b, np.float32(h), size[a] + size[b]))
+        for c in size:
+            if c in (a, b):
+                continue
+            dac = dist[(min(a, c), max(a, c))]
+            dbc = dist[(min(b, c), max(b, c))]
+            dist[(min(a, c), max(a, c))] = max(dac, dbc)
+        size[a] += size.pop(b)
+    return Z
+
+
+def linkage_nn_chain(d: np.ndarray):
+    """O5 by an independent algorithm: nearest-neighbour chain (valid because
+    complete linkage is reducible; X7/X8).  Merges are emitted in chain order and
+    then sorted by the key (h, rep_a, rep_b), which is the greedy order (X9).
+    numpy row scans; medium N."""
+    N = d.shape[0]
+    D = d.astype(np.float64).copy()
+    np.fill_diagonal(D, np.inf)
+    active = np.ones(N, dtype=bool)
+    size = np.ones(N, dtype=np.int64)
+    idx = np.arange(N)
+    Z = []
+    chain = []
+    remaining = N
+    while remaining > 1:
+        if not chain:
+            chain.append(int(np.flatnonzero(active)[0]))
+        x = chain[-1]
+        row = np.where(active, D[x], np.inf)
+        row[x] = np.inf
+        m = row.min()
+        # tie key (d, min rep, max rep): for fixed x this orders candidates by rep.
+        y = int(idx[(row == m) & active & (idx != x)].min())
+        if len(chain) >= 2 and chain[-2] == y:
+            chain.pop()
+            chain.pop()
+            a, b = min(x, y), max(x, y)
+            Z.append((a, b, np.float32(m), int(size[a] + size[b])))
+            newrow = np.maximum(D[a], D[b])
+            D[a, :] = newrow
+            D[:, a] = newrow
+            D[a, a] = np.inf
+            active[b] = False
+            D[b, :] = np.inf
+            D[:, b] = np.inf
+            size[a] += size[b]
+            remaining -= 1
+        else:
+            chain.append(y)
+    Z.sort(key=lambda z: (float(z[2]), z[0], z[1]))
+    return Z
+
+
+def cluster_height(d: np.ndarray, A, B) -> np.float32:
+    """Complete-linkage distance by its definition: max over member pairs."""
+    return np.float32(max(d[a, b] for a in A for b in B))
+
+
+# ------------------------------------------------------------------------ O6-O8
+class Tree:
+    """O6-O8 result: nodes with parent, children (ordered by rep), set, ordered
+    context; leaf paths; offline orders; schedule."""
+
+    def __init__(self):
+        self.parent = []
+        self.children = []
+        self.docset = []
+        self.rep = []
+        self.leaf_of = []   # node -> leaf index or -1
+        self.ordered = []   # node -> list
+        self.leaf_node = []  # leaf index -> node
+        self.path = []       # leaf index -> list of child indices
+
+
+def build_tree(ctxs, Z) -> Tree:
+    """O6: replay the merges; each merge makes a virtual
+    node whose set is the intersection of its children's sets ("virtual node
+    whose context is the sorted intersection"); an empty root sits on top
+    ("root represents an empty context").  Virtual nodes whose set equals their
+    parent's are collapsed (X11); children are ordered by rep (X12).  O7: ordered
+    contexts top-down (X10, X13).  O8: leaf paths ("each leaf node
+    records its search path from the root")."""
+    N = len(ctxs)
+    # raw binary tree
+    r_children = [[] for _ in range(N)]
+    r_set = [frozenset(c) for c in ctxs]
+    r_rep = list(range(N))
+    node_of = {i: i for i in range(N)}  # cluster rep -> current raw node
+    for (a, b, _h, _sz) in Z:
+        na, nb = node_of[a], node_of[b]
+        v = len(r_set)
+        r_children.append([na, nb])
+        r_set.append(r_set[na] & r_set[nb])
+        r_rep.append(min(r_rep[na], r_rep[nb]))
+        node_of[min(a, b)] = v
+        del node_of[max(a, b)]
+    if len(node_of) != 1:
+        raise OracleError("linkage does not join all contexts")
+    top = next(iter(node_of.values()))
+
+    t = Tree()
+    t.leaf_node = [-1] * N
+    t.path = [None] * N
+
+    def new_node(parent, s, rep, leaf):
+        k = len(t.parent)
+        t.parent.append(parent)
+        t.children.append([])
+        t.docset.append(s)
+        t.rep.append(rep)
+        t.leaf_of.append(leaf)
+        t.ordered.append(None)
+        if leaf >= 0:
+            t.leaf_node[leaf] = k
+        return k
+
+    root = new_node(-1, frozenset(), -1, -1)
+    t.ordered[root] = []
+
+    def expand(raw, parent_set):
+        # collapse a virtual node whose set equals its parent's (X11)
+        if raw >= N and r_set[raw] == parent_set:
+            out = []
+            for c in r_children[raw]:
+                out.extend(expand(c, parent_set))
+            return out
+        return [raw]
+
+    stack = [(root, top)]
+    pending = [(root, [top])]
+    while pending:
+        node, raws = pending.pop()
+        kids = []
+        for r in raws:
+            kids.extend(expand(r, t.docset[node]))
+        kids.sort(key=lambda r: r_rep[r])  # X12
+        for r in kids:
+            leaf = r if r < N else -1
+            k = new_node(node, r_set[r], r_rep[r], leaf)
+            t.children[node].append(k)
+            par_ord = t.ordered[node]
+            par_set = t.docset[node]
+            if leaf >= 0:
+                # leaf: parent's prefix ++ remaining docs in original order
+                t.ordered[k] = par_ord + [x for x in ctxs[leaf] if x not in par_set]
+            else:
+                # virtual: parent's prefix ++ ascending new docs (X10)
+                t.ordered[k] = par_ord + sorted(r_set[r] - par_set)
+                pending.append((k, r_children[r]))
+    del stack
+    # paths
+    for leaf in range(N):
+        p = []
+        k = t.leaf_node[leaf]
+        while t.parent[k] != -1:
+            par = t.parent[k]
+            p.append(t.children[par].index(k))
+            k = par
+        t.path[leaf] = p[::-1]
+    return t
+
+
+def offline_order(ctxs, t: Tree):
+    """O7: each indexed context becomes its leaf's ordered list
+    (matched prefix, then the rest in original order); prefix_len = |ord(parent)|."""
+    out = []
+    plen = []
+    for i in range(len(ctxs)):
+        k = t.leaf_node[i]
+        out.append(list(t.ordered[k]))
+        plen.append(len(t.ordered[t.parent[k]]))
+    return out, plen
+
+
+def schedule(paths):
+    """O8: group by the first element of the search
+    path, groups in order of first appearance (X14); within a group sort by path
+    length descending, ties by input index."""
+    groups = {}
+    order = []
+    for i, p in enumerate(paths):
+        key = ("empty", i) if len(p) == 0 else p[0]
+        if key not in groups:
+            groups[key] = []
+            order.append(key)
+        groups[key].append(i)
+    out = []
+    for key in order:
+        out.extend(sorted(groups[key], key=lambda i: (-len(paths[i]), i)))
+    return out
+
+
+def traverse(t: Tree, path):
+    """Context traversal: follow child indices from the root."""
+    k = 0
+    for step in path:
+        k = t.children[k][step]
+    return k
+
+
+# --------------------------------------------------------------------------- O9
+class Session:
+    """O9: the session's seen set starts as the turn-0 context
+    ("follows its stored search path to the first-turn context") and grows by
+    each turn's novel docs ("appended to a copy of the first-turn context state")
+    (X18)."""
+
+    def __init__(self, turn0_docs):
+        self.turn = 0
+        self.seen = {}
+        for x in turn0_docs:
+            self.seen.setdefault(int(x), 0)
+
+    def dedup_turn(self, docs):
+        """Novel docs in retrieval order; refs (doc, first-seen turn) in retrieval
+        order ("These are filtered out, leaving only the novel
+        document")."""
+        self.turn += 1
+        docs = [int(x) for x in docs]
+        if len(set(docs)) != len(docs):
+            raise OracleError("duplicate DocId in retrieval")
+        novel = [x for x in docs if x not in self.seen]
+        refs = [(x, self.seen[x]) for x in docs if x in self.seen]
+        for x in novel:
+            self.seen[x] = self.turn
+        return novel, refs
+
+
+# ------------------------------------------------------------------------- all
+def build_index(ids, lens=None, alpha=Fraction(1, 200)):
+    """Whole path O1-O8 for small N (pure Python distances)."""
+    ctxs = validate(ids, lens)
+    S, Dm, d = pairwise(ctxs, alpha)
+    nn_idx, nn_d = row_nn(d)
+    Z = linkage_greedy(d) if len(ctxs) <= 96 else linkage_nn_chain(d)
+    t = build_tree(ctxs, Z)
+    ordered, plen = offline_order(ctxs, t)
+    sched = schedule(t.path)
+    return dict(S=S, D=Dm, d=d, nn_idx=nn_idx, nn_d=nn_d, Z=Z, tree=t, ordered=ordered,
+                prefix_len=plen, schedule=sched)
