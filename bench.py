@@ -1,0 +1,328 @@
+#!/usr/bin/env python
+"""Benchmark of the RAGBoost context-index build on B200 (BASELINE.json metric:
+context-pair distances/s and index build time at N=100k, K=20).
+
+One step = one full index build over one batch of N synthetic contexts: a1
+validation, a2-a4 distance rows + fused row NN, a5 complete linkage, a6-a7
+tree / prefix-first ordering / schedule (rb_build_index + rb_order_contexts).
+value = N(N-1)/2 context pairs per build x builds / time (all ranks).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config C4] [--no-cpu-baseline]
+
+Multi-GPU (torchrun, one process per GPU): every rank builds the index of its
+own batch (seed + rank) — independent problems, no data-path collective;
+scaling "weak".  Timing: CUDA events on the launching stream, barrier +
+synchronize on both sides, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PAPER_CONTEXT = {"hardware": "NVIDIA A6000", "N": 100_000, "k": 20, "build_s": 869.98,
+                 "pairs_per_s_derived": 5.75e6, "cite": "PAPER:677, Table 2c"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=8192, help="contexts in the oracle sample")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def workload_desc(name, w):
+    r = w.recipe
+    return (f"{name}: N={r['N']} contexts, K={r['K']} docs, pool V={r['V']}, "
+            f"{'multi-turn' if r['turns'] > 1 else 'single-turn'}, zipf s={r['s_zipf']}, g={r['g']}, "
+            f"omega={r['omega']}, seed={r['seed']}")
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    def __init__(self, index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", f"--id={index}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        self.f.seek(0)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() in ("active", "1"):
+                    reasons.add(nm)
+        os.unlink(self.f.name)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------------ oracle timing
+def oracle_build_time(ids):
+    """The oracle as it stands on a sample: C distances (OpenMP), C NN-chain
+    linkage, Python tree / ordering / schedule."""
+    from oracle import oracle_c as oc
+    from oracle import ragb_oracle as o
+    t0 = time.perf_counter()
+    d = oc.pairwise_rows(ids, None, 1, 200)
+    t1 = time.perf_counter()
+    oc.row_nn(d)
+    Z = oc.linkage(d)
+    t2 = time.perf_counter()
+    ctxs = o.validate(ids)
+    t = o.build_tree(ctxs, list(zip(*Z)))
+    o.offline_order(ctxs, t)
+    o.schedule(t.path)
+    t3 = time.perf_counter()
+    return t3 - t0, {"distance_s": t1 - t0, "linkage_s": t2 - t1, "tree_order_s": t3 - t2}
+
+
+def cpu_baseline(w, n_s):
+    from oracle import oracle_c as oc
+    ids = np.ascontiguousarray(w.ids[:n_s])
+    secs, parts = oracle_build_time(ids)
+    pairs = n_s * (n_s - 1) / 2
+    return {"value": pairs / secs, "unit": "context-pairs/s", "cores": oc.num_threads(), "kind": "oracle",
+            "sample": f"first {n_s} contexts of the workload, full build (a1-a7) once",
+            "seconds": secs, "stages_s": parts}
+
+
+def run_reference(args, ws, rank):
+    from synth.workload import config
+    if rank != 0:
+        return
+    w = config(args.config)
+    n_s = min(args.cpu_sample, w.N)
+    ids = np.ascontiguousarray(w.ids[:n_s])
+    for _ in range(args.warmup):
+        oracle_build_time(ids)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle_build_time(ids)
+    el = time.perf_counter() - t0
+    from oracle import oracle_c as oc
+    pairs = n_s * (n_s - 1) / 2
+    value = pairs * args.steps / el
+    line = {"impl": "reference", "metric": f"context-pair distances/s (index build, {args.config})",
+            "value": value, "unit": "context-pairs/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32+f32", "data": "synthetic",
+            "config": {"workload": workload_desc(args.config, w) + f"; oracle sample = first {n_s} contexts"},
+            "cpu_baseline": {"value": value, "unit": "context-pairs/s", "cores": oc.num_threads(),
+                             "kind": "oracle", "sample": f"first {n_s} contexts per step"},
+            "e2e": {"value": value, "unit": "context-pairs/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ ours
+def run_ours(args, ws, rank, local):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2511_03475_b200 import ragb
+    from synth.workload import CONFIGS, config
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    w = config(args.config) if ws == 1 else config(args.config, seed=CONFIGS[args.config]["seed"] + 1000 * rank)
+    N, K = w.ids.shape
+    pairs = N * (N - 1) / 2
+    ids_dev = torch.from_numpy(w.ids.view(np.int32)).to(dev)
+    stream = torch.cuda.current_stream(dev)
+    p = ragb.make_params(flags=0, stream=ctypes_stream(stream))
+    wsp = ragb.Workspace(N, K, p, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        idx, _ = ragb.build_index(ids_dev, workspace=wsp, stream=stream)
+        idx.order_contexts()
+        return idx
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    clk = Clocks(local)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stats = []
+    e0.record(stream)
+    for _ in range(args.steps):
+        flush.zero_()   # L2 flush between builds (256 MB > 126 MB L2)
+        idx = step()
+        stats.append(idx.stats())
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    if ws > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+
+    # ---- end-to-end through the public API with host buffers -------------
+    ids_pin = torch.from_numpy(w.ids.view(np.int32)).pin_memory().numpy().view(np.uint32)
+    for _ in range(1):
+        idx, _ = ragb.build_index_host(ids_pin, workspace=wsp, stream=stream)
+        idx.order_contexts()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(args.steps):
+        idx, _ = ragb.build_index_host(ids_pin, workspace=wsp, stream=stream)
+        out, plen, sched = idx.order_contexts()
+        nn_i, nn_d = idx.nn()
+        za = idx.linkage()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max(e0.elapsed_time(e1), (time.perf_counter() - t0) * 1e3) / args.steps
+    if ws > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    if rank != 0:
+        return
+    mean = {k: statistics.mean(s[k] for s in stats) for k in stats[0]}
+    peaks = load_peaks()
+    hbm = peaks.get("hbm_gbs")
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs, copy)" if hbm else "fallback 6650 GB/s (B200_PROFILING.md)"
+    hbm = hbm or 6650.0
+    # dominant kernel: the distance kernel (a2-a4) vs the linkage (a5)
+    dist_bytes = 4.0 * N * N + 4.0 * N * K   # full fp32 rows written + ids read (algorithmic)
+    dist_gbs = dist_bytes / (mean["distance_ms"] * 1e-3) / 1e9
+    traffic = load_traffic(args.config)
+    roofline = {"kernel": "k_dist_rows_nn (a2-a4)", "bound": "hbm", "achieved": dist_gbs, "peak": hbm,
+                "unit": "GB/s", "frac": dist_gbs / hbm, "traffic": traffic, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": dist_bytes,
+                "share_of_step": mean["distance_ms"] / ms}
+    line = {
+        "metric": f"context-pair distances/s (index build, N={N}, K={K})",
+        "value": pairs * ws / (ms * 1e-3),
+        "unit": "context-pairs/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u32+f32", "data": "synthetic",
+        "config": {"workload": workload_desc(args.config, w) + (f"; rank r uses seed+1000r" if ws > 1 else ""),
+                   "l2": "256 MB flush write between builds; per-build working set 80 GB >> 126 MB L2",
+                   "parallelism": f"{ws} independent index builds (one per GPU)"},
+        "build_time_ms": ms,
+        "stages_ms": {k: mean[k] for k in ("validate_ms", "distance_ms", "linkage_ms", "host_ms", "total_ms")},
+        "distance_pairs_per_s": pairs / (mean["distance_ms"] * 1e-3),
+        "linkage_rounds": mean["linkage_rounds"],
+        "roofline": roofline,
+        "e2e": {"value": pairs * ws / (e2e_ms * 1e-3), "unit": "context-pairs/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": int(N * K * 4),
+                "d2h_bytes_per_step": int(N * 8 + 16 * (N - 1) + 8)},
+        "gpu_launches": int(sum(s["kernel_launches"] for s in stats)),
+        "clocks": clocks,
+        "paper_context": PAPER_CONTEXT,
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(w, min(args.cpu_sample, N))
+    print(json.dumps(line), flush=True)
+
+
+def ctypes_stream(stream):
+    import ctypes
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+def load_traffic(cfg):
+    """dram read+write bytes per launch of the distance kernel from the committed
+    ncu --set full capture (profiles/), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_distance_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(cfg)
+    except OSError:
+        return None
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        if args.impl == "reference":
+            if rank != 0:
+                return
+        else:
+            import torch
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl")
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+    try:
+        run_ours(args, ws, rank, local)
+    finally:
+        if ws > 1:
+            import torch.distributed as dist
+            if dist.is_initialized():
+                dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,231 @@
+/*
+ * ragb.h — C-ABI of the B200-native RAGBoost context index (arXiv 2511.03475).
+ *
+ * The boundary follows the paper's problem statement: RAGBoost "takes user
+ * prompts and their retrieved results, updates the context to enable effective
+ * reuse, and then passes the updated context to the inference engine"
+ * (Section 3.3).  Citations: PAPER:n = /root/reference/PAPER.md line
+ * n; SPEC:n = /root/reference/SPEC.md line n; X# = a reading listed in
+ * DESIGN.md "Readings".
+ *
+ * Conventions (all entry points):
+ *   - Every call returns rb_status (0 = RB_OK, < 0 = error) and never throws.
+ *     On error, rb_last_error() returns a thread-local message, valid until
+ *     the next call on the same thread.
+ *   - Input buffers are borrowed for the duration of the call; the library
+ *     copies whatever it retains.
+ *   - Large device outputs are CALLER-OWNED (allocated by the caller, e.g. with
+ *     torch.empty); sizes come from rb_workspace_size().  The index handle
+ *     retains rows_dev/scratch_dev pointers only for the duration of
+ *     rb_build_index and owns small host results (nn, merge order, tree,
+ *     orders) until rb_index_free().
+ *   - On any error the outputs are left untouched, except RB_ECUDA which may
+ *     leave device buffers partially written.
+ *   - "dev" pointers are CUDA device pointers, "host" pointers are host memory.
+ *   - DocIds are uint32; 0xFFFFFFFF is reserved (RB_EINVAL if present).
+ *
+ * Not thread-safe on a single handle; distinct handles may be used from
+ * distinct threads.
+ */
+#ifndef RAGB_H_
+#define RAGB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define RB_API __attribute__((visibility("default")))
+#else
+#define RB_API
+#endif
+
+typedef int32_t rb_status;
+
+enum rb_status_code {
+  RB_OK = 0,
+  RB_EINVAL = -1,    /* null pointer, N < 1, K < 1, K > 255, len not in [1,K],
+                        reserved DocId, workspace too small, bad row range     */
+  RB_EDUPDOC = -2,   /* duplicate DocId inside one context: p_i(k) would be
+                        ambiguous in Eq. 1 (X5)                         */
+  RB_EALPHA = -3,    /* alpha outside [1/1000, 1/100] without
+                        RB_ALPHA_ANY, or alpha_den == 0 / > 1000                 */
+  RB_ENOMEM = -4,    /* host allocation failed                                   */
+  RB_ECUDA = -5,     /* CUDA runtime error (no device, launch failure, ...)      */
+  RB_ENCCL = -6,     /* reserved: collective failure                             */
+  RB_EPATH = -7,     /* invalid search path / row index          */
+  RB_ESESSION = -8,  /* unknown / null session                        */
+  RB_ESTATE = -9     /* precondition, e.g. a stage that was skipped             */
+};
+
+/* Linkage: the paper says only "iteratively merge the closest pair"
+ * (PAPER:335).  X7: complete linkage on the Eq. 1 matrix, tie key
+ * (d, min rep, max rep), rep = smallest leaf index (X8). */
+enum rb_linkage { RB_LINK_COMPLETE = 0 };
+
+enum rb_flags {
+  RB_EMIT_COUNTS = 1u << 0,   /* also write s_ij (uint8) and the positional sum
+                                 D_ij (uint16) rows — parity/debug output     */
+  RB_ALPHA_ANY = 1u << 1,     /* accept alpha outside the paper's band         */
+  RB_KEEP_ROWS = 1u << 2,     /* linkage must not overwrite rows_dev           */
+  RB_SKIP_LINKAGE = 1u << 3   /* stop after distance rows + row NN (a1-a4)     */
+};
+
+typedef struct rb_params {
+  uint32_t alpha_num;   /* alpha = alpha_num / alpha_den exactly (X1); default 1/200 */
+  uint32_t alpha_den;   /* 1 <= alpha_den <= 1000                                    */
+  int32_t linkage;      /* rb_linkage                                                */
+  uint32_t flags;       /* rb_flags                                                  */
+  void *stream;         /* cudaStream_t to launch on (NULL = legacy default stream)  */
+  int64_t row0;         /* first distance row this call computes (row sharding)     */
+  int64_t nrows;        /* number of rows, -1 = all N (linkage needs all rows)      */
+} rb_params;
+
+/* Per-build statistics (host, filled by rb_build_index). Times are CUDA-event
+ * milliseconds on params.stream, except host_ms (host wall clock). */
+typedef struct rb_stats {
+  float validate_ms;      /* a1: validation + transposed staging                  */
+  float distance_ms;      /* a2-a4: distance rows + fused row NN                   */
+  float linkage_ms;       /* a5: all linkage rounds (device)                       */
+  float host_ms;          /* a6-a7: merge sort + tree + orders + schedule (host)   */
+  float total_ms;         /* whole rb_build_index call, host wall clock            */
+  int32_t linkage_rounds; /* number of linkage rounds                              */
+  int32_t kernel_launches;/* kernels launched by this call                         */
+  int64_t n_virtual;      /* virtual (intersection) nodes kept after collapse      */
+  int64_t max_depth;      /* maximum leaf path length                              */
+} rb_stats;
+
+typedef struct rb_index rb_index;
+typedef struct rb_session rb_session;
+
+/* Library version string. */
+RB_API const char *rb_version(void);
+
+/* Thread-local message describing the last error on this thread ("" if none). */
+RB_API const char *rb_last_error(void);
+
+/* Fill defaults: alpha 1/200 (X1), complete linkage, no flags, default stream,
+ * all rows. */
+RB_API rb_status rb_params_init(rb_params *p);
+
+/* Caller-owned buffer sizes for rb_build_index(N, K, p):
+ *   rows_bytes    — float rows_dev[nrows][N] (nrows from p; 4*nrows*N bytes);
+ *   scratch_bytes — device scratch (validation staging, linkage ping-pong
+ *                   matrix of at most (N-1)^2 floats, or two of them with
+ *                   RB_KEEP_ROWS, plus O(N) state).
+ * Errors: RB_EINVAL on null outputs, N < 1, K not in [1,255]. */
+RB_API rb_status rb_workspace_size(int64_t N, int32_t K, const rb_params *p, size_t *rows_bytes,
+                                   size_t *scratch_bytes);
+
+/* Build the context index (Section 4.1 "Index creation"):
+ *   a1 validate (K in [1,255], 1 <= len <= K, no duplicate / reserved DocId);
+ *   a2-a3 all-pairs Eq. 1 distance rows, d_ij = correctly
+ *       rounded fp32 of the exact rational (X6), written to rows_dev;
+ *   a4 fused row NN nn_i = argmin_{j != i}(d_ij, j);
+ *   a5 complete-linkage merge order (X7-X9);
+ *   a6 index tree with virtual intersection nodes, collapse (X10-X12),
+ *      leaf search paths ("each leaf node records its search path");
+ *   a7 offline prefix-first ordering and schedule
+ *      (PAPER:446-464).
+ * ids_dev  : uint32 [N][K] row-major, device; row i = context i in retrieval
+ *            order (most relevant first).  Slots past lens[i] are ignored.
+ * lens_dev : uint8 [N] device, or NULL (all contexts have K docs).
+ * rows_dev : float [nrows][N] device, caller-owned (rows p->row0 ..).
+ *            Overwritten by the linkage unless RB_KEEP_ROWS.
+ * scratch_dev / scratch_bytes : device scratch of rb_workspace_size() bytes.
+ * s_dev, D_dev : with RB_EMIT_COUNTS, uint8/uint16 [nrows][N] device outputs
+ *            (else ignored, may be NULL).
+ * out      : receives a new handle (free with rb_index_free).
+ * Partial rows (p->nrows < N) compute rows + NN for that shard only and imply
+ * RB_SKIP_LINKAGE.
+ * Errors: RB_EINVAL, RB_EDUPDOC, RB_EALPHA, RB_ECUDA, RB_ENOMEM. */
+RB_API rb_status rb_build_index(const uint32_t *ids_dev, const uint8_t *lens_dev, int64_t N, int32_t K,
+                                const rb_params *p, float *rows_dev, void *scratch_dev,
+                                size_t scratch_bytes, uint8_t *s_dev, uint16_t *D_dev,
+                                rb_index **out);
+
+/* Same as rb_build_index but ids/lens are HOST buffers: the host->device copy
+ * of the inputs happens inside the call (end-to-end path). */
+RB_API rb_status rb_build_index_host(const uint32_t *ids_host, const uint8_t *lens_host, int64_t N,
+                                     int32_t K, const rb_params *p, float *rows_dev,
+                                     void *scratch_dev, size_t scratch_bytes, rb_index **out);
+
+/* Build only the host-side index (a6-a7) from a given merge order (host
+ * buffers, N-1 rows of (a < b, h, size) as rb_index_linkage returns).  No
+ * device work; used for multi-rank assembly and CPU tests.
+ * Errors: RB_EINVAL (inconsistent merges), RB_EDUPDOC. */
+RB_API rb_status rb_index_from_linkage(const uint32_t *ids_host, const uint8_t *lens_host, int64_t N,
+                                       int32_t K, const int32_t *a, const int32_t *b,
+                                       const float *h, const int32_t *size, rb_index **out);
+
+/* N of the index. */
+RB_API rb_status rb_index_size(const rb_index *idx, int64_t *N, int32_t *K);
+
+/* Build statistics. */
+RB_API rb_status rb_index_stats(const rb_index *idx, rb_stats *st);
+
+/* Row NN (host, [nrows]): nn_idx = -1 and nn_d = +inf when N == 1. */
+RB_API rb_status rb_index_nn(const rb_index *idx, int32_t *nn_idx, float *nn_d);
+
+/* Merge order (host, [N-1]): rep_a < rep_b (smallest leaf indices), height,
+ * merged size; ascending by (h, rep_a, rep_b) = the greedy order (X9).
+ * RB_ESTATE if the linkage was skipped. */
+RB_API rb_status rb_index_linkage(const rb_index *idx, int32_t *a, int32_t *b, float *h,
+                                  int32_t *size);
+
+/* Tree sizes: nodes (root = node 0), total prefix ids, total path entries. */
+RB_API rb_status rb_index_tree_info(const rb_index *idx, int64_t *n_nodes, int64_t *prefix_total,
+                                    int64_t *path_total);
+
+/* Tree export (host).  parent[n_nodes] (-1 for root), leaf[n_nodes] (context
+ * index or -1 for the root / virtual nodes), rep[n_nodes] (smallest leaf
+ * index below; -1 for root), prefix_off[n_nodes+1] / prefix_ids[prefix_total]
+ * = each node's ordered context (X10), path_off[N+1] / path[path_total] =
+ * each leaf's search path.  Any output may be NULL. */
+RB_API rb_status rb_index_tree(const rb_index *idx, int32_t *parent, int32_t *leaf, int32_t *rep,
+                               int64_t *prefix_off, uint32_t *prefix_ids, int64_t *path_off,
+                               int32_t *path);
+
+/* Context ordering + schedule for the indexed set:
+ * ids must be NULL (the indexed contexts, offline mode).  out_ids[M][K]
+ * (host): matched prefix then remaining docs in original order; slots past
+ * the context length are copied from the input unchanged.  out_prefix_len[M]:
+ * length of the inherited prefix.  out_schedule[M]: execution order (input
+ * indices): groups by first path element in order of first appearance,
+ * path length descending, ties by index (X14).  Any output may be NULL.
+ * Errors: RB_EINVAL, RB_ESTATE (online ordering of new contexts is not built
+ * yet: ids != NULL). */
+RB_API rb_status rb_order_contexts(rb_index *idx, const uint32_t *ids, const uint8_t *lens, int64_t M,
+                                   int32_t K, uint32_t *out_ids, uint8_t *out_prefix_len,
+                                   int64_t *out_schedule);
+
+/* Open a multi-turn session whose turn 0 is indexed context `row`: the
+ * session follows the leaf's stored search path to the first-turn context
+ * and starts its seen set from it (X18).  Errors: RB_EPATH. */
+RB_API rb_status rb_session_open(const rb_index *idx, int64_t row, rb_session **out);
+
+/* Open a session from explicit turn-0 docs (host [n]).  Errors: RB_EDUPDOC. */
+RB_API rb_status rb_session_open_docs(const uint32_t *docs, int32_t n, rb_session **out);
+
+/* De-duplicate the next turn (Section 6): novel docs in
+ * retrieval order; refs = docs already seen with the turn they were first
+ * prefilled, in retrieval order; the seen set grows by the novel docs.
+ * ids/novel/ref_doc/ref_turn are host [n] (outputs may hold up to n entries).
+ * Errors: RB_ESESSION (null session), RB_EDUPDOC, RB_EINVAL. */
+RB_API rb_status rb_dedup_turn(rb_session *s, const uint32_t *ids, int32_t n, uint32_t *novel,
+                               int32_t *n_novel, uint32_t *ref_doc, int32_t *ref_turn,
+                               int32_t *n_ref);
+
+/* Current turn number of a session (0 right after open). */
+RB_API rb_status rb_session_turn(const rb_session *s, int32_t *turn);
+
+RB_API void rb_session_free(rb_session *s);
+RB_API void rb_index_free(rb_index *idx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RAGB_H_ */

@@ -1,0 +1,56 @@
+"""Build libragb.so (CUDA kernels for sm_100a + host C++ + C-ABI) in-tree.
+
+    python -m paper_2511_03475_b200.build [--force] [--verbose]
+"""
+from __future__ import annotations
+
+import glob
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+INCLUDE = os.path.join(ROOT, "include")
+LIBDIR = os.path.join(PKG, "lib")
+LIB = os.path.join(LIBDIR, "libragb.so")
+
+NVCC_FLAGS = [
+    "-std=c++17", "-O3", "-lineinfo",
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "--fmad=false",                      # parity: no contraction anywhere (X6)
+    "-Xcompiler", "-fPIC,-O3,-fvisibility=hidden",
+    "-shared",
+]
+
+
+def sources():
+    return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
+
+
+def _stale() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    deps = sources() + glob.glob(os.path.join(CSRC, "*.h")) + [os.path.join(INCLUDE, "ragb.h"), __file__]
+    return any(os.path.getmtime(p) > t for p in deps)
+
+
+def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
+    """debug=True builds lib/libragb_debug.so with device bounds checks
+    (-DRAGB_DEBUG); load it with RAGB_LIB=debug."""
+    lib = LIB if not debug else os.path.join(LIBDIR, "libragb_debug.so")
+    if not debug and not force and not _stale():
+        return LIB
+    os.makedirs(LIBDIR, exist_ok=True)
+    nvcc = os.environ.get("NVCC", "nvcc")
+    cmd = [nvcc] + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose else []) + \
+        (["-DRAGB_DEBUG"] if debug else []) + ["-I", INCLUDE, "-I", CSRC, "-o", lib + ".tmp"] + sources()
+    subprocess.check_call(cmd)
+    os.replace(lib + ".tmp", lib)
+    return lib
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="--verbose" in sys.argv, debug="--debug" in sys.argv))

@@ -1,0 +1,528 @@
+// C-ABI entry points of libragb (include/ragb.h): argument checking, scratch
+// carving, stage timing, error mapping, handles and sessions.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <new>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "internal.h"
+#include "ragb.h"
+
+using ragb::HostIndex;
+using ragb::ScratchLayout;
+
+struct rb_index {
+  HostIndex H;
+};
+
+struct rb_session {
+  std::unordered_map<uint32_t, int32_t> seen;  // doc -> turn first prefilled
+  int32_t turn = 0;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+rb_status fail(rb_status code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+rb_status cuda_fail(cudaError_t e, const char *where) {
+  return fail(RB_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+constexpr size_t kAlign = 256;
+
+size_t take(size_t &o, size_t bytes) {
+  o = (o + kAlign - 1) / kAlign * kAlign;
+  const size_t at = o;
+  o += bytes;
+  return at;
+}
+
+rb_status check_params(int64_t N, int32_t K, const rb_params *p, int64_t *row0, int64_t *nrows) {
+  if (!p) return fail(RB_EINVAL, "params is NULL");
+  if (N < 1) return fail(RB_EINVAL, "N must be >= 1");
+  if (N > (int64_t)0x7ffffffe) return fail(RB_EINVAL, "N too large");
+  if (K < 1 || K > 255) return fail(RB_EINVAL, "K must be in [1, 255]");
+  if (p->alpha_den == 0 || p->alpha_den > 1000)
+    return fail(RB_EALPHA, "alpha_den must be in [1, 1000]");
+  if (p->alpha_num > p->alpha_den) return fail(RB_EALPHA, "alpha must be <= 1");
+  if (!(p->flags & RB_ALPHA_ANY)) {
+    // 1/1000 <= num/den <= 1/100
+    const uint64_t n = p->alpha_num, d = p->alpha_den;
+    if (n * 1000 < d || n * 100 > d) return fail(RB_EALPHA, "alpha outside [0.001, 0.01]");
+  }
+  if (p->linkage != RB_LINK_COMPLETE) return fail(RB_EINVAL, "unknown linkage");
+  *row0 = p->row0;
+  *nrows = p->nrows < 0 ? N - p->row0 : p->nrows;
+  if (*row0 < 0 || *nrows < 1 || *row0 + *nrows > N) return fail(RB_EINVAL, "bad row range");
+  return RB_OK;
+}
+
+}  // namespace
+
+namespace ragb {
+
+ScratchLayout ScratchLayout::make(int64_t N, int32_t K, bool keep_rows, bool linkage) {
+  ScratchLayout L{};
+  size_t o = 0;
+  L.err = take(o, 64);
+  L.counters = take(o, 64);
+  L.idsT = take(o, (size_t)K * padded_cols(N) * 4);
+  L.nnkey = take(o, (size_t)N * 8);
+  L.stage_ids = take(o, (size_t)N * K * 4);
+  L.stage_lens = take(o, (size_t)N);
+  L.lut = take(o, (size_t)std::max<int64_t>(eq1_lut_entries(K), 1) * 4);
+  if (linkage && N > 1) {
+    L.key0 = L.nnkey;
+    L.key1 = take(o, (size_t)N * 8);
+    L.rep0 = take(o, (size_t)N * 4);
+    L.rep1 = take(o, (size_t)N * 4);
+    L.sz0 = take(o, (size_t)N * 4);
+    L.sz1 = take(o, (size_t)N * 4);
+    L.leader = take(o, (size_t)N * 4);
+    L.aux0 = take(o, (size_t)N * 4);
+    L.aux1 = take(o, (size_t)(N + 1) * 4);
+    L.aux2 = take(o, (size_t)N * 4);
+    L.aux3 = take(o, (size_t)N * 4);
+    L.aux4 = take(o, (size_t)2 * N * 4);
+    L.alive = take(o, (size_t)N);
+    L.za = take(o, (size_t)N * 4);
+    L.zb = take(o, (size_t)N * 4);
+    L.zh = take(o, (size_t)N * 4);
+    L.zs = take(o, (size_t)N * 4);
+    const size_t mat = (size_t)(N - 1) * (size_t)(N - 1) * 4;
+    L.matA = take(o, mat);
+    L.matB = keep_rows ? take(o, mat) : 0;
+  }
+  L.total = (o + kAlign - 1) / kAlign * kAlign;
+  return L;
+}
+
+}  // namespace ragb
+
+extern "C" {
+
+const char *rb_version(void) { return "ragb 0.1.0 (sm_100a)"; }
+
+const char *rb_last_error(void) { return g_err.c_str(); }
+
+rb_status rb_params_init(rb_params *p) {
+  if (!p) return fail(RB_EINVAL, "params is NULL");
+  std::memset(p, 0, sizeof(*p));
+  p->alpha_num = 1;
+  p->alpha_den = 200;
+  p->linkage = RB_LINK_COMPLETE;
+  p->flags = 0;
+  p->stream = nullptr;
+  p->row0 = 0;
+  p->nrows = -1;
+  return RB_OK;
+}
+
+rb_status rb_workspace_size(int64_t N, int32_t K, const rb_params *p, size_t *rows_bytes,
+                            size_t *scratch_bytes) {
+  if (!rows_bytes || !scratch_bytes) return fail(RB_EINVAL, "NULL output");
+  int64_t row0, nrows;
+  rb_status s = check_params(N, K, p, &row0, &nrows);
+  if (s != RB_OK) return s;
+  const bool linkage = !(p->flags & RB_SKIP_LINKAGE) && nrows == N;
+  *rows_bytes = (size_t)nrows * (size_t)N * sizeof(float);
+  *scratch_bytes = ScratchLayout::make(N, K, (p->flags & RB_KEEP_ROWS) != 0, linkage).total;
+  return RB_OK;
+}
+
+static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, int64_t N, int32_t K,
+                              const rb_params *p, float *rows_dev, void *scratch_dev,
+                              size_t scratch_bytes, uint8_t *s_dev, uint16_t *D_dev,
+                              const uint32_t *ids_host, const uint8_t *lens_host, rb_index **out) {
+  using clock = std::chrono::steady_clock;
+  const auto t_start = clock::now();
+  if (!out) return fail(RB_EINVAL, "out is NULL");
+  int64_t row0, nrows;
+  rb_status s = check_params(N, K, p, &row0, &nrows);
+  if (s != RB_OK) return s;
+  if (!rows_dev || !scratch_dev) return fail(RB_EINVAL, "NULL device buffer");
+  if ((p->flags & RB_EMIT_COUNTS) && (!s_dev || !D_dev))
+    return fail(RB_EINVAL, "RB_EMIT_COUNTS needs s_dev and D_dev");
+  const bool linkage = !(p->flags & RB_SKIP_LINKAGE) && nrows == N;
+  const bool keep_rows = (p->flags & RB_KEEP_ROWS) != 0;
+  const ScratchLayout L = ScratchLayout::make(N, K, keep_rows, linkage);
+  if (scratch_bytes < L.total) return fail(RB_EINVAL, "scratch too small");
+  cudaStream_t st = static_cast<cudaStream_t>(p->stream);
+  unsigned char *sc = static_cast<unsigned char *>(scratch_dev);
+
+  rb_index *idx = new (std::nothrow) rb_index();
+  if (!idx) return fail(RB_ENOMEM, "host allocation failed");
+  HostIndex &H = idx->H;
+  H.N = N;
+  H.K = K;
+  int launches = 0;
+  cudaError_t e;
+  cudaEvent_t ev[4];
+  for (auto &x : ev) cudaEventCreate(&x);
+  auto cleanup = [&](rb_status code) {
+    for (auto &x : ev) cudaEventDestroy(x);
+    if (code != RB_OK) delete idx;
+    return code;
+  };
+#define RB_CUDA(call, where)                                              \
+  do {                                                                    \
+    if ((e = (call)) != cudaSuccess) return cleanup(cuda_fail(e, where)); \
+  } while (0)
+
+  // ---- inputs on the device (host entry: copy inside the call) -----------
+  const uint32_t *ids_d = ids_dev;
+  const uint8_t *lens_d = lens_dev;
+  if (ids_host) {  // end-to-end entry: stage the host inputs in scratch
+    uint32_t *sid = reinterpret_cast<uint32_t *>(sc + L.stage_ids);
+    RB_CUDA(cudaMemcpyAsync(sid, ids_host, (size_t)N * K * 4, cudaMemcpyHostToDevice, st),
+            "H2D ids");
+    ids_d = sid;
+    if (lens_host) {
+      uint8_t *sl = sc + L.stage_lens;
+      RB_CUDA(cudaMemcpyAsync(sl, lens_host, (size_t)N, cudaMemcpyHostToDevice, st), "H2D lens");
+      lens_d = sl;
+    }
+  }
+  if (!ids_d) return cleanup(fail(RB_EINVAL, "ids is NULL"));
+
+  // ---- a1: validate + transposed staging ----------------------------------
+  const int64_t Npad = ragb::padded_cols(N);
+  uint32_t *err_d = reinterpret_cast<uint32_t *>(sc + L.err);
+  uint32_t *idsT = reinterpret_cast<uint32_t *>(sc + L.idsT);
+  RB_CUDA(cudaEventRecord(ev[0], st), "event");
+  RB_CUDA(cudaMemsetAsync(err_d, 0, 4, st), "memset");
+  RB_CUDA(ragb::launch_validate(ids_d, lens_d, N, K, Npad, idsT, err_d, st, &launches), "validate");
+  uint32_t err_h = 0;
+  RB_CUDA(cudaMemcpyAsync(&err_h, err_d, 4, cudaMemcpyDeviceToHost, st), "D2H err");
+  // host copy of the contexts for the tree stage (overlaps the distance kernel)
+  H.ids.resize((size_t)N * K);
+  if (lens_d) H.lens.resize((size_t)N);
+  if (ids_host) {
+    std::memcpy(H.ids.data(), ids_host, (size_t)N * K * 4);
+    if (lens_host) std::memcpy(H.lens.data(), lens_host, (size_t)N);
+  }
+  RB_CUDA(cudaStreamSynchronize(st), "validate sync");
+  if (err_h & ragb::kErrLen) return cleanup(fail(RB_EINVAL, "context length not in [1, K]"));
+  if (err_h & ragb::kErrReserved) return cleanup(fail(RB_EINVAL, "reserved DocId 0xFFFFFFFF"));
+  if (err_h & ragb::kErrDup) return cleanup(fail(RB_EDUPDOC, "duplicate DocId within a context"));
+  if (!ids_host) {
+    // transposed copy holds the same ids; fetch the row-major input directly
+    RB_CUDA(cudaMemcpyAsync(H.ids.data(), ids_d, (size_t)N * K * 4, cudaMemcpyDeviceToHost, st),
+            "D2H ids");
+    if (lens_d)
+      RB_CUDA(cudaMemcpyAsync(H.lens.data(), lens_d, (size_t)N, cudaMemcpyDeviceToHost, st),
+              "D2H lens");
+  }
+  RB_CUDA(cudaEventRecord(ev[1], st), "event");
+
+  // ---- a2-a4: distance rows + fused row NN --------------------------------
+  ragb::DistArgs da{};
+  da.ids = ids_d;
+  da.lens = lens_d;
+  da.idsT = idsT;
+  da.N = N;
+  da.Npad = Npad;
+  da.row0 = row0;
+  da.nrows = nrows;
+  da.K = K;
+  da.an = p->alpha_num;
+  da.ad = p->alpha_den;
+  da.rows = rows_dev;
+  da.s_out = (p->flags & RB_EMIT_COUNTS) ? s_dev : nullptr;
+  da.D_out = (p->flags & RB_EMIT_COUNTS) ? D_dev : nullptr;
+  da.nnkey = reinterpret_cast<unsigned long long *>(sc + L.nnkey);
+  da.lut = nullptr;
+  if (!lens_d && ragb::eq1_lut_entries(K) > 0) {
+    float *lut = reinterpret_cast<float *>(sc + L.lut);
+    RB_CUDA(ragb::launch_eq1_lut(lut, K, p->alpha_num, p->alpha_den, st, &launches), "eq1 table");
+    da.lut = lut;
+  }
+  RB_CUDA(ragb::launch_distance(da, st, &launches), "distance kernel");
+  RB_CUDA(cudaEventRecord(ev[2], st), "event");
+  H.nn_idx.resize(nrows);
+  H.nn_d.resize(nrows);
+  std::vector<unsigned long long> keys(nrows);
+  RB_CUDA(cudaMemcpyAsync(keys.data(), da.nnkey + row0, nrows * 8, cudaMemcpyDeviceToHost, st),
+          "D2H nn");
+
+  // ---- a5: linkage ---------------------------------------------------------
+  ragb::LinkageOut lo;
+  if (linkage) {
+    RB_CUDA(ragb::run_linkage(rows_dev, N, da.nnkey, scratch_dev, L, keep_rows, st, &lo, &launches),
+            "linkage");
+  }
+  RB_CUDA(cudaEventRecord(ev[3], st), "event");
+  RB_CUDA(cudaStreamSynchronize(st), "sync");
+  for (int64_t r = 0; r < nrows; ++r) {
+    const unsigned long long k = keys[r];
+    if (k == ~0ull) {
+      H.nn_idx[r] = -1;
+      H.nn_d[r] = __builtin_inff();
+    } else {
+      H.nn_idx[r] = (int32_t)(k & 0xffffffffu);
+      uint32_t bits = (uint32_t)(k >> 32);
+      float f;
+      std::memcpy(&f, &bits, 4);
+      H.nn_d[r] = f;
+    }
+  }
+  float ms = 0;
+  cudaEventElapsedTime(&ms, ev[0], ev[1]);
+  H.stats.validate_ms = ms;
+  cudaEventElapsedTime(&ms, ev[1], ev[2]);
+  H.stats.distance_ms = ms;
+  cudaEventElapsedTime(&ms, ev[2], ev[3]);
+  H.stats.linkage_ms = ms;
+  H.stats.linkage_rounds = lo.rounds;
+  H.stats.kernel_launches = launches;
+
+  // ---- a6-a7: tree, orders, schedule (host) --------------------------------
+  if (linkage) {
+    const auto th = clock::now();
+    H.za.swap(lo.a);
+    H.zb.swap(lo.b);
+    H.zh.swap(lo.h);
+    H.zs.swap(lo.size);
+    std::string msg;
+    s = ragb::host_build(H, &msg);
+    if (s != RB_OK) return cleanup(fail(s, "internal: " + msg));
+    H.has_linkage = true;
+    H.stats.host_ms = std::chrono::duration<float, std::milli>(clock::now() - th).count();
+  }
+  H.stats.total_ms = std::chrono::duration<float, std::milli>(clock::now() - t_start).count();
+  *out = idx;
+  g_err.clear();
+  return cleanup(RB_OK);
+#undef RB_CUDA
+}
+
+rb_status rb_build_index(const uint32_t *ids_dev, const uint8_t *lens_dev, int64_t N, int32_t K,
+                         const rb_params *p, float *rows_dev, void *scratch_dev, size_t scratch_bytes,
+                         uint8_t *s_dev, uint16_t *D_dev, rb_index **out) {
+  if (!ids_dev) return fail(RB_EINVAL, "ids_dev is NULL");
+  return build_common(ids_dev, lens_dev, N, K, p, rows_dev, scratch_dev, scratch_bytes, s_dev, D_dev,
+                      nullptr, nullptr, out);
+}
+
+rb_status rb_build_index_host(const uint32_t *ids_host, const uint8_t *lens_host, int64_t N,
+                              int32_t K, const rb_params *p, float *rows_dev, void *scratch_dev,
+                              size_t scratch_bytes, rb_index **out) {
+  if (!ids_host) return fail(RB_EINVAL, "ids_host is NULL");
+  return build_common(nullptr, nullptr, N, K, p, rows_dev, scratch_dev, scratch_bytes, nullptr,
+                      nullptr, ids_host, lens_host, out);
+}
+
+rb_status rb_index_from_linkage(const uint32_t *ids_host, const uint8_t *lens_host, int64_t N,
+                                int32_t K, const int32_t *a, const int32_t *b, const float *h,
+                                const int32_t *size, rb_index **out) {
+  if (!ids_host || !out || (N > 1 && (!a || !b || !h || !size)))
+    return fail(RB_EINVAL, "NULL argument");
+  if (N < 1 || K < 1 || K > 255) return fail(RB_EINVAL, "bad N/K");
+  rb_index *idx = new (std::nothrow) rb_index();
+  if (!idx) return fail(RB_ENOMEM, "host allocation failed");
+  HostIndex &H = idx->H;
+  H.N = N;
+  H.K = K;
+  H.ids.assign(ids_host, ids_host + (size_t)N * K);
+  if (lens_host) H.lens.assign(lens_host, lens_host + N);
+  // validate contexts (same rules as the device a1)
+  for (int64_t i = 0; i < N; ++i) {
+    const int L = lens_host ? lens_host[i] : K;
+    if (L < 1 || L > K) {
+      delete idx;
+      return fail(RB_EINVAL, "context length not in [1, K]");
+    }
+    std::unordered_map<uint32_t, int> seen;
+    for (int k = 0; k < L; ++k) {
+      const uint32_t x = H.ids[(size_t)i * K + k];
+      if (x == ragb::kReservedDoc) {
+        delete idx;
+        return fail(RB_EINVAL, "reserved DocId 0xFFFFFFFF");
+      }
+      if (!seen.emplace(x, k).second) {
+        delete idx;
+        return fail(RB_EDUPDOC, "duplicate DocId within a context");
+      }
+    }
+  }
+  if (N > 1) {
+    H.za.assign(a, a + N - 1);
+    H.zb.assign(b, b + N - 1);
+    H.zh.assign(h, h + N - 1);
+    H.zs.assign(size, size + N - 1);
+  }
+  std::string msg;
+  rb_status s = ragb::host_build(H, &msg);
+  if (s != RB_OK) {
+    delete idx;
+    return fail(s, msg);
+  }
+  H.has_linkage = true;
+  *out = idx;
+  return RB_OK;
+}
+
+rb_status rb_index_size(const rb_index *idx, int64_t *N, int32_t *K) {
+  if (!idx) return fail(RB_EINVAL, "NULL index");
+  if (N) *N = idx->H.N;
+  if (K) *K = idx->H.K;
+  return RB_OK;
+}
+
+rb_status rb_index_stats(const rb_index *idx, rb_stats *st) {
+  if (!idx || !st) return fail(RB_EINVAL, "NULL argument");
+  *st = idx->H.stats;
+  return RB_OK;
+}
+
+rb_status rb_index_nn(const rb_index *idx, int32_t *nn_idx, float *nn_d) {
+  if (!idx) return fail(RB_EINVAL, "NULL index");
+  const HostIndex &H = idx->H;
+  if (H.nn_idx.empty()) return fail(RB_ESTATE, "no NN (index built from a linkage)");
+  if (nn_idx) std::memcpy(nn_idx, H.nn_idx.data(), H.nn_idx.size() * 4);
+  if (nn_d) std::memcpy(nn_d, H.nn_d.data(), H.nn_d.size() * 4);
+  return RB_OK;
+}
+
+rb_status rb_index_linkage(const rb_index *idx, int32_t *a, int32_t *b, float *h, int32_t *size) {
+  if (!idx) return fail(RB_EINVAL, "NULL index");
+  const HostIndex &H = idx->H;
+  if (!H.has_linkage) return fail(RB_ESTATE, "linkage was skipped");
+  const size_t n = H.za.size();
+  if (a) std::memcpy(a, H.za.data(), n * 4);
+  if (b) std::memcpy(b, H.zb.data(), n * 4);
+  if (h) std::memcpy(h, H.zh.data(), n * 4);
+  if (size) std::memcpy(size, H.zs.data(), n * 4);
+  return RB_OK;
+}
+
+rb_status rb_index_tree_info(const rb_index *idx, int64_t *n_nodes, int64_t *prefix_total,
+                             int64_t *path_total) {
+  if (!idx) return fail(RB_EINVAL, "NULL index");
+  const HostIndex &H = idx->H;
+  if (!H.has_linkage) return fail(RB_ESTATE, "linkage was skipped");
+  if (n_nodes) *n_nodes = (int64_t)H.parent.size();
+  if (prefix_total) *prefix_total = (int64_t)H.prefix_ids.size();
+  if (path_total) *path_total = (int64_t)H.path.size();
+  return RB_OK;
+}
+
+rb_status rb_index_tree(const rb_index *idx, int32_t *parent, int32_t *leaf, int32_t *rep,
+                        int64_t *prefix_off, uint32_t *prefix_ids, int64_t *path_off,
+                        int32_t *path) {
+  if (!idx) return fail(RB_EINVAL, "NULL index");
+  const HostIndex &H = idx->H;
+  if (!H.has_linkage) return fail(RB_ESTATE, "linkage was skipped");
+  const size_t n = H.parent.size();
+  if (parent) std::memcpy(parent, H.parent.data(), n * 4);
+  if (leaf) std::memcpy(leaf, H.leaf.data(), n * 4);
+  if (rep) std::memcpy(rep, H.rep.data(), n * 4);
+  if (prefix_off) std::memcpy(prefix_off, H.prefix_off.data(), (n + 1) * 8);
+  if (prefix_ids) std::memcpy(prefix_ids, H.prefix_ids.data(), H.prefix_ids.size() * 4);
+  if (path_off) std::memcpy(path_off, H.path_off.data(), H.path_off.size() * 8);
+  if (path) std::memcpy(path, H.path.data(), H.path.size() * 4);
+  return RB_OK;
+}
+
+rb_status rb_order_contexts(rb_index *idx, const uint32_t *ids, const uint8_t *lens, int64_t M,
+                            int32_t K, uint32_t *out_ids, uint8_t *out_prefix_len,
+                            int64_t *out_schedule) {
+  (void)lens;
+  if (!idx) return fail(RB_EINVAL, "NULL index");
+  const HostIndex &H = idx->H;
+  if (ids) return fail(RB_ESTATE, "online ordering of new contexts is not built yet");
+  if (!H.has_linkage) return fail(RB_ESTATE, "linkage was skipped");
+  if (M != H.N || K != H.K) return fail(RB_EINVAL, "M/K must match the index");
+  if (out_ids) std::memcpy(out_ids, H.ordered.data(), H.ordered.size() * 4);
+  if (out_prefix_len) std::memcpy(out_prefix_len, H.prefix_len.data(), H.prefix_len.size());
+  if (out_schedule) std::memcpy(out_schedule, H.schedule.data(), H.schedule.size() * 8);
+  return RB_OK;
+}
+
+static rb_status session_from_docs(const uint32_t *docs, int32_t n, rb_session **out) {
+  rb_session *s = new (std::nothrow) rb_session();
+  if (!s) return fail(RB_ENOMEM, "host allocation failed");
+  s->seen.reserve((size_t)n * 8 + 16);
+  for (int32_t k = 0; k < n; ++k) {
+    if (!s->seen.emplace(docs[k], 0).second) {
+      delete s;
+      return fail(RB_EDUPDOC, "duplicate DocId in turn-0 context");
+    }
+  }
+  *out = s;
+  return RB_OK;
+}
+
+rb_status rb_session_open(const rb_index *idx, int64_t row, rb_session **out) {
+  if (!idx || !out) return fail(RB_EINVAL, "NULL argument");
+  const HostIndex &H = idx->H;
+  if (!H.has_linkage) return fail(RB_ESTATE, "linkage was skipped");
+  if (row < 0 || row >= H.N) return fail(RB_EPATH, "row out of range");
+  // follow the stored search path from the root
+  int64_t node = 0;
+  for (int64_t z = H.path_off[row]; z < H.path_off[row + 1]; ++z) {
+    const int32_t step = H.path[z];
+    int64_t found = -1, seen = 0;
+    for (int64_t c = node + 1; c < (int64_t)H.parent.size() && found < 0; ++c)
+      if (H.parent[c] == node && seen++ == step) found = c;
+    if (found < 0) return fail(RB_EPATH, "stale search path");
+    node = found;
+  }
+  if (H.leaf[node] != row) return fail(RB_EPATH, "path does not reach the context");
+  const int64_t o0 = H.prefix_off[node], o1 = H.prefix_off[node + 1];
+  return session_from_docs(H.prefix_ids.data() + o0, (int32_t)(o1 - o0), out);
+}
+
+rb_status rb_session_open_docs(const uint32_t *docs, int32_t n, rb_session **out) {
+  if (!out || (n > 0 && !docs) || n < 0) return fail(RB_EINVAL, "bad argument");
+  return session_from_docs(docs, n, out);
+}
+
+rb_status rb_dedup_turn(rb_session *s, const uint32_t *ids, int32_t n, uint32_t *novel,
+                        int32_t *n_novel, uint32_t *ref_doc, int32_t *ref_turn, int32_t *n_ref) {
+  if (!s) return fail(RB_ESESSION, "NULL session");
+  if (n < 0 || (n > 0 && (!ids || !novel || !ref_doc || !ref_turn)) || !n_novel || !n_ref)
+    return fail(RB_EINVAL, "bad argument");
+  for (int32_t k = 0; k < n; ++k)  // duplicate check before any state change
+    for (int32_t q = 0; q < k; ++q)
+      if (ids[q] == ids[k]) return fail(RB_EDUPDOC, "duplicate DocId in retrieval");
+  const int32_t turn = s->turn + 1;
+  int32_t nn = 0, nr = 0;
+  for (int32_t k = 0; k < n; ++k) {
+    auto it = s->seen.find(ids[k]);
+    if (it == s->seen.end()) {
+      novel[nn++] = ids[k];
+    } else {
+      ref_doc[nr] = ids[k];
+      ref_turn[nr] = it->second;
+      ++nr;
+    }
+  }
+  for (int32_t k = 0; k < nn; ++k) s->seen.emplace(novel[k], turn);
+  s->turn = turn;
+  *n_novel = nn;
+  *n_ref = nr;
+  return RB_OK;
+}
+
+rb_status rb_session_turn(const rb_session *s, int32_t *turn) {
+  if (!s) return fail(RB_ESESSION, "NULL session");
+  if (!turn) return fail(RB_EINVAL, "NULL output");
+  *turn = s->turn;
+  return RB_OK;
+}
+
+void rb_session_free(rb_session *s) { delete s; }
+void rb_index_free(rb_index *idx) { delete idx; }
+
+}  // extern "C"

@@ -1,0 +1,102 @@
+// Internal interfaces of libragb (not part of the C-ABI; see include/ragb.h).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "ragb.h"
+
+namespace ragb {
+
+constexpr uint32_t kReservedDoc = 0xFFFFFFFFu;  // never a DocId; also the empty-slot key
+
+// Error bits raised by the validation kernel (a1).
+enum : uint32_t { kErrLen = 1u, kErrDup = 2u, kErrReserved = 4u };
+
+// Column chunk of the distance kernel: 256 threads x 4 columns.
+constexpr int kDistThreads = 256;
+constexpr int kColsPerThread = 4;
+constexpr int kChunk = kDistThreads * kColsPerThread;
+
+inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+inline int64_t padded_cols(int64_t N) { return round_up(N, kChunk); }
+
+// ----------------------------------------------------------------- scratch
+// Byte layout of the caller-owned scratch buffer (all offsets 256-aligned).
+struct ScratchLayout {
+  size_t err, idsT, nnkey, stage_ids, stage_lens, lut, key0, key1, rep0, rep1, sz0, sz1, leader, aux0, aux1, aux2, aux3, aux4,
+      alive, za, zb, zh, zs, counters, matA, matB, total;
+  static ScratchLayout make(int64_t N, int32_t K, bool keep_rows, bool linkage);
+};
+
+// ----------------------------------------------------------------- kernels
+struct DistArgs {
+  const uint32_t *ids;   // [N][K] row-major
+  const uint8_t *lens;   // [N] or nullptr
+  const uint32_t *idsT;  // [K][Npad] transposed, padded with kReservedDoc
+  int64_t N, Npad, row0, nrows;
+  int32_t K;
+  uint32_t an, ad;
+  float *rows;                // [nrows][N]
+  uint8_t *s_out;             // [nrows][N] or nullptr
+  uint16_t *D_out;            // [nrows][N] or nullptr
+  unsigned long long *nnkey;  // [N] indexed by global row: (f32 bits << 32) | column
+  const float *lut;           // Eq. 1 table d(s, D) for uniform length K, or nullptr
+};
+
+// Eq. 1 table: (K+1) x (floor(K^2/2)+1) floats for K <= kLutMaxK.
+constexpr int kLutMaxK = 128;
+constexpr int64_t kLutSmemBytes = 20 * 1024;
+int64_t eq1_lut_entries(int32_t K);
+cudaError_t launch_eq1_lut(float *lut, int32_t K, uint32_t an, uint32_t ad, cudaStream_t st,
+                           int *launches);
+
+cudaError_t launch_validate(const uint32_t *ids, const uint8_t *lens, int64_t N, int32_t K,
+                            int64_t Npad, uint32_t *idsT, uint32_t *err, cudaStream_t st,
+                            int *launches);
+cudaError_t launch_distance(const DistArgs &a, cudaStream_t st, int *launches);
+
+struct LinkageOut {
+  std::vector<int32_t> a, b, size;
+  std::vector<float> h;
+  int rounds = 0;
+};
+
+// a5: complete linkage on the full rows (rows ld = N) starting from the fused
+// row-NN keys; merges returned unsorted.
+cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void *scratch,
+                        const ScratchLayout &L, bool keep_rows, cudaStream_t st, LinkageOut *out,
+                        int *launches);
+
+// ----------------------------------------------------------------- host
+struct HostIndex {
+  int64_t N = 0;
+  int32_t K = 0;
+  std::vector<uint32_t> ids;  // [N][K]
+  std::vector<uint8_t> lens;  // [N]
+  bool has_linkage = false;
+  std::vector<int32_t> nn_idx;
+  std::vector<float> nn_d;
+  std::vector<int32_t> za, zb, zs;
+  std::vector<float> zh;
+  // tree (node 0 = root)
+  std::vector<int32_t> parent, leaf, rep, leaf_node;
+  std::vector<int64_t> prefix_off, path_off;  // prefix_off per node; path_off per leaf (context)
+  std::vector<uint32_t> prefix_ids;
+  std::vector<int32_t> path;
+  // offline orders
+  std::vector<uint32_t> ordered;   // [N][K]
+  std::vector<uint8_t> prefix_len;  // [N]
+  std::vector<int64_t> schedule;    // [N]
+  rb_stats stats{};
+};
+
+// Sort merges into greedy key order (X9) and validate them; builds tree,
+// orders and schedule (a6-a7).  Returns RB_OK or RB_EINVAL with msg.
+rb_status host_build(HostIndex &H, std::string *msg);
+
+}  // namespace ragb

@@ -1,0 +1,406 @@
+// a5 on sm_100a: complete-linkage agglomerative clustering of the Eq. 1 rows.
+//
+// PAPER:335 (Section 4.1 "Index creation"): "we iteratively merge the closest
+// pair, creating a virtual node".  Readings: complete linkage
+// D(A u B, C) = max(D(A,C), D(B,C)) (X7), tie key (D, min rep, max rep) with
+// rep = smallest leaf index (X8), merge order = ascending key (X9).
+//
+// Algorithm: level-synchronous rounds over a compacted active matrix.  A round
+// starts from every active row's nearest-neighbour key (the fused row min of
+// the previous pass, or of the distance kernel in round 0) and merges, in one
+// batch, (1) every merge the greedy algorithm performs at the current minimum
+// height h, and (2) every reciprocal-nearest-neighbour pair above h:
+//   (1) at height h the greedy process is a sequence of clique contractions on
+//       the graph of pairs at distance exactly h: take the smallest vertex a with
+//       an h-neighbour, absorb its smallest h-neighbour b, keep the candidates
+//       adjacent to every absorbed vertex (max stays h only if both are h), and
+//       continue; then the next vertex.  This is done by one CTA (k_round_prep).
+//   (2) RNN pairs above h are merges of the unique reducible hierarchy and are
+//       disjoint from (1) (a vertex with an h-neighbour has its NN at h).
+// Then one fused pass (k_merge_compact) writes the merged, order-preserving
+// compacted matrix (max over group members) and the new row-min keys.  Because
+// compaction preserves order and a group's survivor is its smallest member,
+// compacted index order == rep order, so the row key (d bits << 32 | column)
+// orders candidates exactly like the X8 tie key.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "internal.h"
+
+namespace ragb {
+namespace {
+
+typedef unsigned long long u64;
+constexpr int PT = 1024;  // threads of the single-CTA round-prep kernel
+constexpr int MT = 256;   // threads of the merge/compact kernel
+
+struct PrepArgs {
+  const float *D;
+  int64_t ld;
+  int M;
+  const u64 *key;
+  const int *rep;
+  const int *sz;
+  int *leader;
+  uint8_t *alive;
+  int *list, *candA, *candB;  // alias goff/gmem/colsrc (written later)
+  int *za, *zb, *zs;
+  float *zh;
+  int *zcount;
+  int *newidx, *goff, *gmem, *colsrc, *cnt, *cursor;
+  int *rep_n, *sz_n;
+  int *Mn;
+};
+
+struct BlockScratch {
+  int w[32];
+  int total;
+  unsigned h;
+};
+
+// Exclusive scan of v over the 1024 threads; returns the prefix, sets *total.
+__device__ __forceinline__ int block_scan1024(int v, BlockScratch &S, int *total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) S.w[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int t = S.w[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    S.w[lane] = t;
+  }
+  __syncthreads();
+  const int before = (w == 0) ? 0 : S.w[w - 1];
+  *total = S.w[31];
+  __syncthreads();
+  return before + x - v;
+}
+
+// Order-preserving compaction: out[...] = value(i) for i in [0, n) with pred(i).
+template <typename Pred, typename Val>
+__device__ int block_compact(int n, Pred pred, Val value, int *out, BlockScratch &S) {
+  int base = 0;
+  for (int c0 = 0; c0 < n; c0 += PT) {
+    const int i = c0 + (int)threadIdx.x;
+    const bool p = i < n && pred(i);
+    int tot;
+    const int pre = block_scan1024(p ? 1 : 0, S, &tot);
+    if (p) out[base + pre] = value(i);
+    base += tot;
+  }
+  __syncthreads();
+  return base;
+}
+
+__global__ void __launch_bounds__(PT, 1) k_round_prep(PrepArgs a) {
+  __shared__ BlockScratch S;
+  const int tid = threadIdx.x;
+  const int M = a.M;
+
+  // -- 1. current minimum height h ------------------------------------------
+  unsigned hl = 0xffffffffu;
+  for (int x = tid; x < M; x += PT) hl = min(hl, (unsigned)(a.key[x] >> 32));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) hl = min(hl, __shfl_xor_sync(0xffffffffu, hl, o));
+  if (tid == 0) S.h = 0xffffffffu;
+  __syncthreads();
+  if ((tid & 31) == 0) atomicMin(&S.h, hl);
+  __syncthreads();
+  const unsigned h = S.h;
+  const float hf = __uint_as_float(h);
+
+  // -- 2. RNN pairs above h; vertices at h become clique candidates ------------
+  for (int x = tid; x < M; x += PT) {
+    const u64 kx = a.key[x];
+    const unsigned hx = (unsigned)(kx >> 32);
+    const int y = (int)(kx & 0xffffffffu);
+    int lead = x;
+    a.alive[x] = (hx == h) ? 1 : 0;
+    if (hx > h && (int)(a.key[y] & 0xffffffffu) == x) {
+      if (y < x) {
+        lead = y;
+      } else {
+        const int pos = atomicAdd(a.zcount, 1);
+        a.za[pos] = a.rep[x];
+        a.zb[pos] = a.rep[y];
+        a.zh[pos] = __uint_as_float(hx);
+        a.zs[pos] = a.sz[x] + a.sz[y];
+      }
+    }
+    a.leader[x] = lead;
+  }
+  __syncthreads();
+
+  // -- 3. greedy clique contractions at height h (ascending vertex order) -----
+  const uint8_t *alive = a.alive;
+  const int nlist = block_compact(
+      M, [&](int i) { return alive[i] != 0; }, [&](int i) { return i; }, a.list, S);
+  int sza = 0;
+  for (int li = 0; li < nlist; ++li) {
+    const int v = a.list[li];
+    if (!a.alive[v]) continue;  // absorbed by an earlier vertex (uniform branch)
+    // h-neighbours of v: only list vertices (row min == h) can be at h from v,
+    // and the list is ascending, so scanning its suffix keeps candidates sorted.
+    const float *rowv = a.D + (int64_t)v * a.ld;
+    const int *lst = a.list + li + 1;
+    int n = block_compact(
+        nlist - li - 1,
+        [&](int i) {
+          const int c = lst[i];
+          return a.alive[c] != 0 && rowv[c] == hf;
+        },
+        [&](int i) { return lst[i]; }, a.candA, S);
+    int *cin = a.candA, *cout = a.candB;
+    if (tid == 0) sza = a.sz[v];
+    while (n > 0) {
+      const int b = cin[0];
+      if (tid == 0) {
+        sza += a.sz[b];
+        const int pos = atomicAdd(a.zcount, 1);
+        a.za[pos] = a.rep[v];
+        a.zb[pos] = a.rep[b];
+        a.zh[pos] = hf;
+        a.zs[pos] = sza;
+        a.leader[b] = v;
+        a.alive[b] = 0;
+      }
+      const float *rowb = a.D + (int64_t)b * a.ld;
+      const int *cc = cin;
+      n = block_compact(
+          n - 1, [&](int i) { return rowb[cc[1 + i]] == hf; }, [&](int i) { return cc[1 + i]; },
+          cout, S);
+      int *t = cin;
+      cin = cout;
+      cout = t;
+    }
+    if (tid == 0) a.alive[v] = 0;
+    __syncthreads();
+  }
+
+  // -- 4. compaction map: new index of every survivor (order preserving) ------
+  int base = 0;
+  for (int c0 = 0; c0 < M; c0 += PT) {
+    const int x = c0 + tid;
+    const int f = (x < M && a.leader[x] == x) ? 1 : 0;
+    int tot;
+    const int pre = block_scan1024(f, S, &tot);
+    if (x < M) a.newidx[x] = base + pre;  // valid for survivors
+    base += tot;
+  }
+  const int Mn = base;
+  for (int g = tid; g < Mn; g += PT) {
+    a.cnt[g] = 0;
+    a.cursor[g] = 0;
+    a.sz_n[g] = 0;
+  }
+  __syncthreads();
+  for (int x = tid; x < M; x += PT) {
+    const int l = a.leader[x];
+    const int g = a.newidx[l];
+    atomicAdd(&a.cnt[g], 1);
+    atomicAdd(&a.sz_n[g], a.sz[x]);
+    if (l == x) a.rep_n[g] = a.rep[x];
+  }
+  __syncthreads();
+  base = 0;
+  for (int c0 = 0; c0 < Mn; c0 += PT) {
+    const int g = c0 + tid;
+    const int v = g < Mn ? a.cnt[g] : 0;
+    int tot;
+    const int pre = block_scan1024(v, S, &tot);
+    if (g < Mn) a.goff[g] = base + pre;
+    base += tot;
+  }
+  if (tid == 0) {
+    a.goff[Mn] = M;
+    *a.Mn = Mn;
+  }
+  __syncthreads();
+  for (int x = tid; x < M; x += PT) {
+    const int g = a.newidx[a.leader[x]];
+    a.gmem[a.goff[g] + atomicAdd(&a.cursor[g], 1)] = x;
+  }
+  __syncthreads();
+  for (int g = tid; g < Mn; g += PT)
+    a.colsrc[g] = (a.cnt[g] == 1) ? a.gmem[a.goff[g]] : -(a.goff[g] + 1);
+}
+
+// Fused merge + compaction + row min: Dn[c][j] = max over members r of group
+// c and s of group j of D[r][s]; keyn[c] = min_{j != c} (Dn[c][j] bits, j).
+__global__ void __launch_bounds__(MT) k_merge_compact(const float *__restrict__ D, int64_t ld,
+                                                      const int *__restrict__ Mn_p,
+                                                      const int *__restrict__ goff,
+                                                      const int *__restrict__ gmem,
+                                                      const int *__restrict__ colsrc,
+                                                      float *__restrict__ Dn, u64 *__restrict__ keyn) {
+  __shared__ u64 wmin[MT / 32];
+  const int Mn = *Mn_p;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  for (int c = blockIdx.x; c < Mn; c += gridDim.x) {
+    const int rb = goff[c], re = goff[c + 1];
+    const float *r0 = D + (int64_t)gmem[rb] * ld;
+    float *out = Dn + (int64_t)c * Mn;
+    u64 best = ~0ull;
+    for (int j = tid; j < Mn; j += MT) {
+      const int src = colsrc[j];
+      float v;
+      if (src >= 0) {
+        v = r0[src];
+        for (int rr = rb + 1; rr < re; ++rr) v = fmaxf(v, D[(int64_t)gmem[rr] * ld + src]);
+      } else {
+        const int sb = -src - 1, se = goff[j + 1];
+        v = 0.0f;
+        for (int rr = rb; rr < re; ++rr) {
+          const float *row = D + (int64_t)gmem[rr] * ld;
+          for (int ss = sb; ss < se; ++ss) v = fmaxf(v, row[gmem[ss]]);
+        }
+      }
+      if (j == c) {
+        v = 0.0f;
+      } else {
+        const u64 k = ((u64)__float_as_uint(v) << 32) | (unsigned)j;
+        best = k < best ? k : best;
+      }
+      out[j] = v;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const u64 y = __shfl_xor_sync(0xffffffffu, best, o);
+      best = y < best ? y : best;
+    }
+    if (lane == 0) wmin[w] = best;
+    __syncthreads();
+    if (tid == 0) {
+      u64 b = wmin[0];
+#pragma unroll
+      for (int i = 1; i < MT / 32; ++i) b = wmin[i] < b ? wmin[i] : b;
+      keyn[c] = b;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_init_state(int *rep, int *sz, int64_t N) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < N) {
+    rep[i] = (int)i;
+    sz[i] = 1;
+  }
+}
+
+template <typename T>
+T *at(void *base, size_t off) {
+  return reinterpret_cast<T *>(static_cast<unsigned char *>(base) + off);
+}
+
+}  // namespace
+
+cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void *scratch,
+                        const ScratchLayout &L, bool keep_rows, cudaStream_t st, LinkageOut *out,
+                        int *launches) {
+  out->a.clear();
+  out->b.clear();
+  out->h.clear();
+  out->size.clear();
+  out->rounds = 0;
+  if (N <= 1) return cudaSuccess;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+
+  u64 *key[2] = {nnkey, at<u64>(scratch, L.key1)};
+  int *rep[2] = {at<int>(scratch, L.rep0), at<int>(scratch, L.rep1)};
+  int *sz[2] = {at<int>(scratch, L.sz0), at<int>(scratch, L.sz1)};
+  float *matA = at<float>(scratch, L.matA);
+  float *matB = keep_rows ? at<float>(scratch, L.matB) : rows;
+  int *counters = at<int>(scratch, L.counters);  // [0] zcount, [1] Mn
+  cudaError_t e;
+  k_init_state<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(rep[0], sz[0], N);
+  ++*launches;
+  if ((e = cudaMemsetAsync(counters, 0, 2 * sizeof(int), st)) != cudaSuccess) return e;
+
+  PrepArgs pa{};
+  pa.leader = at<int>(scratch, L.leader);
+  pa.alive = at<uint8_t>(scratch, L.alive);
+  pa.newidx = at<int>(scratch, L.aux0);
+  pa.goff = at<int>(scratch, L.aux1);
+  pa.gmem = at<int>(scratch, L.aux2);
+  pa.colsrc = at<int>(scratch, L.aux3);
+  pa.cnt = at<int>(scratch, L.aux4);
+  pa.cursor = pa.cnt + N;
+  pa.list = pa.goff;
+  pa.candA = pa.gmem;
+  pa.candB = pa.colsrc;
+  pa.za = at<int>(scratch, L.za);
+  pa.zb = at<int>(scratch, L.zb);
+  pa.zs = at<int>(scratch, L.zs);
+  pa.zh = at<float>(scratch, L.zh);
+  pa.zcount = counters;
+  pa.Mn = counters + 1;
+
+  const float *cur = rows;
+  int64_t ld = N;
+  int M = (int)N;
+  int p = 0;
+  float *next = matA;
+  while (M > 1) {
+    pa.D = cur;
+    pa.ld = ld;
+    pa.M = M;
+    pa.key = key[p];
+    pa.rep = rep[p];
+    pa.sz = sz[p];
+    pa.rep_n = rep[p ^ 1];
+    pa.sz_n = sz[p ^ 1];
+    k_round_prep<<<1, PT, 0, st>>>(pa);
+    ++*launches;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    int host_c[2];
+    if ((e = cudaMemcpyAsync(host_c, counters, sizeof(host_c), cudaMemcpyDeviceToHost, st)) !=
+        cudaSuccess)
+      return e;
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+    ++out->rounds;
+    const int Mn = host_c[1];
+    if (Mn >= M || Mn < 1) return cudaErrorUnknown;  // no progress: invariant violated
+    if (Mn > 1) {
+      const int grid = std::min<int>(Mn, sms * 8);
+      k_merge_compact<<<grid, MT, 0, st>>>(cur, ld, pa.Mn, pa.goff, pa.gmem, pa.colsrc, next,
+                                           key[p ^ 1]);
+      ++*launches;
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+      cur = next;
+      next = (next == matA) ? matB : matA;
+      ld = Mn;
+    }
+    p ^= 1;
+    M = Mn;
+  }
+  int nz = 0;
+  if ((e = cudaMemcpyAsync(&nz, counters, sizeof(int), cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+    return e;
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+  if (nz != N - 1) return cudaErrorUnknown;
+  out->a.resize(nz);
+  out->b.resize(nz);
+  out->h.resize(nz);
+  out->size.resize(nz);
+  cudaMemcpyAsync(out->a.data(), pa.za, nz * sizeof(int), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(out->b.data(), pa.zb, nz * sizeof(int), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(out->h.data(), pa.zh, nz * sizeof(float), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(out->size.data(), pa.zs, nz * sizeof(int), cudaMemcpyDeviceToHost, st);
+  return cudaStreamSynchronize(st);
+}
+
+}  // namespace ragb

@@ -1,0 +1,320 @@
+"""Thin Python binding of libragb's C-ABI (include/ragb.h).
+
+Argument marshalling only: every step of the index build runs inside the
+library (CUDA kernels for a1-a5, C++ for a6-a8).  PyTorch supplies device
+memory and streams.  There is no fallback: if libragb.so is missing or has no
+GPU to run on, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from fractions import Fraction
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", f"libragb_{os.environ['RAGB_LIB']}.so" if os.environ.get("RAGB_LIB")
+                        else "libragb.so")
+
+RB_OK, RB_EINVAL, RB_EDUPDOC, RB_EALPHA, RB_ENOMEM, RB_ECUDA, RB_ENCCL, RB_EPATH, RB_ESESSION, \
+    RB_ESTATE = 0, -1, -2, -3, -4, -5, -6, -7, -8, -9
+RB_EMIT_COUNTS, RB_ALPHA_ANY, RB_KEEP_ROWS, RB_SKIP_LINKAGE = 1, 2, 4, 8
+
+STATUS_NAMES = {0: "RB_OK", -1: "RB_EINVAL", -2: "RB_EDUPDOC", -3: "RB_EALPHA", -4: "RB_ENOMEM",
+                -5: "RB_ECUDA", -6: "RB_ENCCL", -7: "RB_EPATH", -8: "RB_ESESSION", -9: "RB_ESTATE"}
+
+EXPORTED = [
+    "rb_version", "rb_last_error", "rb_params_init", "rb_workspace_size", "rb_build_index",
+    "rb_build_index_host", "rb_index_from_linkage", "rb_index_size", "rb_index_stats", "rb_index_nn",
+    "rb_index_linkage", "rb_index_tree_info", "rb_index_tree", "rb_order_contexts", "rb_session_open",
+    "rb_session_open_docs", "rb_dedup_turn", "rb_session_turn", "rb_session_free", "rb_index_free",
+]
+
+
+class RagbError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+class Params(ctypes.Structure):
+    _fields_ = [("alpha_num", ctypes.c_uint32), ("alpha_den", ctypes.c_uint32),
+                ("linkage", ctypes.c_int32), ("flags", ctypes.c_uint32),
+                ("stream", ctypes.c_void_p), ("row0", ctypes.c_int64), ("nrows", ctypes.c_int64)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("validate_ms", ctypes.c_float), ("distance_ms", ctypes.c_float),
+                ("linkage_ms", ctypes.c_float), ("host_ms", ctypes.c_float),
+                ("total_ms", ctypes.c_float), ("linkage_rounds", ctypes.c_int32),
+                ("kernel_launches", ctypes.c_int32), ("n_virtual", ctypes.c_int64),
+                ("max_depth", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+
+
+def lib():
+    """Load libragb.so (built by paper_2511_03475_b200.build / __graft_entry__.build)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"libragb.so not built ({LIB_PATH}); run __graft_entry__.build()")
+    L = ctypes.CDLL(LIB_PATH)
+    P, i64, i32, u32, sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32, ctypes.c_size_t
+    PP = ctypes.POINTER(ctypes.c_void_p)
+    sig = {
+        "rb_version": ([], ctypes.c_char_p),
+        "rb_last_error": ([], ctypes.c_char_p),
+        "rb_params_init": ([ctypes.POINTER(Params)], i32),
+        "rb_workspace_size": ([i64, i32, ctypes.POINTER(Params), ctypes.POINTER(sz), ctypes.POINTER(sz)], i32),
+        "rb_build_index": ([P, P, i64, i32, ctypes.POINTER(Params), P, P, sz, P, P, PP], i32),
+        "rb_build_index_host": ([P, P, i64, i32, ctypes.POINTER(Params), P, P, sz, PP], i32),
+        "rb_index_from_linkage": ([P, P, i64, i32, P, P, P, P, PP], i32),
+        "rb_index_size": ([P, ctypes.POINTER(i64), ctypes.POINTER(i32)], i32),
+        "rb_index_stats": ([P, ctypes.POINTER(Stats)], i32),
+        "rb_index_nn": ([P, P, P], i32),
+        "rb_index_linkage": ([P, P, P, P, P], i32),
+        "rb_index_tree_info": ([P, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)], i32),
+        "rb_index_tree": ([P, P, P, P, P, P, P, P], i32),
+        "rb_order_contexts": ([P, P, P, i64, i32, P, P, P], i32),
+        "rb_session_open": ([P, i64, PP], i32),
+        "rb_session_open_docs": ([P, i32, PP], i32),
+        "rb_dedup_turn": ([P, P, i32, P, ctypes.POINTER(i32), P, P, ctypes.POINTER(i32)], i32),
+        "rb_session_turn": ([P, ctypes.POINTER(i32)], i32),
+        "rb_session_free": ([P], None),
+        "rb_index_free": ([P], None),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = L
+    return L
+
+
+def _check(rc: int):
+    if rc != RB_OK:
+        raise RagbError(rc, lib().rb_last_error().decode())
+
+
+def _np_ptr(a):
+    return None if a is None else ctypes.c_void_p(a.ctypes.data)
+
+
+def version() -> str:
+    return lib().rb_version().decode()
+
+
+def alpha_rational(alpha) -> tuple[int, int]:
+    """X1: alpha as an exact rational with denominator <= 1000."""
+    if isinstance(alpha, tuple):
+        return int(alpha[0]), int(alpha[1])
+    f = Fraction(alpha).limit_denominator(1000)
+    return f.numerator, f.denominator
+
+
+def make_params(alpha=(1, 200), flags=0, stream=None, row0=0, nrows=-1) -> Params:
+    p = Params()
+    _check(lib().rb_params_init(ctypes.byref(p)))
+    p.alpha_num, p.alpha_den = alpha_rational(alpha)
+    p.flags = flags
+    p.stream = stream
+    p.row0 = row0
+    p.nrows = nrows
+    return p
+
+
+def workspace_size(N: int, K: int, params: Params) -> tuple[int, int]:
+    rb, sb = ctypes.c_size_t(), ctypes.c_size_t()
+    _check(lib().rb_workspace_size(N, K, ctypes.byref(params), ctypes.byref(rb), ctypes.byref(sb)))
+    return rb.value, sb.value
+
+
+class Index:
+    """Owns an rb_index handle (host results of one build)."""
+
+    def __init__(self, handle: ctypes.c_void_p):
+        self._h = handle
+        n, k = ctypes.c_int64(), ctypes.c_int32()
+        _check(lib().rb_index_size(self._h, ctypes.byref(n), ctypes.byref(k)))
+        self.N, self.K = n.value, k.value
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.rb_index_free(h)
+            self._h = None
+
+    def stats(self) -> dict:
+        s = Stats()
+        _check(lib().rb_index_stats(self._h, ctypes.byref(s)))
+        return s.as_dict()
+
+    def nn(self, nrows=None):
+        n = self.N if nrows is None else nrows
+        idx = np.empty(n, dtype=np.int32)
+        val = np.empty(n, dtype=np.float32)
+        _check(lib().rb_index_nn(self._h, _np_ptr(idx), _np_ptr(val)))
+        return idx, val
+
+    def linkage(self):
+        n = max(self.N - 1, 0)
+        a, b, s = (np.empty(n, dtype=np.int32) for _ in range(3))
+        h = np.empty(n, dtype=np.float32)
+        _check(lib().rb_index_linkage(self._h, _np_ptr(a), _np_ptr(b), _np_ptr(h), _np_ptr(s)))
+        return a, b, h, s
+
+    def tree(self) -> dict:
+        nn_, pt, qt = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().rb_index_tree_info(self._h, ctypes.byref(nn_), ctypes.byref(pt), ctypes.byref(qt)))
+        n = nn_.value
+        parent, leaf, rep = (np.empty(n, dtype=np.int32) for _ in range(3))
+        poff = np.empty(n + 1, dtype=np.int64)
+        pids = np.empty(pt.value, dtype=np.uint32)
+        qoff = np.empty(self.N + 1, dtype=np.int64)
+        path = np.empty(qt.value, dtype=np.int32)
+        _check(lib().rb_index_tree(self._h, _np_ptr(parent), _np_ptr(leaf), _np_ptr(rep), _np_ptr(poff),
+                                   _np_ptr(pids), _np_ptr(qoff), _np_ptr(path)))
+        return dict(parent=parent, leaf=leaf, rep=rep, prefix_off=poff, prefix_ids=pids,
+                    path_off=qoff, path=path)
+
+    def paths(self):
+        t = self.tree()
+        o, p = t["path_off"], t["path"]
+        return [p[o[i]:o[i + 1]].tolist() for i in range(self.N)]
+
+    def order_contexts(self):
+        """Offline prefix-first ordering + schedule of the indexed set."""
+        out = np.empty((self.N, self.K), dtype=np.uint32)
+        plen = np.empty(self.N, dtype=np.uint8)
+        sched = np.empty(self.N, dtype=np.int64)
+        _check(lib().rb_order_contexts(self._h, None, None, self.N, self.K, _np_ptr(out), _np_ptr(plen),
+                                       _np_ptr(sched)))
+        return out, plen, sched
+
+    def session(self, row: int) -> "Session":
+        h = ctypes.c_void_p()
+        _check(lib().rb_session_open(self._h, row, ctypes.byref(h)))
+        return Session(h, keepalive=self)
+
+
+class Session:
+    """Multi-turn de-duplication state."""
+
+    def __init__(self, handle, keepalive=None):
+        self._h = handle
+        self._keep = keepalive
+
+    @classmethod
+    def from_docs(cls, docs) -> "Session":
+        d = np.ascontiguousarray(docs, dtype=np.uint32)
+        h = ctypes.c_void_p()
+        _check(lib().rb_session_open_docs(_np_ptr(d), d.shape[0], ctypes.byref(h)))
+        return cls(h)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.rb_session_free(h)
+            self._h = None
+
+    @property
+    def turn(self) -> int:
+        t = ctypes.c_int32()
+        _check(lib().rb_session_turn(self._h, ctypes.byref(t)))
+        return t.value
+
+    def dedup_turn(self, docs):
+        d = np.ascontiguousarray(docs, dtype=np.uint32)
+        n = d.shape[0]
+        novel = np.empty(max(n, 1), dtype=np.uint32)
+        rdoc = np.empty(max(n, 1), dtype=np.uint32)
+        rturn = np.empty(max(n, 1), dtype=np.int32)
+        nn_, nr = ctypes.c_int32(), ctypes.c_int32()
+        _check(lib().rb_dedup_turn(self._h, _np_ptr(d), n, _np_ptr(novel), ctypes.byref(nn_), _np_ptr(rdoc),
+                                   _np_ptr(rturn), ctypes.byref(nr)))
+        return novel[:nn_.value].copy(), rdoc[:nr.value].copy(), rturn[:nr.value].copy()
+
+
+def index_from_linkage(ids, a, b, h, size, lens=None) -> Index:
+    ids = np.ascontiguousarray(ids, dtype=np.uint32)
+    N, K = ids.shape
+    arrs = [np.ascontiguousarray(x, dtype=t) for x, t in
+            ((a, np.int32), (b, np.int32), (h, np.float32), (size, np.int32))]
+    lens_a = None if lens is None else np.ascontiguousarray(lens, dtype=np.uint8)
+    out = ctypes.c_void_p()
+    _check(lib().rb_index_from_linkage(_np_ptr(ids), _np_ptr(lens_a), N, K, *[_np_ptr(x) for x in arrs],
+                                       ctypes.byref(out)))
+    return Index(out)
+
+
+# ---------------------------------------------------------------- device path
+class Workspace:
+    """Caller-owned device buffers (torch allocations) for one (N, K, flags)."""
+
+    def __init__(self, N, K, params: Params, device="cuda"):
+        import torch
+        self.N, self.K = N, K
+        rb, sb = workspace_size(N, K, params)
+        nrows = rb // (4 * N)
+        self.rows = torch.empty((nrows, N), dtype=torch.float32, device=device)
+        self.scratch = torch.empty(max(sb, 1), dtype=torch.uint8, device=device)
+        self.s = self.D = None
+        if params.flags & RB_EMIT_COUNTS:
+            self.s = torch.empty((nrows, N), dtype=torch.uint8, device=device)
+            self.D = torch.empty((nrows, N), dtype=torch.int16, device=device)
+
+
+def _stream_ptr(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def build_index(ids, lens=None, *, alpha=(1, 200), flags=0, row0=0, nrows=-1, stream=None,
+                workspace: Workspace | None = None):
+    """Build the context index from device ids (torch.int32/uint32 CUDA tensor [N, K]).
+
+    Returns (Index, Workspace); workspace.rows holds the distance rows (unless
+    the linkage consumed them: pass flags |= RB_KEEP_ROWS to keep them)."""
+    import torch
+    if not ids.is_cuda:
+        raise ValueError("build_index expects a CUDA tensor; use build_index_host for host arrays")
+    if ids.dtype not in (torch.int32, torch.uint32):
+        raise TypeError("ids must be int32/uint32 (bit pattern of uint32 DocIds)")
+    ids = ids.contiguous()
+    N, K = ids.shape
+    p = make_params(alpha, flags, _stream_ptr(stream), row0, nrows)
+    ws = workspace or Workspace(N, K, p, device=ids.device)
+    if lens is not None:
+        lens = lens.contiguous()
+        assert lens.dtype == torch.uint8 and lens.is_cuda
+    out = ctypes.c_void_p()
+    _check(lib().rb_build_index(
+        ctypes.c_void_p(ids.data_ptr()), None if lens is None else ctypes.c_void_p(lens.data_ptr()), N, K,
+        ctypes.byref(p), ctypes.c_void_p(ws.rows.data_ptr()), ctypes.c_void_p(ws.scratch.data_ptr()),
+        ws.scratch.numel(), None if ws.s is None else ctypes.c_void_p(ws.s.data_ptr()),
+        None if ws.D is None else ctypes.c_void_p(ws.D.data_ptr()), ctypes.byref(out)))
+    return Index(out), ws
+
+
+def build_index_host(ids, lens=None, *, alpha=(1, 200), flags=0, stream=None,
+                     workspace: Workspace | None = None):
+    """End-to-end entry: ids/lens are host numpy arrays; H2D happens inside."""
+    ids = np.ascontiguousarray(ids, dtype=np.uint32)
+    N, K = ids.shape
+    p = make_params(alpha, flags, _stream_ptr(stream))
+    ws = workspace or Workspace(N, K, p)
+    lens_a = None if lens is None else np.ascontiguousarray(lens, dtype=np.uint8)
+    out = ctypes.c_void_p()
+    _check(lib().rb_build_index_host(_np_ptr(ids), _np_ptr(lens_a), N, K, ctypes.byref(p),
+                                     ctypes.c_void_p(ws.rows.data_ptr()), ctypes.c_void_p(ws.scratch.data_ptr()),
+                                     ws.scratch.numel(), ctypes.byref(out)))
+    return Index(out), ws

@@ -1,0 +1,250 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the CPU oracle, element by
+element on the same seeded inputs.  Bar (BASELINE.json north_star): bit-exact
+s/D counts, fp32 distances (correctly rounded, X6 — stronger than the 1e-6
+relative bound), nearest neighbours, merge order, tree, document ordering and
+schedule."""
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from oracle import oracle_c as oc
+from oracle import ragb_oracle as o
+from synth.workload import config, edge, generate
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2511_03475_b200 import ragb  # noqa: E402
+
+F = ragb
+
+
+def dev_build(ids, lens=None, flags=F.RB_KEEP_ROWS, alpha=(1, 200), **kw):
+    t = torch.from_numpy(np.ascontiguousarray(ids).view(np.int32)).cuda()
+    tl = None if lens is None else torch.from_numpy(np.ascontiguousarray(lens, dtype=np.uint8)).cuda()
+    idx, ws = F.build_index(t, tl, alpha=alpha, flags=flags, **kw)
+    torch.cuda.synchronize()
+    return idx, ws
+
+
+def oracle_linkage_tree(ids, lens, d_full):
+    Z = oc.linkage(d_full)
+    ctxs = o.validate(ids, lens)
+    t = o.build_tree(ctxs, list(zip(*Z)))
+    ordered, plen = o.offline_order(ctxs, t)
+    return Z, t, ordered, plen, o.schedule(t.path)
+
+
+def check_full(ids, lens=None, alpha=(1, 200), counts=True):
+    N, K = ids.shape
+    flags = F.RB_KEEP_ROWS | (F.RB_EMIT_COUNTS if counts else 0)
+    idx, ws = dev_build(ids, lens, flags=flags, alpha=alpha)
+    rows = ws.rows.cpu().numpy()
+    dref, sref, Dref = oc.pairwise_rows(ids, lens, alpha[0], alpha[1], counts=True)
+    if counts:
+        assert np.array_equal(ws.s.cpu().numpy(), sref)
+        assert np.array_equal(ws.D.cpu().numpy().view(np.uint16), Dref)
+    assert np.array_equal(rows.view(np.uint32), dref.view(np.uint32))
+    nn_i, nn_v = idx.nn()
+    ri, rv = oc.row_nn(dref)
+    assert np.array_equal(nn_i, ri) and np.array_equal(nn_v.view(np.uint32), rv.view(np.uint32))
+    Z, t, ordered, plen, sched = oracle_linkage_tree(ids, lens, dref)
+    a, b, h, s = idx.linkage()
+    assert np.array_equal(a, Z[0]) and np.array_equal(b, Z[1])
+    assert np.array_equal(h.view(np.uint32), Z[2].view(np.uint32)) and np.array_equal(s, Z[3])
+    assert idx.paths() == t.path
+    out, pl, sc = idx.order_contexts()
+    for i in range(N):
+        L = K if lens is None else int(lens[i])
+        assert out[i, :L].tolist() == ordered[i]
+    assert pl.tolist() == plen and sc.tolist() == sched
+    return idx
+
+
+def test_paper_fig4(golden):
+    ids = np.array(golden["fig4_build"]["contexts"], dtype=np.uint32)
+    idx = check_full(ids)
+    assert idx.paths() == golden["fig4_build"]["derived"]["paths"]
+    idx2, ws = dev_build(np.array(list(golden["eq1_motivation"]["contexts"].values()), dtype=np.uint32))
+    d = ws.rows.cpu().numpy()
+    assert hex(int(d[0, 1:2].view(np.uint32)[0])) == golden["eq1_motivation"]["derived"]["AB"]["f32_hex"]
+
+
+def test_C1_full():
+    w = config("C1")
+    check_full(w.ids)
+    # the python (definition-level) oracle agrees too
+    ref = o.build_index(w.ids)
+    idx, ws = dev_build(w.ids)
+    assert np.array_equal(ws.rows.cpu().numpy().view(np.uint32), ref["d"].view(np.uint32))
+    a, b, h, s = idx.linkage()
+    assert [(int(x), int(y), np.float32(z), int(q)) for x, y, z, q in zip(a, b, h, s)] == \
+        [(x, y, np.float32(z), q) for x, y, z, q in ref["Z"]]
+
+
+def test_C2_full():
+    w = config("C2")
+    check_full(w.ids, counts=False)
+
+
+@pytest.mark.parametrize("N", [1, 2, 3, 31, 77, 1000, 1029, 2053])
+def test_ragged_sizes(N):
+    w = generate(N, 8, max(40, 3 * N), 100 + N)
+    check_full(w.ids)
+
+
+@pytest.mark.parametrize("K", [1, 5, 10, 15, 20, 32, 33, 50, 75, 100, 128, 200, 255])
+def test_K_sweep(K):
+    w = generate(700 if K <= 100 else 300, K, max(4 * K, 3000), 5)
+    check_full(w.ids, counts=K <= 100)
+
+
+@pytest.mark.parametrize("alpha", [(1, 1000), (1, 100), (3, 700), (7, 997)])
+def test_alpha(alpha):
+    w = generate(600, 12, 2000, 9)
+    check_full(w.ids, alpha=alpha, counts=False)
+
+
+def test_variable_lengths():
+    w = generate(900, 16, 3000, 21, len_min=2)
+    check_full(w.ids, w.lens)
+
+
+@pytest.mark.parametrize("kind", ["disjoint", "identical", "permutations"])
+def test_edges(kind):
+    check_full(edge(kind, 300, 7).ids)
+
+
+def test_errors():
+    ids = np.array([[1, 2, 3], [4, 5, 4]], dtype=np.uint32)
+    with pytest.raises(F.RagbError) as e:
+        dev_build(ids)
+    assert e.value.code == F.RB_EDUPDOC
+    with pytest.raises(F.RagbError) as e:
+        dev_build(np.array([[1, 0xFFFFFFFF]], dtype=np.uint32))
+    assert e.value.code == F.RB_EINVAL
+    with pytest.raises(F.RagbError) as e:
+        dev_build(np.array([[1, 2]], dtype=np.uint32), lens=np.array([3], dtype=np.uint8))
+    assert e.value.code == F.RB_EINVAL
+    # duplicates beyond lens are ignored
+    dev_build(np.array([[1, 2, 2], [3, 4, 5]], dtype=np.uint32), lens=np.array([2, 3], dtype=np.uint8))
+
+
+def test_row_shard_and_skip_linkage():
+    w = generate(1500, 20, 8000, 31)
+    dref = oc.pairwise_rows(w.ids, None, 1, 200)
+    for row0, nrows in [(0, 700), (700, 800), (13, 1)]:
+        idx, ws = dev_build(w.ids, flags=0, row0=row0, nrows=nrows)
+        assert np.array_equal(ws.rows.cpu().numpy().view(np.uint32),
+                              dref[row0:row0 + nrows].view(np.uint32))
+        ni, nv = idx.nn(nrows)
+        ri, rv = oc.row_nn(dref[row0:row0 + nrows], row0=row0)
+        assert np.array_equal(ni, ri) and np.array_equal(nv, rv)
+        with pytest.raises(F.RagbError):
+            idx.linkage()
+
+
+def test_host_entry_matches_device_entry():
+    w = generate(1200, 20, 6000, 8)
+    idx1, _ = dev_build(w.ids, flags=0)
+    idx2, _ = F.build_index_host(w.ids)
+    for x, y in zip(idx1.linkage(), idx2.linkage()):
+        assert np.array_equal(x, y)
+    assert np.array_equal(idx1.order_contexts()[0], idx2.order_contexts()[0])
+
+
+def test_consumed_rows_linkage_equals_kept():
+    w = generate(3000, 20, 1_000_000 // 30, 4)
+    i1, _ = dev_build(w.ids, flags=0)
+    i2, _ = dev_build(w.ids, flags=F.RB_KEEP_ROWS)
+    for x, y in zip(i1.linkage(), i2.linkage()):
+        assert np.array_equal(x, y)
+
+
+def test_deterministic_repeat():
+    w = generate(2000, 20, 20000, 77)
+    runs = [dev_build(w.ids, flags=0)[0] for _ in range(3)]
+    for r in runs[1:]:
+        for x, y in zip(r.linkage(), runs[0].linkage()):
+            assert np.array_equal(x, y)
+        assert np.array_equal(r.order_contexts()[2], runs[0].order_contexts()[2])
+
+
+# ------------------------------------------------------------- full sizes
+def linkage_properties(a, b, h, s, N):
+    """Properties of a complete-linkage merge order that hold at any size."""
+    assert len(a) == N - 1
+    assert np.all(a < b)
+    h0, h1, a0, a1, b0, b1 = h[:-1], h[1:], a[:-1], a[1:], b[:-1], b[1:]
+    inc = (h1 > h0) | ((h1 == h0) & ((a1 > a0) | ((a1 == a0) & (b1 > b0))))
+    assert np.all(inc)   # strictly increasing key (X9)
+    rep_alive = np.ones(N, dtype=bool)
+    size = np.ones(N, dtype=np.int64)
+    for x, y, z in zip(a.tolist(), b.tolist(), s.tolist()):
+        assert rep_alive[x] and rep_alive[y]
+        size[x] += size[y]
+        rep_alive[y] = False
+        assert size[x] == z
+    assert rep_alive.sum() == 1 and size[0] == N
+
+
+def sampled_rows_check(ids, rows_dev, sample, lens=None, alpha=(1, 200)):
+    for r in sample:
+        ref = oc.pairwise_rows(ids, lens, alpha[0], alpha[1], row0=int(r), nrows=1)
+        got = rows_dev[int(r)].cpu().numpy()
+        assert np.array_equal(got.view(np.uint32), ref[0].view(np.uint32)), f"row {r}"
+
+
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_full_size_configs(name):
+    """BASELINE.json configs at full size, bench launch configuration: sampled
+    rows vs the oracle one by one, nn of sampled rows, linkage/tree/order
+    properties, sampled merges against the complete-linkage definition."""
+    w = config(name)
+    N, K = w.ids.shape
+    rng = np.random.default_rng(0)
+    sample = np.unique(np.concatenate([[0, N - 1], rng.integers(0, N, 30)]))
+    idx, ws = dev_build(w.ids, flags=F.RB_SKIP_LINKAGE)
+    sampled_rows_check(w.ids, ws.rows, sample)
+    ni, nv = idx.nn()
+    for r in sample:
+        ref = oc.pairwise_rows(w.ids, None, 1, 200, row0=int(r), nrows=1)
+        ri, rv = oc.row_nn(ref, row0=int(r))
+        assert ni[r] == ri[0] and nv[r] == rv[0]
+    del ws
+    torch.cuda.empty_cache()
+    idx, ws = dev_build(w.ids, flags=0)   # bench configuration: rows consumed by the linkage
+    a, b, h, s = idx.linkage()
+    linkage_properties(a, b, h, s, N)
+    # first merge = global min pair of the nn array (greedy's first step)
+    i0 = int(np.lexsort((np.arange(N), nv))[0])
+    assert (a[0], b[0]) == tuple(sorted((i0, int(ni[i0]))))
+    # sampled small merges: height == max over member pairs (definition, X7)
+    members = {i: [i] for i in range(N)}   # member lists of small clusters only
+    checked = 0
+    for x, y, z in zip(a.tolist(), b.tolist(), h.tolist()):
+        A, B = members.get(x), members.pop(y, None)
+        if A is not None and B is not None and checked < 40 and len(A) * len(B) <= 64 \
+                and rng.random() < 0.02:
+            dsub = oc.pairwise_rows(w.ids[A + B], None, 1, 200)
+            assert np.float32(dsub[:len(A), len(A):].max()) == np.float32(z)
+            checked += 1
+        if A is not None and B is not None and len(A) + len(B) <= 16:
+            members[x] = A + B
+        else:
+            members.pop(x, None)
+    assert checked > 0
+    out, pl, sc = idx.order_contexts()
+    assert np.array_equal(np.sort(out, axis=1), np.sort(w.ids, axis=1))  # permutations
+    assert np.array_equal(np.sort(sc), np.arange(N))
+    paths = idx.paths()
+    firsts = np.array([paths[i][0] for i in sc])
+    change = np.flatnonzero(firsts[1:] != firsts[:-1])
+    assert len(change) + 1 == len(np.unique(firsts))   # contiguous groups
+    # tree/order: host step re-run from the device merge order == library result
+    idx2 = F.index_from_linkage(w.ids, a, b, h, s)
+    assert np.array_equal(idx2.order_contexts()[0], out)
