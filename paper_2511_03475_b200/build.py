@@ -20,8 +20,8 @@ NVCC_FLAGS = [
     "-std=c++17", "-O3", "-lineinfo",
     "-gencode", "arch=compute_100a,code=sm_100a",
     "--fmad=false",                      # parity: no contraction anywhere (X6)
-    "-Xcompiler", "-fPIC,-O3,-fvisibility=hidden",
-    "-shared",
+    "-Xcompiler", "-fPIC,-O3,-fvisibility=hidden,-fopenmp",
+    "-shared", "-lgomp",
 ]
 
 

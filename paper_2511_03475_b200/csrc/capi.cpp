@@ -80,7 +80,12 @@ ScratchLayout ScratchLayout::make(int64_t N, int32_t K, bool keep_rows, bool lin
   L.nnkey = take(o, (size_t)N * 8);
   L.stage_ids = take(o, (size_t)N * K * 4);
   L.stage_lens = take(o, (size_t)N);
-  L.lut = take(o, (size_t)std::max<int64_t>(eq1_lut_entries(K), 1) * 4);
+  {
+    int stride;
+    int64_t entries;
+    distance_lut_layout(K, true, &stride, &entries);
+    L.lut = take(o, (size_t)std::max<int64_t>(entries, 1) * 4);
+  }
   if (linkage && N > 1) {
     L.key0 = L.nnkey;
     L.key1 = take(o, (size_t)N * 8);
@@ -92,14 +97,15 @@ ScratchLayout ScratchLayout::make(int64_t N, int32_t K, bool keep_rows, bool lin
     L.aux0 = take(o, (size_t)N * 4);
     L.aux1 = take(o, (size_t)(N + 1) * 4);
     L.aux2 = take(o, (size_t)N * 4);
-    L.aux3 = take(o, (size_t)N * 4);
+    L.aux3 = take(o, (size_t)(N + 4) * 4);
     L.aux4 = take(o, (size_t)2 * N * 4);
     L.alive = take(o, (size_t)N);
     L.za = take(o, (size_t)N * 4);
     L.zb = take(o, (size_t)N * 4);
     L.zh = take(o, (size_t)N * 4);
     L.zs = take(o, (size_t)N * 4);
-    const size_t mat = (size_t)(N - 1) * (size_t)(N - 1) * 4;
+    // compacted matrices: at most (N-1) rows with a leading dimension padded to 4
+    const size_t mat = (size_t)(N - 1) * (size_t)((N + 2) & ~3ll) * 4;
     L.matA = take(o, mat);
     L.matB = keep_rows ? take(o, mat) : 0;
   }
@@ -242,10 +248,17 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
   da.D_out = (p->flags & RB_EMIT_COUNTS) ? D_dev : nullptr;
   da.nnkey = reinterpret_cast<unsigned long long *>(sc + L.nnkey);
   da.lut = nullptr;
-  if (!lens_d && ragb::eq1_lut_entries(K) > 0) {
-    float *lut = reinterpret_cast<float *>(sc + L.lut);
-    RB_CUDA(ragb::launch_eq1_lut(lut, K, p->alpha_num, p->alpha_den, st, &launches), "eq1 table");
-    da.lut = lut;
+  {
+    int stride;
+    int64_t entries;
+    ragb::distance_lut_layout(K, lens_d == nullptr, &stride, &entries);
+    if (entries > 0) {
+      float *lut = reinterpret_cast<float *>(sc + L.lut);
+      RB_CUDA(ragb::launch_eq1_lut(lut, K, stride, entries, p->alpha_num, p->alpha_den, st,
+                                   &launches),
+              "eq1 table");
+      da.lut = lut;
+    }
   }
   RB_CUDA(ragb::launch_distance(da, st, &launches), "distance kernel");
   RB_CUDA(cudaEventRecord(ev[2], st), "event");
@@ -406,13 +419,19 @@ rb_status rb_index_linkage(const rb_index *idx, int32_t *a, int32_t *b, float *h
   return RB_OK;
 }
 
+static int64_t node_count(const HostIndex &H) { return 1 + H.V + H.N; }
+
 rb_status rb_index_tree_info(const rb_index *idx, int64_t *n_nodes, int64_t *prefix_total,
                              int64_t *path_total) {
   if (!idx) return fail(RB_EINVAL, "NULL index");
   const HostIndex &H = idx->H;
   if (!H.has_linkage) return fail(RB_ESTATE, "linkage was skipped");
-  if (n_nodes) *n_nodes = (int64_t)H.parent.size();
-  if (prefix_total) *prefix_total = (int64_t)H.prefix_ids.size();
+  if (n_nodes) *n_nodes = node_count(H);
+  if (prefix_total) {
+    int64_t t = H.vpre_off[H.V + 1];
+    for (int64_t i = 0; i < H.N; ++i) t += H.lens.empty() ? H.K : H.lens[i];
+    *prefix_total = t;
+  }
   if (path_total) *path_total = (int64_t)H.path.size();
   return RB_OK;
 }
@@ -423,12 +442,37 @@ rb_status rb_index_tree(const rb_index *idx, int32_t *parent, int32_t *leaf, int
   if (!idx) return fail(RB_EINVAL, "NULL index");
   const HostIndex &H = idx->H;
   if (!H.has_linkage) return fail(RB_ESTATE, "linkage was skipped");
-  const size_t n = H.parent.size();
-  if (parent) std::memcpy(parent, H.parent.data(), n * 4);
-  if (leaf) std::memcpy(leaf, H.leaf.data(), n * 4);
-  if (rep) std::memcpy(rep, H.rep.data(), n * 4);
-  if (prefix_off) std::memcpy(prefix_off, H.prefix_off.data(), (n + 1) * 8);
-  if (prefix_ids) std::memcpy(prefix_ids, H.prefix_ids.data(), H.prefix_ids.size() * 4);
+  const int64_t V = H.V, N = H.N, K = H.K;
+  if (parent) {
+    parent[0] = -1;
+    for (int64_t k = 1; k <= V; ++k) parent[k] = H.vparent[k - 1];
+    for (int64_t i = 0; i < N; ++i) parent[V + 1 + i] = H.lparent[i];
+  }
+  if (leaf) {
+    for (int64_t k = 0; k <= V; ++k) leaf[k] = -1;
+    for (int64_t i = 0; i < N; ++i) leaf[V + 1 + i] = (int32_t)i;
+  }
+  if (rep) {
+    rep[0] = -1;
+    for (int64_t k = 1; k <= V; ++k) rep[k] = H.vrep[k - 1];
+    for (int64_t i = 0; i < N; ++i) rep[V + 1 + i] = (int32_t)i;
+  }
+  if (prefix_off || prefix_ids) {
+    int64_t o = 0;
+    for (int64_t k = 0; k <= V; ++k) {
+      const int64_t a = H.vpre_off[k], b = H.vpre_off[k + 1];
+      if (prefix_off) prefix_off[k] = o;
+      if (prefix_ids) std::memcpy(prefix_ids + o, H.vpre.data() + a, 4 * (size_t)(b - a));
+      o += b - a;
+    }
+    for (int64_t i = 0; i < N; ++i) {
+      const int64_t L = H.lens.empty() ? K : H.lens[i];
+      if (prefix_off) prefix_off[V + 1 + i] = o;
+      if (prefix_ids) std::memcpy(prefix_ids + o, H.ordered.data() + i * K, 4 * (size_t)L);
+      o += L;
+    }
+    if (prefix_off) prefix_off[V + 1 + N] = o;
+  }
   if (path_off) std::memcpy(path_off, H.path_off.data(), H.path_off.size() * 8);
   if (path) std::memcpy(path, H.path.data(), H.path.size() * 4);
   return RB_OK;
@@ -472,15 +516,14 @@ rb_status rb_session_open(const rb_index *idx, int64_t row, rb_session **out) {
   int64_t node = 0;
   for (int64_t z = H.path_off[row]; z < H.path_off[row + 1]; ++z) {
     const int32_t step = H.path[z];
-    int64_t found = -1, seen = 0;
-    for (int64_t c = node + 1; c < (int64_t)H.parent.size() && found < 0; ++c)
-      if (H.parent[c] == node && seen++ == step) found = c;
-    if (found < 0) return fail(RB_EPATH, "stale search path");
-    node = found;
+    if (node > H.V) return fail(RB_EPATH, "stale search path");
+    const int64_t c0 = H.kids_off[node], c1 = H.kids_off[node + 1];
+    if (step < 0 || step >= c1 - c0) return fail(RB_EPATH, "stale search path");
+    node = H.kids[c0 + step];
   }
-  if (H.leaf[node] != row) return fail(RB_EPATH, "path does not reach the context");
-  const int64_t o0 = H.prefix_off[node], o1 = H.prefix_off[node + 1];
-  return session_from_docs(H.prefix_ids.data() + o0, (int32_t)(o1 - o0), out);
+  if (node != H.V + 1 + row) return fail(RB_EPATH, "path does not reach the context");
+  const int32_t L = H.lens.empty() ? H.K : H.lens[row];
+  return session_from_docs(H.ordered.data() + row * H.K, L, out);
 }
 
 rb_status rb_session_open_docs(const uint32_t *docs, int32_t n, rb_session **out) {

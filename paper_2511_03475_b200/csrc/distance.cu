@@ -25,6 +25,7 @@
 #include <cstdint>
 #include <cstdlib>
 
+#include "device_util.cuh"
 #include "internal.h"
 
 #ifdef RAGB_DEBUG
@@ -50,10 +51,6 @@ namespace {
 constexpr int NT = kDistThreads;
 constexpr int CPT = kColsPerThread;
 constexpr int NW = NT / 32;
-
-__device__ __forceinline__ uint32_t hash_slot(uint32_t x, int logT) {
-  return (x * 0x9E3779B1u) >> (32 - logT);
-}
 
 // Correctly rounded fp32 of num/den (X6).  num, den < 2^24: both exact in
 // fp32 and IEEE division is correctly rounded.  Otherwise den < 2^29 holds for
@@ -105,41 +102,10 @@ __device__ __forceinline__ void unpack4(const uint4 &v, uint32_t p[4]) {
   p[3] = v.w;
 }
 
-__device__ __forceinline__ unsigned long long umin64(unsigned long long a, unsigned long long b) {
-  return a < b ? a : b;
-}
-
 __device__ __forceinline__ unsigned long long warp_min64(unsigned long long v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = umin64(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
-}
-
-// Block-wide exclusive scan of one value per thread (NT threads).
-__device__ __forceinline__ int block_excl_scan(int v, int *wsum) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) wsum[w] = x;
-  __syncwarp();
-  __syncthreads();
-  if (w == 0) {
-    int t = lane < NW ? wsum[lane] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, t, o);
-      if (lane >= o) t += y;
-    }
-    if (lane < NW) wsum[lane] = t;  // inclusive warp prefix
-  }
-  __syncwarp();
-  __syncthreads();
-  const int before = (w == 0) ? 0 : wsum[w - 1];
-  return before + x - v;
 }
 
 struct SmemPlan {
@@ -215,7 +181,7 @@ __global__ void __launch_bounds__(NT) k_dist_rows_nn(DistArgs a, SmemPlan P) {
       const int per = T / NT;
       int cnt = 0;
       for (int i = 0; i < per; ++i) cnt += __popc(tmask[tid * per + i]);
-      int base = block_excl_scan(cnt, wsum);
+      int base = block_excl_scan<NT>(cnt, wsum);
       for (int i = 0; i < per; ++i) {
         tbase[tid * per + i] = (uint16_t)base;
         base += __popc(tmask[tid * per + i]);
@@ -450,29 +416,40 @@ cudaError_t launch_validate(const uint32_t *ids, const uint8_t *lens, int64_t N,
   return cudaGetLastError();
 }
 
-int64_t eq1_lut_entries(int32_t K) {
-  return K <= kLutMaxK ? (int64_t)(K + 1) * (K * K / 2 + 1) : 0;
+void distance_lut_layout(int32_t K, bool uniform, int *stride, int64_t *entries) {
+  *stride = 0;
+  *entries = 0;
+  if (!uniform) return;
+  if (tile_path_ok(K, true)) {
+    *stride = 1 << tile_lut_shift(K);
+    *entries = tile_lut_entries(K);
+  } else if (K <= kLutMaxK) {
+    *stride = K * K / 2 + 1;
+    *entries = (int64_t)(K + 1) * *stride;
+  }
 }
 
-cudaError_t launch_eq1_lut(float *lut, int32_t K, uint32_t an, uint32_t ad, cudaStream_t st,
-                           int *launches) {
-  const int64_t n = eq1_lut_entries(K);
-  if (n == 0) return cudaSuccess;
-  k_eq1_lut<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(lut, K, K * K / 2 + 1, an, ad);
+cudaError_t launch_eq1_lut(float *lut, int32_t K, int stride, int64_t entries, uint32_t an,
+                           uint32_t ad, cudaStream_t st, int *launches) {
+  if (entries == 0) return cudaSuccess;
+  k_eq1_lut<<<(unsigned)((entries + 255) / 256), 256, 0, st>>>(lut, K, stride, an, ad);
   ++*launches;
   return cudaGetLastError();
 }
 
 cudaError_t launch_distance(const DistArgs &a, cudaStream_t st, int *launches) {
   ++*launches;
-  // Finalize: a table of d(s, D) when every context has K docs (smem copy if
-  // it is small, else read through L1/L2), else the exact division.
-  const int64_t lutn = a.lut ? eq1_lut_entries(a.K) : 0;
+  if (tile_path_ok(a.K, a.lens == nullptr) && a.lut) return launch_distance_tile(a, st);
+  // General path (variable lengths, K > 32): a table of d(s, D) when every
+  // context has K docs (smem copy if small, else read through L1/L2), else the
+  // exact division.
+  int stride = 0;
+  int64_t lutn = 0;
+  distance_lut_layout(a.K, a.lens == nullptr, &stride, &lutn);
+  if (!a.lut) lutn = 0;
   int fin = kFinDiv;
   if (a.lens == nullptr && lutn > 0) fin = (lutn * 4 <= kLutSmemBytes) ? kFinLutSmem : kFinLutGlobal;
   const int smemLut = fin == kFinLutSmem ? (int)lutn : 0;
-  // K <= 32: R = 32 rows per tile, 16-bit packed (s, D) accumulators (~105 KB
-  // smem at K = 20 with the table -> 2 CTAs/SM).  Larger K: R = 16, 32-bit.
   if (a.K <= 32) return dispatch<32, uint16_t>(a, plan_smem(32, a.K, 2, smemLut), st, fin);
   return dispatch<16, uint32_t>(a, plan_smem(16, a.K, 4, smemLut), st, fin);
 }

@@ -1,0 +1,331 @@
+// a2-a4 fast path on sm_100a: every context has exactly K <= 32 docs (the
+// paper's setting: a retriever returns top-K lists).  Same math as
+// distance.cu (Eq. 1; X2, X3, X6), restructured so that warps stay
+// converged:
+//
+//  * A CTA (256 threads) owns R = 32 rows; it streams all N columns in chunks
+//    of 512 (2 per thread).  The tile's docs sit in a shared-memory hash table
+//    (doc -> row mask, positions) plus a 2^16-bit filter.
+//  * Probe phase, per k: each thread tests its 2 column docs against the
+//    filter (one LDS, branch-free).  Candidates (~20 %) are appended to a
+//    per-warp queue with ballots.
+//  * Hit phase: the warp drains its queue with all 32 lanes: table lookup, then
+//    one shared-memory atomicAdd of (1 << SHIFT) + |p_i - p_j| per (row, column)
+//    incidence into packed 16-bit (s, D) accumulators.
+//  * Finalize: the packed accumulator IS the index of a d(s, D) table (stride
+//    1 << SHIFT), so d costs one LDS; 8-byte streaming row stores; the row
+//    min/argmin runs in registers (32 rows unrolled) and is reduced once per
+//    tile, not per chunk.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+
+#include "device_util.cuh"
+#include "internal.h"
+
+namespace ragb {
+namespace {
+
+constexpr int NT = 256;        // threads per CTA
+constexpr int NW = NT / 32;    // warps per CTA
+constexpr int CPT = 2;         // columns per thread per chunk
+constexpr int CH = NT * CPT;   // columns per chunk
+constexpr int R = 32;          // rows per tile
+constexpr int QCAP = 384;      // queue entries per warp
+constexpr int FWORDS = 2048;   // filter words (65536 bits)
+
+struct Plan {
+  int T, logT, shift, lutEntries;
+  size_t off_acc, off_key, off_mask, off_base, off_slot, off_plist, off_filter, off_qdoc, off_qmeta,
+      off_red, off_wsum, off_lut, total;
+};
+
+template <int SHIFT, bool LUT_SMEM, bool COUNTS>
+__global__ void __launch_bounds__(NT, 2) k_dist_tile(DistArgs a, Plan P) {
+  constexpr uint32_t DMASK = (1u << SHIFT) - 1u;
+  constexpr uint32_t INC = 1u << SHIFT;
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint32_t *accw = reinterpret_cast<uint32_t *>(smem + P.off_acc);    // [R][NT] packed 2 x u16
+  uint32_t *tkey = reinterpret_cast<uint32_t *>(smem + P.off_key);    // [T]
+  uint32_t *tmask = reinterpret_cast<uint32_t *>(smem + P.off_mask);  // [T]
+  uint16_t *tbase = reinterpret_cast<uint16_t *>(smem + P.off_base);  // [T]
+  uint16_t *slot = reinterpret_cast<uint16_t *>(smem + P.off_slot);   // [R*K]
+  uint8_t *plist = smem + P.off_plist;                                // [R*K]
+  uint32_t *filt = reinterpret_cast<uint32_t *>(smem + P.off_filter); // [FWORDS]
+  uint32_t *qdoc = reinterpret_cast<uint32_t *>(smem + P.off_qdoc);   // [NW][QCAP]
+  uint32_t *qmeta = reinterpret_cast<uint32_t *>(smem + P.off_qmeta); // [NW][QCAP]
+  unsigned long long *red = reinterpret_cast<unsigned long long *>(smem + P.off_red);  // [NW][R]
+  int *wsum = reinterpret_cast<int *>(smem + P.off_wsum);
+  float *slut = reinterpret_cast<float *>(smem + P.off_lut);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int K = a.K, T = P.T, logT = P.logT;
+  const int64_t N = a.N, Npad = a.Npad;
+  const int64_t ntiles = (a.nrows + R - 1) / R;
+  const float *lut = LUT_SMEM ? slut : a.lut;
+  if (LUT_SMEM)
+    for (int i = tid; i < P.lutEntries; i += NT) slut[i] = a.lut[i];
+  uint32_t *myq_doc = qdoc + warp * QCAP;
+  uint32_t *myq_meta = qmeta + warp * QCAP;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const bool even_n = (N & 1) == 0;
+
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t r0 = a.row0 + tile * R;
+    const int64_t rem = a.row0 + a.nrows - r0;
+    const int rcount = rem < R ? (int)rem : R;
+
+    // ---- tile table + filter ---------------------------------------------
+    for (int i = tid; i < T; i += NT) {
+      tkey[i] = kReservedDoc;
+      tmask[i] = 0u;
+    }
+    for (int i = tid; i < FWORDS; i += NT) filt[i] = 0u;
+    for (int i = tid; i < R * NT; i += NT) accw[i] = 0u;
+    __syncthreads();
+    for (int it = tid; it < rcount * K; it += NT) {
+      const int r = it / K, k = it - r * K;
+      const uint32_t doc = a.ids[(r0 + r) * (int64_t)K + k];
+      uint32_t h = hash_slot(doc, logT);
+      while (true) {
+        const uint32_t prev = atomicCAS(&tkey[h], kReservedDoc, doc);
+        if (prev == kReservedDoc || prev == doc) break;
+        h = (h + 1) & (T - 1);
+      }
+      atomicOr(&tmask[h], 1u << r);
+      const uint32_t fb = hash_filter(doc);
+      atomicOr(&filt[fb >> 5], 1u << (fb & 31));
+      slot[it] = (uint16_t)h;
+    }
+    __syncthreads();
+    {
+      const int per = T / NT;
+      int cnt = 0;
+      for (int i = 0; i < per; ++i) cnt += __popc(tmask[tid * per + i]);
+      int base = block_excl_scan<NT>(cnt, wsum);
+      for (int i = 0; i < per; ++i) {
+        tbase[tid * per + i] = (uint16_t)base;
+        base += __popc(tmask[tid * per + i]);
+      }
+    }
+    __syncthreads();
+    for (int it = tid; it < rcount * K; it += NT) {
+      const int r = it / K, k = it - r * K;
+      const int h = slot[it];
+      plist[tbase[h] + __popc(tmask[h] & ((1u << r) - 1u))] = (uint8_t)k;
+    }
+    __syncthreads();
+
+    float bv[R];
+    uint32_t bj[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      bv[r] = __int_as_float(0x7f800000);
+      bj[r] = 0xffffffffu;
+    }
+
+    for (int64_t c0 = 0; c0 < N; c0 += CH) {
+      const int64_t jb = c0 + (int64_t)tid * CPT;
+      const uint32_t *colp = a.idsT + jb;
+      int qn = 0;  // warp-uniform queue length
+
+      // drain: all 32 lanes process queued (doc, k, column) candidates
+      auto drain = [&]() {
+        __syncwarp();
+        for (int base = 0; base < qn; base += 32) {
+          const int i = base + lane;
+          const uint32_t doc = i < qn ? myq_doc[i] : kReservedDoc;
+          const uint32_t meta = i < qn ? myq_meta[i] : 0u;
+          const int k = (int)(meta >> 16), col = (int)(meta & 0xffffu);
+          uint32_t h = hash_slot(doc, logT);
+          uint32_t key = tkey[h];
+          while (key != doc && key != kReservedDoc) {
+            h = (h + 1) & (T - 1);
+            key = tkey[h];
+          }
+          uint32_t m = key == doc ? tmask[h] : 0u;
+          int idx = tbase[h];
+          const uint32_t sh = (uint32_t)(col & 1) * 16u;
+          uint32_t *wp = accw + (col >> 1);
+          while (m) {
+            const int r = __ffs(m) - 1;
+            m &= m - 1u;
+            const int pr = plist[idx++];
+            const uint32_t dp = (uint32_t)(pr > k ? pr - k : k - pr);
+            atomicAdd(wp + r * NT, (INC + dp) << sh);
+          }
+        }
+        __syncwarp();
+        qn = 0;
+      };
+
+#pragma unroll 2
+      for (int k = 0; k < K; ++k) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2 *>(colp + (int64_t)k * Npad));
+        const uint32_t f0 = hash_filter(v.x), f1 = hash_filter(v.y);
+        const bool h0 = (filt[f0 >> 5] >> (f0 & 31)) & 1u;
+        const bool h1 = (filt[f1 >> 5] >> (f1 & 31)) & 1u;
+        const unsigned b0 = __ballot_sync(0xffffffffu, h0);
+        const unsigned b1 = __ballot_sync(0xffffffffu, h1);
+        const int n0 = __popc(b0);
+        const uint32_t colb = (uint32_t)(tid * CPT) & 0xffffu;
+        if (h0) {
+          const int pos = qn + __popc(b0 & lt_mask);
+          myq_doc[pos] = v.x;
+          myq_meta[pos] = ((uint32_t)k << 16) | colb;
+        }
+        if (h1) {
+          const int pos = qn + n0 + __popc(b1 & lt_mask);
+          myq_doc[pos] = v.y;
+          myq_meta[pos] = ((uint32_t)k << 16) | (colb + 1u);
+        }
+        qn += n0 + __popc(b1);
+        if (qn > QCAP - 64) drain();
+      }
+      drain();
+
+      // ---- finalize: d = table[packed (s, D)], stores, row min in registers
+      const bool vec_ok = even_n && (c0 + (int64_t)(warp + 1) * 32 * CPT <= N);
+      const bool special = (c0 < r0 + R && r0 < c0 + CH) || (c0 + CH > N);
+      const uint32_t j0 = (uint32_t)jb, j1 = (uint32_t)jb + 1u;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (r < rcount) {
+          const uint32_t w = accw[r * NT + tid];
+          accw[r * NT + tid] = 0u;
+          const uint32_t p0 = w & 0xffffu, p1 = w >> 16;
+          const float d0 = LUT_SMEM ? lut[p0] : __ldg(lut + p0);
+          const float d1 = LUT_SMEM ? lut[p1] : __ldg(lut + p1);
+          const int64_t gi = r0 + r;
+          float *orow = a.rows + (gi - a.row0) * N;
+          if (vec_ok) {
+            __stcs(reinterpret_cast<float2 *>(orow + jb), make_float2(d0, d1));
+          } else {
+            if (jb < N) __stcs(orow + jb, d0);
+            if (jb + 1 < N) __stcs(orow + jb + 1, d1);
+          }
+          if (COUNTS) {
+            if (jb < N) {
+              a.s_out[(gi - a.row0) * N + jb] = (uint8_t)(p0 >> SHIFT);
+              a.D_out[(gi - a.row0) * N + jb] = (uint16_t)(p0 & DMASK);
+            }
+            if (jb + 1 < N) {
+              a.s_out[(gi - a.row0) * N + jb + 1] = (uint8_t)(p1 >> SHIFT);
+              a.D_out[(gi - a.row0) * N + jb + 1] = (uint16_t)(p1 & DMASK);
+            }
+          }
+          float e0 = d0, e1 = d1;
+          if (special) {
+            const float inf = __int_as_float(0x7f800000);
+            e0 = (jb < N && jb != gi) ? d0 : inf;
+            e1 = (jb + 1 < N && jb + 1 != gi) ? d1 : inf;
+          }
+          // strict '<' keeps the smallest column among equal distances (X8)
+          const bool u0 = e0 < bv[r];
+          bv[r] = u0 ? e0 : bv[r];
+          bj[r] = u0 ? j0 : bj[r];
+          const bool u1 = e1 < bv[r];
+          bv[r] = u1 ? e1 : bv[r];
+          bj[r] = u1 ? j1 : bj[r];
+        }
+      }
+    }
+
+    // ---- row NN: warp reduce each row, then across warps -------------------
+    unsigned long long mine = ~0ull;  // lane r: this warp's best key of row r
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      unsigned long long key = ((unsigned long long)__float_as_uint(bv[r]) << 32) | bj[r];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) key = umin64(key, __shfl_xor_sync(0xffffffffu, key, o));
+      mine = (lane == r) ? key : mine;
+    }
+    red[warp * R + lane] = mine;
+    __syncthreads();
+    if (tid < rcount) {
+      unsigned long long best = ~0ull;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) best = umin64(best, red[w * R + tid]);
+      a.nnkey[r0 + tid] = best;
+    }
+    __syncthreads();
+  }
+}
+
+Plan plan(int K, int shift, int lutSmemEntries) {
+  Plan P{};
+  const int need = 2 * R * K;
+  int T = 512, logT = 9;
+  while (T < need) {
+    T <<= 1;
+    ++logT;
+  }
+  P.T = T;
+  P.logT = logT;
+  P.shift = shift;
+  P.lutEntries = lutSmemEntries;
+  size_t o = 0;
+  auto take = [&](size_t bytes, size_t align) {
+    o = (o + align - 1) / align * align;
+    const size_t at = o;
+    o += bytes;
+    return at;
+  };
+  P.off_acc = take((size_t)R * NT * 4, 16);
+  P.off_key = take((size_t)T * 4, 16);
+  P.off_mask = take((size_t)T * 4, 16);
+  P.off_base = take((size_t)T * 2, 16);
+  P.off_slot = take((size_t)R * K * 2, 16);
+  P.off_plist = take((size_t)R * K, 16);
+  P.off_filter = take((size_t)FWORDS * 4, 16);
+  P.off_qdoc = take((size_t)NW * QCAP * 4, 16);
+  P.off_qmeta = take((size_t)NW * QCAP * 4, 16);
+  P.off_red = take((size_t)NW * R * 8, 16);
+  P.off_wsum = take(32 * 4, 16);
+  P.off_lut = take((size_t)lutSmemEntries * 4, 16);
+  P.total = (o + 15) / 16 * 16;
+  return P;
+}
+
+template <int SHIFT, bool LS, bool C>
+cudaError_t launch(const DistArgs &a, const Plan &P, cudaStream_t st) {
+  auto kern = k_dist_tile<SHIFT, LS, C>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)P.total);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, P.total);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t ntiles = (a.nrows + R - 1) / R;
+  int64_t grid = std::min<int64_t>(ntiles, (int64_t)sms * per_sm);
+  if (const char *g = std::getenv("RAGB_DIST_GRID")) grid = std::min<int64_t>(ntiles, std::atoll(g));
+  kern<<<(unsigned)grid, NT, P.total, st>>>(a, P);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int tile_lut_shift(int32_t K) { return K <= 22 ? 8 : 10; }
+
+int64_t tile_lut_entries(int32_t K) {
+  return (int64_t)(K + 1) << tile_lut_shift(K);
+}
+
+bool tile_path_ok(int32_t K, bool uniform) { return uniform && K <= 32; }
+
+cudaError_t launch_distance_tile(const DistArgs &a, cudaStream_t st) {
+  const int shift = tile_lut_shift(a.K);
+  const int64_t entries = tile_lut_entries(a.K);
+  const bool lut_smem = shift == 8;  // (K+1) * 256 floats <= 23.5 KB
+  const Plan P = plan(a.K, shift, lut_smem ? (int)entries : 0);
+  const bool C = a.s_out != nullptr;
+  if (shift == 8) return C ? launch<8, true, true>(a, P, st) : launch<8, true, false>(a, P, st);
+  return C ? launch<10, false, true>(a, P, st) : launch<10, false, false>(a, P, st);
+}
+
+}  // namespace ragb

@@ -11,9 +11,19 @@
 // descending order".  Readings X9-X14: greedy key order, top-down
 // ordered prefixes, collapse of virtual nodes equal to their parent, children
 // by rep, schedule groups by first appearance with index ties.
+//
+// Node ids: 0 = root, 1..V = kept virtual nodes, V+1+i = leaf (context) i.
+// The replay accepts any dependency-respecting merge order (the device emits
+// rounds); the exported merge order is sorted by key (X9).
+#include <omp.h>
+
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <parallel/algorithm>
 #include <string>
 #include <vector>
 
@@ -23,232 +33,306 @@ namespace ragb {
 
 namespace {
 
-struct Pool {  // flat storage of sorted doc sets
-  std::vector<uint32_t> ids;
-  std::vector<int64_t> off;
-  std::vector<int32_t> len;
-  const uint32_t *ptr(int64_t i) const { return ids.data() + off[i]; }
+struct MergeKey {
+  float h;
+  int32_t a, b, size;
 };
 
-bool equal_sets(const Pool &P, int64_t x, int64_t y) {
-  if (P.len[x] != P.len[y]) return false;
-  return std::memcmp(P.ptr(x), P.ptr(y), sizeof(uint32_t) * (size_t)P.len[x]) == 0;
+bool key_less(const MergeKey &x, const MergeKey &y) {
+  if (x.h != y.h) return x.h < y.h;
+  if (x.a != y.a) return x.a < y.a;
+  return x.b < y.b;
+}
+
+// membership of x in a small sorted array
+inline bool in_sorted(const uint32_t *s, int n, uint32_t x) {
+  if (n <= 8) {
+    for (int i = 0; i < n; ++i)
+      if (s[i] == x) return true;
+    return false;
+  }
+  return std::binary_search(s, s + n, x);
 }
 
 }  // namespace
 
+int host_threads() {
+  static int n = [] {
+    if (const char *e = std::getenv("RAGB_HOST_THREADS")) return std::max(1, std::atoi(e));
+    return std::max(1, std::min(16, omp_get_num_procs()));
+  }();
+  return n;
+}
+
 rb_status host_build(HostIndex &H, std::string *msg) {
   const int64_t N = H.N;
   const int32_t K = H.K;
-  // ---- merge order: ascending (h, a, b) (X9) ------------------------------
+  const bool uniform = H.lens.empty();
+  const int nth = host_threads();
+  const bool trace = std::getenv("RAGB_TRACE") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto lap = [&](const char *what) {
+    if (!trace) return;
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[ragb host] %-12s %.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t - t_last).count());
+    t_last = t;
+  };
+  auto len_of = [&](int64_t i) -> int { return uniform ? K : H.lens[i]; };
   const int64_t nz = (int64_t)H.za.size();
   if (nz != N - 1) {
     *msg = "merge list must have N-1 rows";
     return RB_EINVAL;
   }
-  {
-    std::vector<int64_t> perm(nz);
-    std::iota(perm.begin(), perm.end(), 0);
-    std::sort(perm.begin(), perm.end(), [&](int64_t x, int64_t y) {
-      if (H.zh[x] != H.zh[y]) return H.zh[x] < H.zh[y];
-      if (H.za[x] != H.za[y]) return H.za[x] < H.za[y];
-      return H.zb[x] < H.zb[y];
-    });
-    std::vector<int32_t> a(nz), b(nz), s(nz);
-    std::vector<float> h(nz);
-    for (int64_t t = 0; t < nz; ++t) {
-      a[t] = H.za[perm[t]];
-      b[t] = H.zb[perm[t]];
-      s[t] = H.zs[perm[t]];
-      h[t] = H.zh[perm[t]];
-    }
-    H.za.swap(a);
-    H.zb.swap(b);
-    H.zs.swap(s);
-    H.zh.swap(h);
-  }
 
-  // ---- raw binary tree with intersection sets -----------------------------
-  const int64_t nraw = 2 * N - 1;
-  Pool P;
-  P.off.resize(nraw);
-  P.len.resize(nraw);
-  P.ids.reserve((size_t)N * K * 2);
+  // ---- sorted leaf sets (parallel) ----------------------------------------
+  std::vector<uint32_t> lset((size_t)N * K);
+#pragma omp parallel for num_threads(nth) schedule(static)
   for (int64_t i = 0; i < N; ++i) {
-    const int L = H.lens.empty() ? K : H.lens[i];
-    P.off[i] = (int64_t)P.ids.size();
-    P.len[i] = L;
-    P.ids.insert(P.ids.end(), H.ids.begin() + i * K, H.ids.begin() + i * K + L);
-    std::sort(P.ids.begin() + P.off[i], P.ids.end());
+    uint32_t *d = lset.data() + i * K;
+    const uint32_t *s = H.ids.data() + i * K;
+    const int L = len_of(i);
+    for (int k = 0; k < L; ++k) {  // insertion sort (K <= 255, typically 5-20)
+      const uint32_t x = s[k];
+      int q = k;
+      while (q > 0 && d[q - 1] > x) {
+        d[q] = d[q - 1];
+        --q;
+      }
+      d[q] = x;
+    }
   }
+  lap("leaf sets");
+
+  // ---- raw binary tree with intersection sets (replay) --------------------
+  // raw node r < N: leaf r (set in lset); r = N + t: merge t (set in pool)
+  std::vector<int64_t> voff(nz + 1, 0);
+  std::vector<uint32_t> vpool;
+  vpool.reserve((size_t)N * 4 + 64);
   std::vector<int32_t> rchild(2 * std::max<int64_t>(nz, 0));
-  std::vector<int32_t> rrep(nraw);
-  std::vector<int64_t> cur(N);
+  std::vector<int32_t> cur(N);
   std::vector<int32_t> csize(N, 1);
-  for (int64_t i = 0; i < N; ++i) {
-    rrep[i] = (int32_t)i;
-    cur[i] = i;
-  }
+  std::iota(cur.begin(), cur.end(), 0);
+  auto set_ptr = [&](int64_t r, int *n) -> const uint32_t * {
+    if (r < N) {
+      *n = len_of(r);
+      return lset.data() + r * K;
+    }
+    *n = (int)(voff[r - N + 1] - voff[r - N]);
+    return vpool.data() + voff[r - N];
+  };
   for (int64_t t = 0; t < nz; ++t) {
     const int32_t a = H.za[t], b = H.zb[t];
     if (a < 0 || b >= N || a >= b || cur[a] < 0 || cur[b] < 0 || csize[a] + csize[b] != H.zs[t]) {
       *msg = "inconsistent merge at row " + std::to_string(t);
       return RB_EINVAL;
     }
-    const int64_t A = cur[a], B = cur[b], v = N + t;
-    rchild[2 * t] = (int32_t)A;
-    rchild[2 * t + 1] = (int32_t)B;
-    rrep[v] = a;
-    const uint32_t *pa = P.ptr(A), *pb = P.ptr(B);
-    const int la = P.len[A], lb = P.len[B];
-    P.off[v] = (int64_t)P.ids.size();
-    int ia = 0, ib = 0, n = 0;
+    const int32_t A = cur[a], B = cur[b];
+    rchild[2 * t] = A;
+    rchild[2 * t + 1] = B;
+    int la, lb;
+    const uint32_t *pa = set_ptr(A, &la);
+    const uint32_t *pb = set_ptr(B, &lb);
+    uint32_t tmp[256];
+    int n = 0, ia = 0, ib = 0;
     while (ia < la && ib < lb) {  // sorted intersection
       if (pa[ia] < pb[ib]) {
         ++ia;
       } else if (pb[ib] < pa[ia]) {
         ++ib;
       } else {
-        P.ids.push_back(pa[ia]);
-        pa = P.ptr(A);  // push_back may reallocate
-        pb = P.ptr(B);
+        tmp[n++] = pa[ia];
         ++ia;
         ++ib;
-        ++n;
       }
     }
-    P.len[v] = n;
-    cur[a] = v;
+    vpool.insert(vpool.end(), tmp, tmp + n);
+    voff[t + 1] = (int64_t)vpool.size();
+    cur[a] = (int32_t)(N + t);
     cur[b] = -1;
     csize[a] += csize[b];
   }
-  const int64_t top = (N == 1) ? 0 : N + nz - 1;
-  if (cur[0] != top) {
+  const int64_t top = cur[0];
+  if (csize[0] != N) {
     *msg = "merges do not join all contexts";
     return RB_EINVAL;
   }
+  lap("raw tree");
 
-  // ---- collapse + ordered prefixes + paths, breadth first ------------------
-  H.parent.assign(1, -1);
-  H.leaf.assign(1, -1);
-  H.rep.assign(1, -1);
-  std::vector<int64_t> setref(1, -1);  // raw node whose set is the node's set (-1: empty)
-  std::vector<int64_t> node_raw(1, -1);
-  H.prefix_off.assign(2, 0);  // [off[c], off[c+1]) = node c's ordered context
-  H.prefix_ids.clear();
-  H.prefix_ids.reserve((size_t)N * K * 2);
-  std::vector<int64_t> npath_off(2, 0);  // root: empty path
-  std::vector<int32_t> npath;
-  H.leaf_node.assign(N, -1);
-  std::vector<int64_t> kids, stack;
-  std::vector<uint32_t> tmp;
-  int64_t n_virtual = 0;
-
-  for (int64_t q = 0; q < (int64_t)H.parent.size(); ++q) {
-    // children raw nodes of q, expanded through collapsed virtual nodes
-    kids.clear();
-    stack.clear();
-    if (q == 0) {
-      stack.push_back(top);
-    } else if (node_raw[q] >= N) {
-      const int64_t t = node_raw[q] - N;
-      stack.push_back(rchild[2 * t + 1]);
-      stack.push_back(rchild[2 * t]);
-    } else {
-      continue;  // leaf
-    }
-    const int64_t pset = setref[q];
-    while (!stack.empty()) {
-      const int64_t r = stack.back();
-      stack.pop_back();
-      const bool same = r >= N && (pset < 0 ? P.len[r] == 0 : equal_sets(P, r, pset));
-      if (same) {  // collapse (X11)
-        const int64_t t = r - N;
-        stack.push_back(rchild[2 * t + 1]);
-        stack.push_back(rchild[2 * t]);
+  // ---- collapse (X11): DFS over the raw tree ------------------------------
+  // kept virtual node k (1..V): raw node vraw[k-1], parent node id vpar[k-1].
+  std::vector<int64_t> vraw;
+  std::vector<int32_t> vpar;
+  vraw.reserve(nz);
+  vpar.reserve(nz);
+  H.lparent.assign(N, 0);
+  {
+    struct Item {
+      int64_t raw;
+      int32_t kept_parent;
+      int64_t eff;  // raw node holding the effective parent set (-1: empty root set)
+    };
+    std::vector<Item> st;
+    st.reserve(64);
+    st.push_back({top, 0, -1});
+    while (!st.empty()) {
+      const Item it = st.back();
+      st.pop_back();
+      if (it.raw < N) {
+        H.lparent[it.raw] = it.kept_parent;
+        continue;
+      }
+      int n1, n2;
+      const uint32_t *s1 = set_ptr(it.raw, &n1);
+      bool same;
+      if (it.eff < 0) {
+        same = n1 == 0;
       } else {
-        kids.push_back(r);
+        const uint32_t *s2 = set_ptr(it.eff, &n2);
+        same = n1 == n2 && std::memcmp(s1, s2, 4 * (size_t)n1) == 0;
       }
-    }
-    std::sort(kids.begin(), kids.end(), [&](int64_t x, int64_t y) { return rrep[x] < rrep[y]; });
-    // parent's ordered context and set
-    const int64_t poff = H.prefix_off[q], plen = H.prefix_off[q + 1] - H.prefix_off[q];
-    const uint32_t *pset_ids = pset < 0 ? nullptr : P.ptr(pset);
-    const int pset_len = pset < 0 ? 0 : P.len[pset];
-    for (size_t ci = 0; ci < kids.size(); ++ci) {
-      const int64_t r = kids[ci];
-      const int64_t c = (int64_t)H.parent.size();
-      H.parent.push_back((int32_t)q);
-      H.leaf.push_back(r < N ? (int32_t)r : -1);
-      H.rep.push_back(rrep[r]);
-      setref.push_back(r);
-      node_raw.push_back(r);
-      // path = parent's path + child index
-      const int64_t pp0 = npath_off[q], pp1 = npath_off[q + 1];
-      for (int64_t z = pp0; z < pp1; ++z) npath.push_back(npath[z]);
-      npath.push_back((int32_t)ci);
-      npath_off.push_back((int64_t)npath.size());
-      // ordered context
-      tmp.assign(H.prefix_ids.begin() + poff, H.prefix_ids.begin() + poff + plen);
-      if (r < N) {  // leaf: prefix ++ remaining docs in original order
-        const int L = H.lens.empty() ? K : H.lens[r];
-        const uint32_t *row = H.ids.data() + r * K;
-        for (int k = 0; k < L; ++k)
-          if (!std::binary_search(pset_ids, pset_ids + pset_len, row[k])) tmp.push_back(row[k]);
-        H.leaf_node[r] = c;
-      } else {  // virtual: prefix ++ ascending new docs (X10)
-        ++n_virtual;
-        const uint32_t *s = P.ptr(r);
-        for (int k = 0; k < P.len[r]; ++k)
-          if (!std::binary_search(pset_ids, pset_ids + pset_len, s[k])) tmp.push_back(s[k]);
+      const int64_t t = it.raw - N;
+      int32_t kp = it.kept_parent;
+      int64_t eff = it.eff;
+      if (!same) {
+        vraw.push_back(it.raw);
+        vpar.push_back(it.kept_parent);
+        kp = (int32_t)vraw.size();
+        eff = it.raw;
       }
-      H.prefix_ids.insert(H.prefix_ids.end(), tmp.begin(), tmp.end());
-      H.prefix_off.push_back((int64_t)H.prefix_ids.size());
+      st.push_back({rchild[2 * t + 1], kp, eff});
+      st.push_back({rchild[2 * t], kp, eff});
     }
   }
-  // leaf paths in context order
-  H.path_off.assign(N + 1, 0);
-  H.path.clear();
-  int64_t max_depth = 0;
-  for (int64_t i = 0; i < N; ++i) {
-    const int64_t c = H.leaf_node[i];
-    const int64_t p0 = npath_off[c], p1 = npath_off[c + 1];
-    H.path.insert(H.path.end(), npath.begin() + p0, npath.begin() + p1);
-    H.path_off[i + 1] = (int64_t)H.path.size();
-    max_depth = std::max(max_depth, p1 - p0);
-  }
-  H.stats.n_virtual = n_virtual;
-  H.stats.max_depth = max_depth;
+  const int64_t V = (int64_t)vraw.size();
+  lap("collapse");
 
-  // ---- offline order (a7) -------------------------------------------------
+  // ---- children CSR over nodes 0..V, ordered by rep (X12) -----------------
+  std::vector<int32_t> rep_of(1 + V + N);
+  rep_of[0] = -1;
+  for (int64_t k = 1; k <= V; ++k) rep_of[k] = H.za[vraw[k - 1] - N];  // rep = a (< b)
+  for (int64_t i = 0; i < N; ++i) rep_of[V + 1 + i] = (int32_t)i;
+  H.kids_off.assign(V + 2, 0);
+  for (int64_t k = 1; k <= V; ++k) ++H.kids_off[vpar[k - 1] + 1];
+  for (int64_t i = 0; i < N; ++i) ++H.kids_off[H.lparent[i] + 1];
+  for (int64_t k = 0; k <= V; ++k) H.kids_off[k + 1] += H.kids_off[k];
+  H.kids.assign(V + N, 0);
+  {
+    std::vector<int64_t> fill(H.kids_off.begin(), H.kids_off.end() - 1);
+    for (int64_t k = 1; k <= V; ++k) H.kids[fill[vpar[k - 1]]++] = (int32_t)k;
+    for (int64_t i = 0; i < N; ++i) H.kids[fill[H.lparent[i]]++] = (int32_t)(V + 1 + i);
+  }
+  std::vector<int32_t> child_idx(1 + V + N, 0);
+#pragma omp parallel for num_threads(nth) schedule(dynamic, 256)
+  for (int64_t k = 0; k <= V; ++k) {
+    int32_t *b = H.kids.data() + H.kids_off[k], *e = H.kids.data() + H.kids_off[k + 1];
+    std::sort(b, e, [&](int32_t x, int32_t y) { return rep_of[x] < rep_of[y]; });
+    for (int32_t *p = b; p < e; ++p) child_idx[*p] = (int32_t)(p - b);
+  }
+  lap("children");
+
+  // ---- virtual nodes: ordered prefixes (X10) and paths, top-down ----------
+  // DFS creation order puts every parent before its children.
+  H.V = V;
+  H.vparent.assign(vpar.begin(), vpar.end());
+  H.vrep.resize(V);
+  H.vpre_off.assign(V + 2, 0);  // by node id 0..V (root: empty)
+  H.vpre.clear();
+  H.vpre.reserve((size_t)V * 4 + 16);
+  std::vector<int64_t> vpath_off(V + 2, 0);
+  std::vector<int32_t> vpath;
+  vpath.reserve((size_t)V * 6 + 16);
+  std::vector<int32_t> depth(V + 1, 0);
+  for (int64_t k = 1; k <= V; ++k) {
+    const int32_t p = vpar[k - 1];
+    H.vrep[k - 1] = rep_of[k];
+    // prefix = prefix(parent) ++ sorted(set(k) \ set(parent))
+    const int64_t p0 = H.vpre_off[p], p1 = H.vpre_off[p + 1];
+    for (int64_t z = p0; z < p1; ++z) H.vpre.push_back(H.vpre[z]);
+    int nk, np = 0;
+    const uint32_t *sk = set_ptr(vraw[k - 1], &nk);
+    const uint32_t *sp = p > 0 ? set_ptr(vraw[p - 1], &np) : nullptr;
+    int q = 0;
+    for (int x = 0; x < nk; ++x) {  // both sorted: merge-difference
+      while (q < np && sp[q] < sk[x]) ++q;
+      if (q < np && sp[q] == sk[x]) continue;
+      H.vpre.push_back(sk[x]);
+    }
+    H.vpre_off[k + 1] = (int64_t)H.vpre.size();
+    depth[k] = depth[p] + 1;
+    for (int64_t z = vpath_off[p]; z < vpath_off[p + 1]; ++z) vpath.push_back(vpath[z]);
+    vpath.push_back(child_idx[k]);
+    vpath_off[k + 1] = (int64_t)vpath.size();
+  }
+  lap("virtual");
+
+  // ---- leaves (parallel): ordered contexts (a7), prefix lengths, paths -----
   H.ordered.assign(H.ids.begin(), H.ids.end());
   H.prefix_len.assign(N, 0);
+  H.path_off.assign(N + 1, 0);
+  for (int64_t i = 0; i < N; ++i) H.path_off[i + 1] = H.path_off[i] + depth[H.lparent[i]] + 1;
+  H.path.assign(H.path_off[N], 0);
+  int64_t max_depth = 0;
+#pragma omp parallel for num_threads(nth) schedule(static) reduction(max : max_depth)
   for (int64_t i = 0; i < N; ++i) {
-    const int64_t c = H.leaf_node[i];
-    const int64_t o0 = H.prefix_off[c], o1 = H.prefix_off[c + 1];
-    std::copy(H.prefix_ids.begin() + o0, H.prefix_ids.begin() + o1, H.ordered.begin() + i * K);
-    const int64_t p = H.parent[c];
-    H.prefix_len[i] = (uint8_t)(H.prefix_off[p + 1] - H.prefix_off[p]);
+    const int32_t p = H.lparent[i];
+    const int64_t p0 = H.vpre_off[p], p1 = H.vpre_off[p + 1];
+    uint32_t *out = H.ordered.data() + i * K;
+    int o = 0;
+    for (int64_t z = p0; z < p1; ++z) out[o++] = H.vpre[z];
+    int np = 0;
+    const uint32_t *sp = p > 0 ? set_ptr(vraw[p - 1], &np) : nullptr;
+    const uint32_t *row = H.ids.data() + i * K;
+    const int L = len_of(i);
+    for (int k = 0; k < L; ++k)
+      if (!in_sorted(sp, np, row[k])) out[o++] = row[k];
+    H.prefix_len[i] = (uint8_t)(p1 - p0);
+    int32_t *pp = H.path.data() + H.path_off[i];
+    for (int64_t z = vpath_off[p]; z < vpath_off[p + 1]; ++z) *pp++ = vpath[z];
+    *pp = child_idx[V + 1 + i];
+    max_depth = std::max<int64_t>(max_depth, H.path_off[i + 1] - H.path_off[i]);
   }
-  // ---- schedule: group by path[0], first appearance; length desc; index ---
+  H.stats.n_virtual = V;
+  H.stats.max_depth = max_depth;
+  lap("leaves");
+
+  // ---- schedule: counting sort by (group of first appearance, -len, index) -
   {
-    std::vector<int64_t> gorder(N, -1);  // root-child index -> group rank
-    std::vector<int64_t> grank(N);
+    const int64_t G = H.kids_off[1] - H.kids_off[0];  // root children
+    std::vector<int64_t> grank(G, -1);
     int64_t ng = 0;
+    std::vector<int64_t> key(N);
+    const int64_t LMAX = max_depth + 1;
     for (int64_t i = 0; i < N; ++i) {
       const int32_t g = H.path[H.path_off[i]];
-      if (gorder[g] < 0) gorder[g] = ng++;
-      grank[i] = gorder[g];
+      if (grank[g] < 0) grank[g] = ng++;
+      const int64_t len = H.path_off[i + 1] - H.path_off[i];
+      key[i] = grank[g] * LMAX + (LMAX - len);  // length descending within a group
     }
+    std::vector<int64_t> cnt(ng * LMAX + 1, 0);
+    for (int64_t i = 0; i < N; ++i) ++cnt[key[i] + 1];
+    for (size_t z = 1; z < cnt.size(); ++z) cnt[z] += cnt[z - 1];
     H.schedule.resize(N);
-    std::iota(H.schedule.begin(), H.schedule.end(), 0);
-    std::sort(H.schedule.begin(), H.schedule.end(), [&](int64_t x, int64_t y) {
-      if (grank[x] != grank[y]) return grank[x] < grank[y];
-      const int64_t lx = H.path_off[x + 1] - H.path_off[x], ly = H.path_off[y + 1] - H.path_off[y];
-      if (lx != ly) return lx > ly;
-      return x < y;
-    });
+    for (int64_t i = 0; i < N; ++i) H.schedule[cnt[key[i]]++] = i;  // stable: index order
   }
+  lap("schedule");
+
+  // ---- exported merge order: ascending key (X9) ---------------------------
+  {
+    std::vector<MergeKey> zk(nz);
+    for (int64_t t = 0; t < nz; ++t) zk[t] = {H.zh[t], H.za[t], H.zb[t], H.zs[t]};
+    if (nth > 1 && nz > 4096)
+      __gnu_parallel::sort(zk.begin(), zk.end(), key_less);
+    else
+      std::sort(zk.begin(), zk.end(), key_less);
+    for (int64_t t = 0; t < nz; ++t) {
+      H.za[t] = zk[t].a;
+      H.zb[t] = zk[t].b;
+      H.zh[t] = zk[t].h;
+      H.zs[t] = zk[t].size;
+    }
+  }
+  lap("sort merges");
   return RB_OK;
 }
 

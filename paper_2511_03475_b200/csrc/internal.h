@@ -48,12 +48,19 @@ struct DistArgs {
   const float *lut;           // Eq. 1 table d(s, D) for uniform length K, or nullptr
 };
 
-// Eq. 1 table: (K+1) x (floor(K^2/2)+1) floats for K <= kLutMaxK.
+// Eq. 1 table d(s, D) at index s * stride + D.  Tile path (uniform K <= 32):
+// stride = 1 << shift (the packed accumulator is the index); general path
+// (uniform K <= kLutMaxK): stride = floor(K^2/2) + 1; variable lengths: none.
 constexpr int kLutMaxK = 128;
 constexpr int64_t kLutSmemBytes = 20 * 1024;
-int64_t eq1_lut_entries(int32_t K);
-cudaError_t launch_eq1_lut(float *lut, int32_t K, uint32_t an, uint32_t ad, cudaStream_t st,
-                           int *launches);
+void distance_lut_layout(int32_t K, bool uniform, int *stride, int64_t *entries);
+cudaError_t launch_eq1_lut(float *lut, int32_t K, int stride, int64_t entries, uint32_t an,
+                           uint32_t ad, cudaStream_t st, int *launches);
+// Fast path (distance_tile.cu): uniform contexts with K <= 32.
+bool tile_path_ok(int32_t K, bool uniform);
+int tile_lut_shift(int32_t K);
+int64_t tile_lut_entries(int32_t K);
+cudaError_t launch_distance_tile(const DistArgs &a, cudaStream_t st);
 
 cudaError_t launch_validate(const uint32_t *ids, const uint8_t *lens, int64_t N, int32_t K,
                             int64_t Npad, uint32_t *idsT, uint32_t *err, cudaStream_t st,
@@ -83,10 +90,15 @@ struct HostIndex {
   std::vector<float> nn_d;
   std::vector<int32_t> za, zb, zs;
   std::vector<float> zh;
-  // tree (node 0 = root)
-  std::vector<int32_t> parent, leaf, rep, leaf_node;
-  std::vector<int64_t> prefix_off, path_off;  // prefix_off per node; path_off per leaf (context)
-  std::vector<uint32_t> prefix_ids;
+  // tree: node 0 = root, 1..V = kept virtual nodes, V+1+i = leaf (context) i
+  int64_t V = 0;
+  std::vector<int32_t> vparent, vrep;  // [V] parent node id / rep of virtual node k (k-1)
+  std::vector<int64_t> vpre_off;       // [V+2] ordered prefix CSR by node id 0..V
+  std::vector<uint32_t> vpre;
+  std::vector<int32_t> lparent;        // [N] parent node id of leaf i
+  std::vector<int64_t> kids_off;       // [V+2] children CSR over nodes 0..V, rep order
+  std::vector<int32_t> kids;
+  std::vector<int64_t> path_off;       // [N+1] leaf search paths
   std::vector<int32_t> path;
   // offline orders
   std::vector<uint32_t> ordered;   // [N][K]
@@ -98,5 +110,6 @@ struct HostIndex {
 // Sort merges into greedy key order (X9) and validate them; builds tree,
 // orders and schedule (a6-a7).  Returns RB_OK or RB_EINVAL with msg.
 rb_status host_build(HostIndex &H, std::string *msg);
+int host_threads();
 
 }  // namespace ragb

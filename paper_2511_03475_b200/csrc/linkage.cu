@@ -17,7 +17,7 @@
 //       continue; then the next vertex.  This is done by one CTA (k_round_prep).
 //   (2) RNN pairs above h are merges of the unique reducible hierarchy and are
 //       disjoint from (1) (a vertex with an h-neighbour has its NN at h).
-// Then one fused pass (k_merge_compact) writes the merged, order-preserving
+// Then one fused pass (k_merge_rows) writes the merged, order-preserving
 // compacted matrix (max over group members) and the new row-min keys.  Because
 // compaction preserves order and a group's survivor is its smallest member,
 // compacted index order == rep order, so the row key (d bits << 32 | column)
@@ -26,6 +26,8 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -34,7 +36,6 @@ namespace {
 
 typedef unsigned long long u64;
 constexpr int PT = 1024;  // threads of the single-CTA round-prep kernel
-constexpr int MT = 256;   // threads of the merge/compact kernel
 
 struct PrepArgs {
   const float *D;
@@ -49,7 +50,7 @@ struct PrepArgs {
   int *za, *zb, *zs;
   float *zh;
   int *zcount;
-  int *newidx, *goff, *gmem, *colsrc, *cnt, *cursor;
+  int *newidx, *goff, *gmem, *colsrc /* colmap */, *cnt, *cursor /* then first_old */;
   int *rep_n, *sz_n;
   int *Mn;
 };
@@ -232,47 +233,82 @@ __global__ void __launch_bounds__(PT, 1) k_round_prep(PrepArgs a) {
     a.gmem[a.goff[g] + atomicAdd(&a.cursor[g], 1)] = x;
   }
   __syncthreads();
-  for (int g = tid; g < Mn; g += PT)
-    a.colsrc[g] = (a.cnt[g] == 1) ? a.gmem[a.goff[g]] : -(a.goff[g] + 1);
+  // old column -> new column; new column -> its leader (smallest old member)
+  for (int x = tid; x < M; x += PT) {
+    const int l = a.leader[x];
+    const int g = a.newidx[l];
+    a.colsrc[x] = g;
+    if (l == x) a.cursor[g] = x;  // cursor is free after the scatter: first_old
+  }
 }
 
-// Fused merge + compaction + row min: Dn[c][j] = max over members r of group
-// c and s of group j of D[r][s]; keyn[c] = min_{j != c} (Dn[c][j] bits, j).
-__global__ void __launch_bounds__(MT) k_merge_compact(const float *__restrict__ D, int64_t ld,
-                                                      const int *__restrict__ Mn_p,
-                                                      const int *__restrict__ goff,
-                                                      const int *__restrict__ gmem,
-                                                      const int *__restrict__ colsrc,
-                                                      float *__restrict__ Dn, u64 *__restrict__ keyn) {
-  __shared__ u64 wmin[MT / 32];
+// Fused merge + compaction + row min (complete linkage, X7):
+//   Dn[c][t] = max over old rows r in group c and old columns s in group t of
+//   D[r][s];  keyn[c] = min_{t != c} (Dn[c][t] bits, t).
+// One CTA builds one new row in a shared-memory window: it streams the old
+// row(s) of group c with coalesced loads, maps every old column s to its new
+// column t = colmap[s], and folds the value in with a shared-memory integer
+// atomicMax (d >= 0, so int order == float order).  The window is then written
+// out with coalesced stores and scanned for the row min.  Rows wider than the
+// window are done in several windows; a window starting at new column T0 only
+// needs old columns >= first_old[T0] (members of later groups are never
+// smaller than their leader).
+constexpr int MT2 = 1024;
+
+__global__ void __launch_bounds__(MT2) k_merge_rows(const float *__restrict__ D, int64_t ld, int M,
+                                                    const int *__restrict__ Mn_p,
+                                                    const int *__restrict__ goff,
+                                                    const int *__restrict__ gmem,
+                                                    const int *__restrict__ colmap,
+                                                    const int *__restrict__ first_old, int W,
+                                                    float *__restrict__ Dn, u64 *__restrict__ keyn) {
+  extern __shared__ __align__(16) int win[];  // [W] float bits
+  __shared__ u64 wmin[MT2 / 32];
   const int Mn = *Mn_p;
+  const int64_t ldn = (Mn + 3) & ~3;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   for (int c = blockIdx.x; c < Mn; c += gridDim.x) {
     const int rb = goff[c], re = goff[c + 1];
-    const float *r0 = D + (int64_t)gmem[rb] * ld;
-    float *out = Dn + (int64_t)c * Mn;
+    const float *row0 = D + (int64_t)gmem[rb] * ld;
     u64 best = ~0ull;
-    for (int j = tid; j < Mn; j += MT) {
-      const int src = colsrc[j];
-      float v;
-      if (src >= 0) {
-        v = r0[src];
-        for (int rr = rb + 1; rr < re; ++rr) v = fmaxf(v, D[(int64_t)gmem[rr] * ld + src]);
-      } else {
-        const int sb = -src - 1, se = goff[j + 1];
-        v = 0.0f;
-        for (int rr = rb; rr < re; ++rr) {
-          const float *row = D + (int64_t)gmem[rr] * ld;
-          for (int ss = sb; ss < se; ++ss) v = fmaxf(v, row[gmem[ss]]);
+    for (int T0 = 0; T0 < Mn; T0 += W) {
+      const int Wn = min(W, Mn - T0);
+      for (int i = tid; i < Wn; i += MT2) win[i] = 0;
+      __syncthreads();
+      const int s0 = T0 == 0 ? 0 : first_old[T0];
+      // 4 independent (colmap, value) load pairs in flight per thread
+      constexpr int U = 4;
+      for (int sb = s0; sb < M; sb += U * MT2) {
+        int t[U];
+        float v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int s = sb + u * MT2 + tid;
+          t[u] = s < M ? __ldg(colmap + s) - T0 : -1;
+          v[u] = s < M ? __ldcs(row0 + s) : 0.0f;
         }
+        for (int rr = rb + 1; rr < re; ++rr) {
+          const float *rowk = D + (int64_t)gmem[rr] * ld;
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int s = sb + u * MT2 + tid;
+            if (s < M) v[u] = fmaxf(v[u], __ldcs(rowk + s));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (t[u] >= 0 && t[u] < Wn) atomicMax(win + t[u], __float_as_int(v[u]));
       }
-      if (j == c) {
-        v = 0.0f;
-      } else {
-        const u64 k = ((u64)__float_as_uint(v) << 32) | (unsigned)j;
-        best = k < best ? k : best;
+      __syncthreads();
+      float *out = Dn + (int64_t)c * ldn + T0;
+      for (int i = tid; i < Wn; i += MT2) {
+        const int t = T0 + i;
+        const float v = t == c ? 0.0f : __int_as_float(win[i]);
+        __stcs(out + i, v);
+        const u64 key = ((u64)__float_as_uint(v) << 32) | (unsigned)t;
+        best = (t != c && key < best) ? key : best;
       }
-      out[j] = v;
+      __syncthreads();
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -284,7 +320,7 @@ __global__ void __launch_bounds__(MT) k_merge_compact(const float *__restrict__ 
     if (tid == 0) {
       u64 b = wmin[0];
 #pragma unroll
-      for (int i = 1; i < MT / 32; ++i) b = wmin[i] < b ? wmin[i] : b;
+      for (int i = 1; i < MT2 / 32; ++i) b = wmin[i] < b ? wmin[i] : b;
       keyn[c] = b;
     }
     __syncthreads();
@@ -354,7 +390,14 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
   int M = (int)N;
   int p = 0;
   float *next = matA;
+  // RAGB_TRACE=1: per-round timing on stderr (diagnostics only).
+  const bool trace = std::getenv("RAGB_TRACE") != nullptr;
+  cudaEvent_t tev[3];
+  if (trace)
+    for (auto &x : tev) cudaEventCreate(&x);
+  int prev_z = 0;
   while (M > 1) {
+    if (trace) cudaEventRecord(tev[0], st);
     pa.D = cur;
     pa.ld = ld;
     pa.M = M;
@@ -366,6 +409,7 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
     k_round_prep<<<1, PT, 0, st>>>(pa);
     ++*launches;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (trace) cudaEventRecord(tev[1], st);
     int host_c[2];
     if ((e = cudaMemcpyAsync(host_c, counters, sizeof(host_c), cudaMemcpyDeviceToHost, st)) !=
         cudaSuccess)
@@ -375,18 +419,37 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
     const int Mn = host_c[1];
     if (Mn >= M || Mn < 1) return cudaErrorUnknown;  // no progress: invariant violated
     if (Mn > 1) {
-      const int grid = std::min<int>(Mn, sms * 8);
-      k_merge_compact<<<grid, MT, 0, st>>>(cur, ld, pa.Mn, pa.goff, pa.gmem, pa.colsrc, next,
-                                           key[p ^ 1]);
+      // window: the whole new row if it fits in shared memory, else pieces
+      const int maxW = 56 * 1024;
+      const int W = std::min<int>((Mn + 3) & ~3, maxW);
+      const size_t smem = (size_t)W * 4;
+      cudaFuncSetAttribute(k_merge_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      int per_sm = 1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_merge_rows, MT2, smem);
+      const int grid = std::min<int>(Mn, sms * std::max(per_sm, 1));
+      k_merge_rows<<<grid, MT2, smem, st>>>(cur, ld, M, pa.Mn, pa.goff, pa.gmem, pa.colsrc,
+                                            pa.cursor, W, next, key[p ^ 1]);
       ++*launches;
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
       cur = next;
       next = (next == matA) ? matB : matA;
-      ld = Mn;
+      ld = ((int64_t)Mn + 3) & ~3ll;  // padded leading dimension of the new matrix
+    }
+    if (trace) {
+      cudaEventRecord(tev[2], st);
+      cudaEventSynchronize(tev[2]);
+      float a = 0, b = 0;
+      cudaEventElapsedTime(&a, tev[0], tev[1]);
+      cudaEventElapsedTime(&b, tev[1], tev[2]);
+      std::fprintf(stderr, "[ragb linkage] round %d M=%d Mn=%d merges=%d prep=%.3fms merge=%.3fms\n",
+                   out->rounds, M, Mn, host_c[0] - prev_z, a, b);
+      prev_z = host_c[0];
     }
     p ^= 1;
     M = Mn;
   }
+  if (trace)
+    for (auto &x : tev) cudaEventDestroy(x);
   int nz = 0;
   if ((e = cudaMemcpyAsync(&nz, counters, sizeof(int), cudaMemcpyDeviceToHost, st)) != cudaSuccess)
     return e;

@@ -101,6 +101,8 @@ def canon_lib(tr):
     kids = [[] for _ in range(n)]
     for k in range(1, n):
         kids[parent[k]].append(k)
+    for kk in kids:  # children are ordered by rep (X12)
+        kk.sort(key=lambda x: int(tr["rep"][x]))
     out = {}
     stack = [(0, ())]
     while stack:
