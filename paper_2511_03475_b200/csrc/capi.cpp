@@ -4,6 +4,9 @@
 
 #include <algorithm>
 #include <chrono>
+#include <condition_variable>
+#include <mutex>
+#include <thread>
 #include <cstring>
 #include <new>
 #include <string>
@@ -268,11 +271,49 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
   RB_CUDA(cudaMemcpyAsync(keys.data(), da.nnkey + row0, nrows * 8, cudaMemcpyDeviceToHost, st),
           "D2H nn");
 
-  // ---- a5: linkage ---------------------------------------------------------
+  // ---- a5 (device) with the a6 replay pipelined on a host worker ------------
   ragb::LinkageOut lo;
+  ragb::TreeBuild T;
   if (linkage) {
-    RB_CUDA(ragb::run_linkage(rows_dev, N, da.nnkey, scratch_dev, L, keep_rows, st, &lo, &launches),
-            "linkage");
+    H.za.assign(N - 1, 0);
+    H.zb.assign(N - 1, 0);
+    H.zh.assign(N - 1, 0.0f);
+    H.zs.assign(N - 1, 0);
+    std::mutex mu;
+    std::condition_variable cv;
+    int64_t avail = 0;
+    bool finished = false;
+    std::thread worker([&] {
+      ragb::host_begin(H, T);  // sorted leaf sets overlap the device work
+      for (;;) {
+        int64_t upto;
+        bool fin;
+        {
+          std::unique_lock<std::mutex> lk(mu);
+          cv.wait(lk, [&] { return avail > T.done || finished; });
+          upto = avail;
+          fin = finished;
+        }
+        ragb::host_replay(H, T, upto);
+        if (!T.ok || (fin && T.done >= upto)) break;
+      }
+    });
+    const cudaError_t le = ragb::run_linkage(
+        rows_dev, N, da.nnkey, scratch_dev, L, keep_rows, st, H.za.data(), H.zb.data(),
+        H.zh.data(), H.zs.data(), &lo, &launches, [&](int64_t upto) {
+          {
+            std::lock_guard<std::mutex> lk(mu);
+            avail = upto;
+          }
+          cv.notify_one();
+        });
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      finished = true;
+    }
+    cv.notify_one();
+    worker.join();
+    if (le != cudaSuccess) return cleanup(cuda_fail(le, "linkage"));
   }
   RB_CUDA(cudaEventRecord(ev[3], st), "event");
   RB_CUDA(cudaStreamSynchronize(st), "sync");
@@ -302,12 +343,8 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
   // ---- a6-a7: tree, orders, schedule (host) --------------------------------
   if (linkage) {
     const auto th = clock::now();
-    H.za.swap(lo.a);
-    H.zb.swap(lo.b);
-    H.zh.swap(lo.h);
-    H.zs.swap(lo.size);
     std::string msg;
-    s = ragb::host_build(H, &msg);
+    s = ragb::host_finish(H, T, &msg);
     if (s != RB_OK) return cleanup(fail(s, "internal: " + msg));
     H.has_linkage = true;
     H.stats.host_ms = std::chrono::duration<float, std::milli>(clock::now() - th).count();

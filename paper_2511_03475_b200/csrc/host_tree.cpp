@@ -64,7 +64,108 @@ int host_threads() {
   return n;
 }
 
+// Incremental raw-tree state (see internal.h TreeBuild).
+void host_begin(HostIndex &H, TreeBuild &T) {
+  const int64_t N = H.N;
+  const int32_t K = H.K;
+  const bool uniform = H.lens.empty();
+  const int nth = host_threads();
+  // sorted leaf sets (parallel)
+  T.lset.resize((size_t)N * K);
+#pragma omp parallel for num_threads(nth) schedule(static)
+  for (int64_t i = 0; i < N; ++i) {
+    uint32_t *d = T.lset.data() + i * K;
+    const uint32_t *src = H.ids.data() + i * K;
+    const int L = uniform ? K : H.lens[i];
+    for (int k = 0; k < L; ++k) {  // insertion sort (K <= 255, typically 5-20)
+      const uint32_t x = src[k];
+      int q = k;
+      while (q > 0 && d[q - 1] > x) {
+        d[q] = d[q - 1];
+        --q;
+      }
+      d[q] = x;
+    }
+  }
+  const int64_t nz = std::max<int64_t>(N - 1, 0);
+  T.voff.assign(nz + 1, 0);
+  T.vpool.clear();
+  T.vpool.reserve((size_t)N * 4 + 64);
+  T.rchild.assign(2 * nz, 0);
+  T.cur.resize(N);
+  std::iota(T.cur.begin(), T.cur.end(), 0);
+  T.csize.assign(N, 1);
+  T.done = 0;
+  T.ok = true;
+}
+
+// Replay merges [T.done, upto) of H.za/zb/zs: any order in which every merge
+// follows the merges that built its two clusters (the device emits rounds).
+void host_replay(HostIndex &H, TreeBuild &T, int64_t upto) {
+  const int64_t N = H.N;
+  const int32_t K = H.K;
+  const bool uniform = H.lens.empty();
+  for (int64_t t = T.done; t < upto && T.ok; ++t) {
+    const int32_t a = H.za[t], b = H.zb[t];
+    if (a < 0 || b >= N || a >= b || T.cur[a] < 0 || T.cur[b] < 0 ||
+        T.csize[a] + T.csize[b] != H.zs[t]) {
+      T.ok = false;
+      T.err = "inconsistent merge at row " + std::to_string(t);
+      break;
+    }
+    const int32_t A = T.cur[a], B = T.cur[b];
+    T.rchild[2 * t] = A;
+    T.rchild[2 * t + 1] = B;
+    int la, lb;
+    const uint32_t *pa, *pb;
+    if (A < N) {
+      la = uniform ? K : H.lens[A];
+      pa = T.lset.data() + (int64_t)A * K;
+    } else {
+      la = (int)(T.voff[A - N + 1] - T.voff[A - N]);
+      pa = T.vpool.data() + T.voff[A - N];
+    }
+    if (B < N) {
+      lb = uniform ? K : H.lens[B];
+      pb = T.lset.data() + (int64_t)B * K;
+    } else {
+      lb = (int)(T.voff[B - N + 1] - T.voff[B - N]);
+      pb = T.vpool.data() + T.voff[B - N];
+    }
+    uint32_t tmp[256];
+    int n = 0, ia = 0, ib = 0;
+    while (ia < la && ib < lb) {  // sorted intersection (PAPER:335)
+      if (pa[ia] < pb[ib]) {
+        ++ia;
+      } else if (pb[ib] < pa[ia]) {
+        ++ib;
+      } else {
+        tmp[n++] = pa[ia];
+        ++ia;
+        ++ib;
+      }
+    }
+    T.vpool.insert(T.vpool.end(), tmp, tmp + n);
+    T.voff[t + 1] = (int64_t)T.vpool.size();
+    T.cur[a] = (int32_t)(N + t);
+    T.cur[b] = -1;
+    T.csize[a] += T.csize[b];
+    T.done = t + 1;
+  }
+}
+
 rb_status host_build(HostIndex &H, std::string *msg) {
+  if ((int64_t)H.za.size() != H.N - 1) {
+    *msg = "merge list must have N-1 rows";
+    return RB_EINVAL;
+  }
+  TreeBuild T;
+  host_begin(H, T);
+  host_replay(H, T, (int64_t)H.za.size());
+  return host_finish(H, T, msg);
+}
+
+rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg) {
   const int64_t N = H.N;
   const int32_t K = H.K;
   const bool uniform = H.lens.empty();
@@ -84,35 +185,15 @@ rb_status host_build(HostIndex &H, std::string *msg) {
     *msg = "merge list must have N-1 rows";
     return RB_EINVAL;
   }
-
-  // ---- sorted leaf sets (parallel) ----------------------------------------
-  std::vector<uint32_t> lset((size_t)N * K);
-#pragma omp parallel for num_threads(nth) schedule(static)
-  for (int64_t i = 0; i < N; ++i) {
-    uint32_t *d = lset.data() + i * K;
-    const uint32_t *s = H.ids.data() + i * K;
-    const int L = len_of(i);
-    for (int k = 0; k < L; ++k) {  // insertion sort (K <= 255, typically 5-20)
-      const uint32_t x = s[k];
-      int q = k;
-      while (q > 0 && d[q - 1] > x) {
-        d[q] = d[q - 1];
-        --q;
-      }
-      d[q] = x;
-    }
+  host_replay(H, T, nz);
+  if (!T.ok) {
+    *msg = T.err;
+    return RB_EINVAL;
   }
-  lap("leaf sets");
-
-  // ---- raw binary tree with intersection sets (replay) --------------------
-  // raw node r < N: leaf r (set in lset); r = N + t: merge t (set in pool)
-  std::vector<int64_t> voff(nz + 1, 0);
-  std::vector<uint32_t> vpool;
-  vpool.reserve((size_t)N * 4 + 64);
-  std::vector<int32_t> rchild(2 * std::max<int64_t>(nz, 0));
-  std::vector<int32_t> cur(N);
-  std::vector<int32_t> csize(N, 1);
-  std::iota(cur.begin(), cur.end(), 0);
+  const std::vector<uint32_t> &lset = T.lset;
+  const std::vector<int64_t> &voff = T.voff;
+  const std::vector<uint32_t> &vpool = T.vpool;
+  const std::vector<int32_t> &rchild = T.rchild;
   auto set_ptr = [&](int64_t r, int *n) -> const uint32_t * {
     if (r < N) {
       *n = len_of(r);
@@ -121,43 +202,12 @@ rb_status host_build(HostIndex &H, std::string *msg) {
     *n = (int)(voff[r - N + 1] - voff[r - N]);
     return vpool.data() + voff[r - N];
   };
-  for (int64_t t = 0; t < nz; ++t) {
-    const int32_t a = H.za[t], b = H.zb[t];
-    if (a < 0 || b >= N || a >= b || cur[a] < 0 || cur[b] < 0 || csize[a] + csize[b] != H.zs[t]) {
-      *msg = "inconsistent merge at row " + std::to_string(t);
-      return RB_EINVAL;
-    }
-    const int32_t A = cur[a], B = cur[b];
-    rchild[2 * t] = A;
-    rchild[2 * t + 1] = B;
-    int la, lb;
-    const uint32_t *pa = set_ptr(A, &la);
-    const uint32_t *pb = set_ptr(B, &lb);
-    uint32_t tmp[256];
-    int n = 0, ia = 0, ib = 0;
-    while (ia < la && ib < lb) {  // sorted intersection (PAPER:335)
-      if (pa[ia] < pb[ib]) {
-        ++ia;
-      } else if (pb[ib] < pa[ia]) {
-        ++ib;
-      } else {
-        tmp[n++] = pa[ia];
-        ++ia;
-        ++ib;
-      }
-    }
-    vpool.insert(vpool.end(), tmp, tmp + n);
-    voff[t + 1] = (int64_t)vpool.size();
-    cur[a] = (int32_t)(N + t);
-    cur[b] = -1;
-    csize[a] += csize[b];
-  }
-  const int64_t top = cur[0];
-  if (csize[0] != N) {
+  const int64_t top = T.cur[0];
+  if (T.csize[0] != N) {
     *msg = "merges do not join all contexts";
     return RB_EINVAL;
   }
-  lap("raw tree");
+  lap("replay tail");
 
   // ---- collapse (X11): DFS over the raw tree ------------------------------
   // kept virtual node k (1..V): raw node vraw[k-1], parent node id vpar[k-1].

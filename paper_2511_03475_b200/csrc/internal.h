@@ -5,6 +5,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -68,16 +69,18 @@ cudaError_t launch_validate(const uint32_t *ids, const uint8_t *lens, int64_t N,
 cudaError_t launch_distance(const DistArgs &a, cudaStream_t st, int *launches);
 
 struct LinkageOut {
-  std::vector<int32_t> a, b, size;
-  std::vector<float> h;
   int rounds = 0;
 };
 
 // a5: complete linkage on the full rows (rows ld = N) starting from the fused
-// row-NN keys; merges returned unsorted.
+// row-NN keys.  Merges are written to the host arrays za/zb/zh/zs ([N-1]) in a
+// dependency-respecting order, round by round; on_round(upto) is called after
+// each round with the number of merges available so far (used to pipeline the
+// host tree build with the device rounds; may be empty).
 cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void *scratch,
-                        const ScratchLayout &L, bool keep_rows, cudaStream_t st, LinkageOut *out,
-                        int *launches);
+                        const ScratchLayout &L, bool keep_rows, cudaStream_t st, int32_t *za,
+                        int32_t *zb, float *zh, int32_t *zs, LinkageOut *out, int *launches,
+                        const std::function<void(int64_t)> &on_round);
 
 // ----------------------------------------------------------------- host
 struct HostIndex {
@@ -111,5 +114,21 @@ struct HostIndex {
 // orders and schedule (a6-a7).  Returns RB_OK or RB_EINVAL with msg.
 rb_status host_build(HostIndex &H, std::string *msg);
 int host_threads();
+
+// Incremental raw-tree replay, so the host tree can be built while the device
+// is still running later linkage rounds.
+struct TreeBuild {
+  std::vector<uint32_t> lset;   // [N][K] sorted leaf sets
+  std::vector<int64_t> voff;    // [N] offsets of merge t's intersection set
+  std::vector<uint32_t> vpool;
+  std::vector<int32_t> rchild;  // [2(N-1)] raw children of merge t
+  std::vector<int32_t> cur, csize;
+  int64_t done = 0;
+  bool ok = true;
+  std::string err;
+};
+void host_begin(HostIndex &H, TreeBuild &T);
+void host_replay(HostIndex &H, TreeBuild &T, int64_t upto);
+rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg);
 
 }  // namespace ragb

@@ -28,6 +28,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <functional>
 
 #include "internal.h"
 
@@ -53,6 +54,7 @@ struct PrepArgs {
   int *newidx, *goff, *gmem, *colsrc /* colmap */, *cnt, *cursor /* then first_old */;
   int *rep_n, *sz_n;
   int *Mn;
+  int *level;  // [0] level list length, [1] h bits
 };
 
 struct BlockScratch {
@@ -104,7 +106,9 @@ __device__ int block_compact(int n, Pred pred, Val value, int *out, BlockScratch
   return base;
 }
 
-__global__ void __launch_bounds__(PT, 1) k_round_prep(PrepArgs a) {
+// Round step 1 (one CTA): h = min row key; RNN pairs above h (emitted); the
+// vertices whose row min equals h become the level list (ascending).
+__global__ void __launch_bounds__(PT, 1) k_prep_mark(PrepArgs a) {
   __shared__ BlockScratch S;
   const int tid = threadIdx.x;
   const int M = a.M;
@@ -143,52 +147,117 @@ __global__ void __launch_bounds__(PT, 1) k_round_prep(PrepArgs a) {
   }
   __syncthreads();
 
-  // -- 3. greedy clique contractions at height h (ascending vertex order) -----
+  // level list: vertices at h, ascending
   const uint8_t *alive = a.alive;
   const int nlist = block_compact(
       M, [&](int i) { return alive[i] != 0; }, [&](int i) { return i; }, a.list, S);
-  int sza = 0;
-  for (int li = 0; li < nlist; ++li) {
-    const int v = a.list[li];
-    if (!a.alive[v]) continue;  // absorbed by an earlier vertex (uniform branch)
-    // h-neighbours of v: only list vertices (row min == h) can be at h from v,
-    // and the list is ascending, so scanning its suffix keeps candidates sorted.
-    const float *rowv = a.D + (int64_t)v * a.ld;
-    const int *lst = a.list + li + 1;
-    int n = block_compact(
-        nlist - li - 1,
-        [&](int i) {
-          const int c = lst[i];
-          return a.alive[c] != 0 && rowv[c] == hf;
-        },
-        [&](int i) { return lst[i]; }, a.candA, S);
-    int *cin = a.candA, *cout = a.candB;
+  if (tid == 0) {
+    a.level[0] = nlist;
+    a.level[1] = (int)h;
+  }
+}
+
+// Round step 2 (grid): adjacency bits of the level graph, adj[i][w] bit j <=>
+// D[list[i]][list[32w + j]] == h (j != i).  One warp per word: 32 lanes read
+// 32 ascending columns of the same row.
+__global__ void k_level_adj(PrepArgs a, uint32_t *__restrict__ adj) {
+  const int n = a.level[0];
+  if (n < 2) return;
+  const float hf = __uint_as_float((unsigned)a.level[1]);
+  const int W = (n + 31) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t total = (int64_t)n * W;
+  for (int64_t q = gw; q < total; q += nw) {
+    const int i = (int)(q / W), w = (int)(q - (int64_t)i * W);
+    const int j = w * 32 + lane;
+    bool bit = false;
+    if (j < n && j != i) bit = __ldg(a.D + (int64_t)a.list[i] * a.ld + a.list[j]) == hf;
+    const unsigned word = __ballot_sync(0xffffffffu, bit);
+    if (lane == 0) adj[q] = word;
+  }
+}
+
+// Round step 3 (one CTA): greedy clique contractions at height h.  At the
+// current minimum height the greedy algorithm takes the smallest vertex with
+// an h-neighbour and absorbs its smallest h-neighbour; the merged cluster stays
+// at h only from vertices at h from both (max(h, h') = h iff h' = h), so the
+// candidate set shrinks by intersection; then the next vertex.  Candidate and
+// alive sets are bitsets over list positions; each step is one AND pass over
+// an adjacency row plus a block-wide find-first.
+__global__ void __launch_bounds__(PT, 1) k_level_cliques(PrepArgs a,
+                                                         const uint32_t *__restrict__ adj) {
+  extern __shared__ uint32_t bits[];  // [2][W]: alive, candidates
+  __shared__ int s_first[PT / 32];
+  __shared__ int s_b;
+  const int n = a.level[0];
+  if (n < 2) return;
+  const float hf = __uint_as_float((unsigned)a.level[1]);
+  const int W = (n + 31) >> 5;
+  uint32_t *A = bits, *C = bits + W;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int w = tid; w < W; w += PT) {
+    const int rem = n - w * 32;
+    A[w] = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
+  }
+  __syncthreads();
+  int sza = 0;  // thread 0: running size of the current clique
+  // block-wide: C[w] = f(w) for w >= w0, returns the first set bit position (or n)
+  auto pass = [&](int w0, auto f) {
+    int first = 0x7fffffff;
+    for (int w = w0 + tid; w < W; w += PT) {
+      const uint32_t c = f(w);
+      C[w] = c;
+      if (c && first == 0x7fffffff) first = w * 32 + __ffs(c) - 1;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+    if (lane == 0) s_first[wid] = first;
+    __syncthreads();
+    if (tid == 0) {
+      int m = s_first[0];
+      for (int i = 1; i < PT / 32; ++i) m = min(m, s_first[i]);
+      s_b = m;
+    }
+    __syncthreads();
+    return s_b;
+  };
+  for (int ia = 0; ia < n; ++ia) {
+    if (!((A[ia >> 5] >> (ia & 31)) & 1u)) continue;  // absorbed earlier (uniform)
+    const int v = a.list[ia];
+    const int w0 = ia >> 5;
+    const uint32_t gt = (ia & 31) == 31 ? 0u : (0xffffffffu << ((ia & 31) + 1));
+    const uint32_t *row = adj + (int64_t)ia * W;
+    int b = pass(w0, [&](int w) { return __ldg(row + w) & A[w] & (w == w0 ? gt : 0xffffffffu); });
     if (tid == 0) sza = a.sz[v];
-    while (n > 0) {
-      const int b = cin[0];
+    while (b < 0x7fffffff) {
+      const int vb = a.list[b];
       if (tid == 0) {
-        sza += a.sz[b];
+        sza += a.sz[vb];
         const int pos = atomicAdd(a.zcount, 1);
         a.za[pos] = a.rep[v];
-        a.zb[pos] = a.rep[b];
+        a.zb[pos] = a.rep[vb];
         a.zh[pos] = hf;
         a.zs[pos] = sza;
-        a.leader[b] = v;
-        a.alive[b] = 0;
+        a.leader[vb] = v;
+        A[b >> 5] &= ~(1u << (b & 31));
       }
-      const float *rowb = a.D + (int64_t)b * a.ld;
-      const int *cc = cin;
-      n = block_compact(
-          n - 1, [&](int i) { return rowb[cc[1 + i]] == hf; }, [&](int i) { return cc[1 + i]; },
-          cout, S);
-      int *t = cin;
-      cin = cout;
-      cout = t;
+      const uint32_t *rb = adj + (int64_t)b * W;
+      const int wb = b >> 5;
+      // candidates before b are already excluded (b is the first set bit)
+      b = pass(wb, [&](int w) { return C[w] & __ldg(rb + w) & (w == wb ? ~(0xffffffffu >> (31 - (b & 31))) : 0xffffffffu); });
     }
-    if (tid == 0) a.alive[v] = 0;
+    if (tid == 0) A[w0] &= ~(1u << (ia & 31));
     __syncthreads();
   }
+}
 
+// Round step 4 (one CTA): order-preserving compaction map and group CSR.
+__global__ void __launch_bounds__(PT, 1) k_prep_compact(PrepArgs a) {
+  __shared__ BlockScratch S;
+  const int tid = threadIdx.x;
+  const int M = a.M;
   // -- 4. compaction map: new index of every survivor (order preserving) ------
   int base = 0;
   for (int c0 = 0; c0 < M; c0 += PT) {
@@ -343,12 +412,9 @@ T *at(void *base, size_t off) {
 }  // namespace
 
 cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void *scratch,
-                        const ScratchLayout &L, bool keep_rows, cudaStream_t st, LinkageOut *out,
-                        int *launches) {
-  out->a.clear();
-  out->b.clear();
-  out->h.clear();
-  out->size.clear();
+                        const ScratchLayout &L, bool keep_rows, cudaStream_t st, int32_t *za,
+                        int32_t *zb, float *zh, int32_t *zs, LinkageOut *out, int *launches,
+                        const std::function<void(int64_t)> &on_round) {
   out->rounds = 0;
   if (N <= 1) return cudaSuccess;
   int dev = 0, sms = 0;
@@ -384,6 +450,7 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
   pa.zh = at<float>(scratch, L.zh);
   pa.zcount = counters;
   pa.Mn = counters + 1;
+  pa.level = counters + 2;
 
   const float *cur = rows;
   int64_t ld = N;
@@ -396,6 +463,7 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
   if (trace)
     for (auto &x : tev) cudaEventCreate(&x);
   int prev_z = 0;
+  int zdone = 0;
   while (M > 1) {
     if (trace) cudaEventRecord(tev[0], st);
     pa.D = cur;
@@ -406,8 +474,17 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
     pa.sz = sz[p];
     pa.rep_n = rep[p ^ 1];
     pa.sz_n = sz[p ^ 1];
-    k_round_prep<<<1, PT, 0, st>>>(pa);
-    ++*launches;
+    k_prep_mark<<<1, PT, 0, st>>>(pa);
+    uint32_t *adj = reinterpret_cast<uint32_t *>(next);  // free until the merge writes it
+    k_level_adj<<<sms * 4, 256, 0, st>>>(pa, adj);
+    {
+      const size_t smem = 2 * (size_t)((M + 31) / 32) * 4;
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k_level_cliques, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      k_level_cliques<<<1, PT, smem, st>>>(pa, adj);
+    }
+    k_prep_compact<<<1, PT, 0, st>>>(pa);
+    *launches += 4;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (trace) cudaEventRecord(tev[1], st);
     int host_c[2];
@@ -416,6 +493,22 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
       return e;
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
     ++out->rounds;
+    {  // this round's merges to the host, then let the host tree catch up
+      const int z0 = zdone, z1 = host_c[0];
+      if (z1 > (int)N - 1 || z1 < z0) return cudaErrorUnknown;
+      if (z1 > z0) {
+        const size_t n = (size_t)(z1 - z0);
+        cudaMemcpyAsync(za + z0, pa.za + z0, n * 4, cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(zb + z0, pa.zb + z0, n * 4, cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(zh + z0, pa.zh + z0, n * 4, cudaMemcpyDeviceToHost, st);
+        if ((e = cudaMemcpyAsync(zs + z0, pa.zs + z0, n * 4, cudaMemcpyDeviceToHost, st)) !=
+            cudaSuccess)
+          return e;
+        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+        zdone = z1;
+        if (on_round) on_round(zdone);
+      }
+    }
     const int Mn = host_c[1];
     if (Mn >= M || Mn < 1) return cudaErrorUnknown;  // no progress: invariant violated
     if (Mn > 1) {
@@ -450,20 +543,8 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
   }
   if (trace)
     for (auto &x : tev) cudaEventDestroy(x);
-  int nz = 0;
-  if ((e = cudaMemcpyAsync(&nz, counters, sizeof(int), cudaMemcpyDeviceToHost, st)) != cudaSuccess)
-    return e;
-  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
-  if (nz != N - 1) return cudaErrorUnknown;
-  out->a.resize(nz);
-  out->b.resize(nz);
-  out->h.resize(nz);
-  out->size.resize(nz);
-  cudaMemcpyAsync(out->a.data(), pa.za, nz * sizeof(int), cudaMemcpyDeviceToHost, st);
-  cudaMemcpyAsync(out->b.data(), pa.zb, nz * sizeof(int), cudaMemcpyDeviceToHost, st);
-  cudaMemcpyAsync(out->h.data(), pa.zh, nz * sizeof(float), cudaMemcpyDeviceToHost, st);
-  cudaMemcpyAsync(out->size.data(), pa.zs, nz * sizeof(int), cudaMemcpyDeviceToHost, st);
-  return cudaStreamSynchronize(st);
+  if (zdone != N - 1) return cudaErrorUnknown;
+  return cudaSuccess;
 }
 
 }  // namespace ragb
