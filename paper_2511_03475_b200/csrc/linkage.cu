@@ -184,13 +184,13 @@ __global__ void k_level_adj(PrepArgs a, uint32_t *__restrict__ adj) {
 // an h-neighbour and absorbs its smallest h-neighbour; the merged cluster stays
 // at h only from vertices at h from both (max(h, h') = h iff h' = h), so the
 // candidate set shrinks by intersection; then the next vertex.  Candidate and
-// alive sets are bitsets over list positions; each step is one AND pass over
-// an adjacency row plus a block-wide find-first.
+// alive sets are bitsets over list positions in shared memory; each step is
+// one AND pass over an adjacency row (one word per thread) plus a block-wide
+// find-first with a single barrier (double-buffered warp minima).
 __global__ void __launch_bounds__(PT, 1) k_level_cliques(PrepArgs a,
                                                          const uint32_t *__restrict__ adj) {
   extern __shared__ uint32_t bits[];  // [2][W]: alive, candidates
-  __shared__ int s_first[PT / 32];
-  __shared__ int s_b;
+  __shared__ int s_first[2][PT / 32];
   const int n = a.level[0];
   if (n < 2) return;
   const float hf = __uint_as_float((unsigned)a.level[1]);
@@ -202,8 +202,8 @@ __global__ void __launch_bounds__(PT, 1) k_level_cliques(PrepArgs a,
     A[w] = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
   }
   __syncthreads();
-  int sza = 0;  // thread 0: running size of the current clique
-  // block-wide: C[w] = f(w) for w >= w0, returns the first set bit position (or n)
+  int parity = 0;
+  // C[w] = f(w) for w >= w0; returns the first set bit position (or INT_MAX)
   auto pass = [&](int w0, auto f) {
     int first = 0x7fffffff;
     for (int w = w0 + tid; w < W; w += PT) {
@@ -213,16 +213,15 @@ __global__ void __launch_bounds__(PT, 1) k_level_cliques(PrepArgs a,
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
-    if (lane == 0) s_first[wid] = first;
+    if (lane == 0) s_first[parity][wid] = first;
     __syncthreads();
-    if (tid == 0) {
-      int m = s_first[0];
-      for (int i = 1; i < PT / 32; ++i) m = min(m, s_first[i]);
-      s_b = m;
-    }
-    __syncthreads();
-    return s_b;
+    int m = s_first[parity][lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+    parity ^= 1;
+    return m;
   };
+  int sza = 0;
   for (int ia = 0; ia < n; ++ia) {
     if (!((A[ia >> 5] >> (ia & 31)) & 1u)) continue;  // absorbed earlier (uniform)
     const int v = a.list[ia];
@@ -230,25 +229,27 @@ __global__ void __launch_bounds__(PT, 1) k_level_cliques(PrepArgs a,
     const uint32_t gt = (ia & 31) == 31 ? 0u : (0xffffffffu << ((ia & 31) + 1));
     const uint32_t *row = adj + (int64_t)ia * W;
     int b = pass(w0, [&](int w) { return __ldg(row + w) & A[w] & (w == w0 ? gt : 0xffffffffu); });
-    if (tid == 0) sza = a.sz[v];
+    sza = a.sz[v];
     while (b < 0x7fffffff) {
       const int vb = a.list[b];
+      sza += a.sz[vb];
       if (tid == 0) {
-        sza += a.sz[vb];
         const int pos = atomicAdd(a.zcount, 1);
         a.za[pos] = a.rep[v];
         a.zb[pos] = a.rep[vb];
         a.zh[pos] = hf;
         a.zs[pos] = sza;
         a.leader[vb] = v;
-        A[b >> 5] &= ~(1u << (b & 31));
       }
-      const uint32_t *rb = adj + (int64_t)b * W;
+      // the thread owning word b/32 clears b's alive bit before the next pass reads it
       const int wb = b >> 5;
-      // candidates before b are already excluded (b is the first set bit)
-      b = pass(wb, [&](int w) { return C[w] & __ldg(rb + w) & (w == wb ? ~(0xffffffffu >> (31 - (b & 31))) : 0xffffffffu); });
+      if (tid == wb % PT) A[wb] &= ~(1u << (b & 31));
+      const uint32_t *rb = adj + (int64_t)b * W;
+      const uint32_t above = (b & 31) == 31 ? 0u : (0xffffffffu << ((b & 31) + 1));
+      // candidates up to b are already excluded (b was the first set bit)
+      b = pass(wb, [&](int w) { return C[w] & __ldg(rb + w) & (w == wb ? above : 0xffffffffu); });
     }
-    if (tid == 0) A[w0] &= ~(1u << (ia & 31));
+    if (tid == w0 % PT) A[w0] &= ~(1u << (ia & 31));
     __syncthreads();
   }
 }
