@@ -244,7 +244,7 @@ def run_ours(args, ws, rank, local):
     dist_bytes = 4.0 * N * N + 4.0 * N * K   # full fp32 rows written + ids read (algorithmic)
     dist_gbs = dist_bytes / (mean["distance_ms"] * 1e-3) / 1e9
     traffic = load_traffic(args.config)
-    roofline = {"kernel": "k_dist_rows_nn (a2-a4)", "bound": "hbm", "achieved": dist_gbs, "peak": hbm,
+    roofline = {"kernel": "k_dist_tile (a2-a4, distance rows + fused row NN)", "bound": "hbm", "achieved": dist_gbs, "peak": hbm,
                 "unit": "GB/s", "frac": dist_gbs / hbm, "traffic": traffic, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": dist_bytes,
                 "share_of_step": mean["distance_ms"] / ms}
