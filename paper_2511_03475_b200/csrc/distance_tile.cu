@@ -33,11 +33,10 @@ constexpr int NW = NT / 32;    // warps per CTA
 constexpr int CPT = 2;         // columns per thread per chunk
 constexpr int CH = NT * CPT;   // columns per chunk
 constexpr int R = 32;          // rows per tile
-constexpr int QCAP = 384;      // queue entries per warp
 constexpr int FWORDS = 2048;   // filter words (65536 bits)
 
 struct Plan {
-  int T, logT, shift, lutEntries;
+  int T, logT, shift, lutEntries, qcap;
   size_t off_acc, off_key, off_mask, off_base, off_slot, off_plist, off_filter, off_qdoc, off_qmeta,
       off_red, off_wsum, off_lut, total;
 };
@@ -54,8 +53,7 @@ __global__ void __launch_bounds__(NT, 2) k_dist_tile(DistArgs a, Plan P) {
   uint16_t *slot = reinterpret_cast<uint16_t *>(smem + P.off_slot);   // [R*K]
   uint8_t *plist = smem + P.off_plist;                                // [R*K]
   uint32_t *filt = reinterpret_cast<uint32_t *>(smem + P.off_filter); // [FWORDS]
-  uint32_t *qdoc = reinterpret_cast<uint32_t *>(smem + P.off_qdoc);   // [NW][QCAP]
-  uint32_t *qmeta = reinterpret_cast<uint32_t *>(smem + P.off_qmeta); // [NW][QCAP]
+  uint16_t *qent = reinterpret_cast<uint16_t *>(smem + P.off_qdoc);   // [NW][qcap]
   unsigned long long *red = reinterpret_cast<unsigned long long *>(smem + P.off_red);  // [NW][R]
   int *wsum = reinterpret_cast<int *>(smem + P.off_wsum);
   float *slut = reinterpret_cast<float *>(smem + P.off_lut);
@@ -67,9 +65,6 @@ __global__ void __launch_bounds__(NT, 2) k_dist_tile(DistArgs a, Plan P) {
   const float *lut = LUT_SMEM ? slut : a.lut;
   if (LUT_SMEM)
     for (int i = tid; i < P.lutEntries; i += NT) slut[i] = a.lut[i];
-  uint32_t *myq_doc = qdoc + warp * QCAP;
-  uint32_t *myq_meta = qmeta + warp * QCAP;
-  const unsigned lt_mask = (1u << lane) - 1u;
   const bool even_n = (N & 1) == 0;
 
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -126,19 +121,50 @@ __global__ void __launch_bounds__(NT, 2) k_dist_tile(DistArgs a, Plan P) {
       bj[r] = 0xffffffffu;
     }
 
+    uint16_t *myq = qent + warp * P.qcap;
     for (int64_t c0 = 0; c0 < N; c0 += CH) {
       const int64_t jb = c0 + (int64_t)tid * CPT;
       const uint32_t *colp = a.idsT + jb;
-      int qn = 0;  // warp-uniform queue length
 
-      // drain: all 32 lanes process queued (doc, k, column) candidates
-      auto drain = [&]() {
+      // ---- probe: filter every column doc, keep candidate bits per column --
+      uint32_t cm0 = 0u, cm1 = 0u;  // bit k: doc k of column 0 / 1 may be in the tile
+#pragma unroll 4
+      for (int k = 0; k < K; ++k) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2 *>(colp + (int64_t)k * Npad));
+        const uint32_t f0 = hash_filter(v.x), f1 = hash_filter(v.y);
+        cm0 |= ((filt[f0 >> 5] >> (f0 & 31)) & 1u) << k;
+        cm1 |= ((filt[f1 >> 5] >> (f1 & 31)) & 1u) << k;
+      }
+      // ---- compact candidates into the warp queue (entry = k << 9 | column)
+      {
+        const int n = __popc(cm0) + __popc(cm1);
+        int x = n;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        const int qn = __shfl_sync(0xffffffffu, x, 31);
+        int pos = x - n;
+        const uint32_t col0 = (uint32_t)(tid * CPT);
+        while (cm0) {
+          const int k = __ffs(cm0) - 1;
+          cm0 &= cm0 - 1u;
+          myq[pos++] = (uint16_t)((k << 9) | col0);
+        }
+        while (cm1) {
+          const int k = __ffs(cm1) - 1;
+          cm1 &= cm1 - 1u;
+          myq[pos++] = (uint16_t)((k << 9) | (col0 + 1u));
+        }
         __syncwarp();
+        // ---- drain: all 32 lanes process the warp's candidates -------------
         for (int base = 0; base < qn; base += 32) {
           const int i = base + lane;
-          const uint32_t doc = i < qn ? myq_doc[i] : kReservedDoc;
-          const uint32_t meta = i < qn ? myq_meta[i] : 0u;
-          const int k = (int)(meta >> 16), col = (int)(meta & 0xffffu);
+          const uint32_t e = i < qn ? myq[i] : 0u;
+          const int k = (int)(e >> 9), col = (int)(e & 511u);
+          const uint32_t doc =
+              i < qn ? __ldg(a.idsT + (int64_t)k * Npad + (c0 + col)) : kReservedDoc;
           uint32_t h = hash_slot(doc, logT);
           uint32_t key = tkey[h];
           while (key != doc && key != kReservedDoc) {
@@ -158,77 +184,66 @@ __global__ void __launch_bounds__(NT, 2) k_dist_tile(DistArgs a, Plan P) {
           }
         }
         __syncwarp();
-        qn = 0;
-      };
-
-#pragma unroll 2
-      for (int k = 0; k < K; ++k) {
-        const uint2 v = __ldg(reinterpret_cast<const uint2 *>(colp + (int64_t)k * Npad));
-        const uint32_t f0 = hash_filter(v.x), f1 = hash_filter(v.y);
-        const bool h0 = (filt[f0 >> 5] >> (f0 & 31)) & 1u;
-        const bool h1 = (filt[f1 >> 5] >> (f1 & 31)) & 1u;
-        const unsigned b0 = __ballot_sync(0xffffffffu, h0);
-        const unsigned b1 = __ballot_sync(0xffffffffu, h1);
-        const int n0 = __popc(b0);
-        const uint32_t colb = (uint32_t)(tid * CPT) & 0xffffu;
-        if (h0) {
-          const int pos = qn + __popc(b0 & lt_mask);
-          myq_doc[pos] = v.x;
-          myq_meta[pos] = ((uint32_t)k << 16) | colb;
-        }
-        if (h1) {
-          const int pos = qn + n0 + __popc(b1 & lt_mask);
-          myq_doc[pos] = v.y;
-          myq_meta[pos] = ((uint32_t)k << 16) | (colb + 1u);
-        }
-        qn += n0 + __popc(b1);
-        if (qn > QCAP - 64) drain();
       }
-      drain();
 
       // ---- finalize: d = table[packed (s, D)], stores, row min in registers
       const bool vec_ok = even_n && (c0 + (int64_t)(warp + 1) * 32 * CPT <= N);
       const bool special = (c0 < r0 + R && r0 < c0 + CH) || (c0 + CH > N);
       const uint32_t j0 = (uint32_t)jb, j1 = (uint32_t)jb + 1u;
+      float *orow = a.rows + (r0 - a.row0) * N + jb;
+      uint32_t *ap = accw + tid;
+      if (!special && vec_ok && !COUNTS) {
+        // common case: no diagonal, no tail, aligned stores
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        if (r < rcount) {
-          const uint32_t w = accw[r * NT + tid];
-          accw[r * NT + tid] = 0u;
-          const uint32_t p0 = w & 0xffffu, p1 = w >> 16;
-          const float d0 = LUT_SMEM ? lut[p0] : __ldg(lut + p0);
-          const float d1 = LUT_SMEM ? lut[p1] : __ldg(lut + p1);
-          const int64_t gi = r0 + r;
-          float *orow = a.rows + (gi - a.row0) * N;
-          if (vec_ok) {
-            __stcs(reinterpret_cast<float2 *>(orow + jb), make_float2(d0, d1));
-          } else {
-            if (jb < N) __stcs(orow + jb, d0);
-            if (jb + 1 < N) __stcs(orow + jb + 1, d1);
+        for (int r = 0; r < R; ++r) {
+          if (r < rcount) {
+            const uint32_t w = ap[r * NT];
+            ap[r * NT] = 0u;
+            const float d0 = LUT_SMEM ? lut[w & 0xffffu] : __ldg(lut + (w & 0xffffu));
+            const float d1 = LUT_SMEM ? lut[w >> 16] : __ldg(lut + (w >> 16));
+            __stcs(reinterpret_cast<float2 *>(orow + (int64_t)r * N), make_float2(d0, d1));
+            // strict '<' keeps the smallest column among equal distances (X8)
+            const float m = fminf(d0, d1);
+            const bool u = m < bv[r];
+            bj[r] = u ? (d0 <= d1 ? j0 : j1) : bj[r];
+            bv[r] = u ? m : bv[r];
           }
-          if (COUNTS) {
-            if (jb < N) {
-              a.s_out[(gi - a.row0) * N + jb] = (uint8_t)(p0 >> SHIFT);
-              a.D_out[(gi - a.row0) * N + jb] = (uint16_t)(p0 & DMASK);
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (r < rcount) {
+            const uint32_t w = ap[r * NT];
+            ap[r * NT] = 0u;
+            const uint32_t p0 = w & 0xffffu, p1 = w >> 16;
+            const float d0 = LUT_SMEM ? lut[p0] : __ldg(lut + p0);
+            const float d1 = LUT_SMEM ? lut[p1] : __ldg(lut + p1);
+            const int64_t gi = r0 + r;
+            float *o = orow + (int64_t)r * N;
+            if (vec_ok) {
+              __stcs(reinterpret_cast<float2 *>(o), make_float2(d0, d1));
+            } else {
+              if (jb < N) __stcs(o, d0);
+              if (jb + 1 < N) __stcs(o + 1, d1);
             }
-            if (jb + 1 < N) {
-              a.s_out[(gi - a.row0) * N + jb + 1] = (uint8_t)(p1 >> SHIFT);
-              a.D_out[(gi - a.row0) * N + jb + 1] = (uint16_t)(p1 & DMASK);
+            if (COUNTS) {
+              if (jb < N) {
+                a.s_out[(gi - a.row0) * N + jb] = (uint8_t)(p0 >> SHIFT);
+                a.D_out[(gi - a.row0) * N + jb] = (uint16_t)(p0 & DMASK);
+              }
+              if (jb + 1 < N) {
+                a.s_out[(gi - a.row0) * N + jb + 1] = (uint8_t)(p1 >> SHIFT);
+                a.D_out[(gi - a.row0) * N + jb + 1] = (uint16_t)(p1 & DMASK);
+              }
             }
-          }
-          float e0 = d0, e1 = d1;
-          if (special) {
             const float inf = __int_as_float(0x7f800000);
-            e0 = (jb < N && jb != gi) ? d0 : inf;
-            e1 = (jb + 1 < N && jb + 1 != gi) ? d1 : inf;
+            const float e0 = (jb < N && jb != gi) ? d0 : inf;
+            const float e1 = (jb + 1 < N && jb + 1 != gi) ? d1 : inf;
+            const float m = fminf(e0, e1);
+            const bool u = m < bv[r];
+            bj[r] = u ? (e0 <= e1 ? j0 : j1) : bj[r];
+            bv[r] = u ? m : bv[r];
           }
-          // strict '<' keeps the smallest column among equal distances (X8)
-          const bool u0 = e0 < bv[r];
-          bv[r] = u0 ? e0 : bv[r];
-          bj[r] = u0 ? j0 : bj[r];
-          const bool u1 = e1 < bv[r];
-          bv[r] = u1 ? e1 : bv[r];
-          bj[r] = u1 ? j1 : bj[r];
         }
       }
     }
@@ -280,8 +295,9 @@ Plan plan(int K, int shift, int lutSmemEntries) {
   P.off_slot = take((size_t)R * K * 2, 16);
   P.off_plist = take((size_t)R * K, 16);
   P.off_filter = take((size_t)FWORDS * 4, 16);
-  P.off_qdoc = take((size_t)NW * QCAP * 4, 16);
-  P.off_qmeta = take((size_t)NW * QCAP * 4, 16);
+  P.qcap = 32 * CPT * K;  // every (lane, column, k) can be a candidate
+  P.off_qdoc = take((size_t)NW * P.qcap * 2, 16);
+  P.off_qmeta = P.off_qdoc;
   P.off_red = take((size_t)NW * R * 8, 16);
   P.off_wsum = take(32 * 4, 16);
   P.off_lut = take((size_t)lutSmemEntries * 4, 16);

@@ -310,6 +310,7 @@ __global__ void __launch_bounds__(PT, 1) k_prep_compact(PrepArgs a) {
     a.colsrc[x] = g;
     if (l == x) a.cursor[g] = x;  // cursor is free after the scatter: first_old
   }
+  if (tid < 4) a.colsrc[M + tid] = -1;  // padding for 16-byte colmap loads
 }
 
 // Fused merge + compaction + row min (complete linkage, X7):
@@ -323,63 +324,121 @@ __global__ void __launch_bounds__(PT, 1) k_prep_compact(PrepArgs a) {
 // window are done in several windows; a window starting at new column T0 only
 // needs old columns >= first_old[T0] (members of later groups are never
 // smaller than their leader).
-constexpr int MT2 = 1024;
 
-__global__ void __launch_bounds__(MT2) k_merge_rows(const float *__restrict__ D, int64_t ld, int M,
+// VEC: 16-byte loads of 4 consecutive old columns (old row stride and base are
+// multiples of 4 floats: every compacted matrix; the original rows when N % 4
+// == 0); colmap is padded with -1 to a multiple of 4.
+template <bool VEC, int NTH>
+__global__ void __launch_bounds__(NTH) k_merge_rows(const float *__restrict__ D, int64_t ld, int M,
                                                     const int *__restrict__ Mn_p,
                                                     const int *__restrict__ goff,
                                                     const int *__restrict__ gmem,
                                                     const int *__restrict__ colmap,
                                                     const int *__restrict__ first_old, int W,
                                                     float *__restrict__ Dn, u64 *__restrict__ keyn) {
-  extern __shared__ __align__(16) int win[];  // [W] float bits
-  __shared__ u64 wmin[MT2 / 32];
+  extern __shared__ __align__(16) int win[];  // [W] float bits (d >= 0: int order == float order)
+  __shared__ u64 wmin[NTH / 32];
   const int Mn = *Mn_p;
   const int64_t ldn = (Mn + 3) & ~3;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   for (int c = blockIdx.x; c < Mn; c += gridDim.x) {
     const int rb = goff[c], re = goff[c + 1];
-    const float *row0 = D + (int64_t)gmem[rb] * ld;
-    u64 best = ~0ull;
+    const float *__restrict__ row0 = D + (int64_t)gmem[rb] * ld;
+    int bval = 0x7fffffff, bidx = 0x7fffffff;  // running (value bits, column) minimum
     for (int T0 = 0; T0 < Mn; T0 += W) {
       const int Wn = min(W, Mn - T0);
-      for (int i = tid; i < Wn; i += MT2) win[i] = 0;
+      for (int i = tid * 4; i < Wn; i += NTH * 4) *reinterpret_cast<int4 *>(win + i) = int4{0, 0, 0, 0};
       __syncthreads();
-      const int s0 = T0 == 0 ? 0 : first_old[T0];
-      // 4 independent (colmap, value) load pairs in flight per thread
-      constexpr int U = 4;
-      for (int sb = s0; sb < M; sb += U * MT2) {
-        int t[U];
-        float v[U];
+      const int s0 = T0 == 0 ? 0 : (first_old[T0] & ~3);
+      if (VEC) {
+        const float4 *__restrict__ r4 = reinterpret_cast<const float4 *>(row0);
+        const int4 *__restrict__ c4 = reinterpret_cast<const int4 *>(colmap);
+        constexpr int UV = 2;
+        for (int qb = (s0 >> 2) + tid; qb * 4 < M; qb += NTH * UV) {
+          int4 t4[UV];
+          float4 v4[UV];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int s = sb + u * MT2 + tid;
-          t[u] = s < M ? __ldg(colmap + s) - T0 : -1;
-          v[u] = s < M ? __ldcs(row0 + s) : 0.0f;
-        }
-        for (int rr = rb + 1; rr < re; ++rr) {
-          const float *rowk = D + (int64_t)gmem[rr] * ld;
+          for (int u = 0; u < UV; ++u) {
+            const int q = qb + u * NTH;
+            const bool ok = q * 4 < M;
+            t4[u] = ok ? __ldg(c4 + q) : int4{-1, -1, -1, -1};
+            v4[u] = ok ? __ldcs(r4 + q) : float4{0, 0, 0, 0};
+          }
+          for (int rr = rb + 1; rr < re; ++rr) {  // other row members (max)
+            const float4 *__restrict__ k4 = reinterpret_cast<const float4 *>(D + (int64_t)gmem[rr] * ld);
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int s = sb + u * MT2 + tid;
-            if (s < M) v[u] = fmaxf(v[u], __ldcs(rowk + s));
+            for (int u = 0; u < UV; ++u) {
+              const int q = qb + u * NTH;
+              if (q * 4 < M) {
+                const float4 x = __ldcs(k4 + q);
+                v4[u].x = fmaxf(v4[u].x, x.x);
+                v4[u].y = fmaxf(v4[u].y, x.y);
+                v4[u].z = fmaxf(v4[u].z, x.z);
+                v4[u].w = fmaxf(v4[u].w, x.w);
+              }
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < UV; ++u) {
+            const int tt[4] = {t4[u].x - T0, t4[u].y - T0, t4[u].z - T0, t4[u].w - T0};
+            const float vv[4] = {v4[u].x, v4[u].y, v4[u].z, v4[u].w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              if ((unsigned)tt[k] < (unsigned)Wn) atomicMax(win + tt[k], __float_as_int(vv[k]));
           }
         }
+      } else {
+        constexpr int U = 4;
+        for (int sb = s0; sb < M; sb += U * NTH) {
+          int t[U];
+          float v[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (t[u] >= 0 && t[u] < Wn) atomicMax(win + t[u], __float_as_int(v[u]));
+          for (int u = 0; u < U; ++u) {
+            const int s = sb + u * NTH + tid;
+            t[u] = s < M ? __ldg(colmap + s) - T0 : -1;
+            v[u] = s < M ? __ldcs(row0 + s) : 0.0f;
+          }
+          for (int rr = rb + 1; rr < re; ++rr) {
+            const float *rowk = D + (int64_t)gmem[rr] * ld;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const int s = sb + u * NTH + tid;
+              if (s < M) v[u] = fmaxf(v[u], __ldcs(rowk + s));
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if ((unsigned)t[u] < (unsigned)Wn) atomicMax(win + t[u], __float_as_int(v[u]));
+        }
       }
       __syncthreads();
-      float *out = Dn + (int64_t)c * ldn + T0;
-      for (int i = tid; i < Wn; i += MT2) {
-        const int t = T0 + i;
-        const float v = t == c ? 0.0f : __int_as_float(win[i]);
-        __stcs(out + i, v);
-        const u64 key = ((u64)__float_as_uint(v) << 32) | (unsigned)t;
-        best = (t != c && key < best) ? key : best;
+      // write out (16-byte stores; the new leading dimension is a multiple of 4)
+      float4 *__restrict__ out4 = reinterpret_cast<float4 *>(Dn + (int64_t)c * ldn + T0);
+      const int cd = c - T0;  // diagonal position inside the window
+      for (int i = tid * 4; i < Wn; i += NTH * 4) {
+        int4 q = *reinterpret_cast<const int4 *>(win + i);
+        // diagonal -> 0 in the matrix, excluded from the row minimum
+        const int4 qm = {(i == cd || i >= Wn) ? 0x7fffffff : q.x,
+                         (i + 1 == cd || i + 1 >= Wn) ? 0x7fffffff : q.y,
+                         (i + 2 == cd || i + 2 >= Wn) ? 0x7fffffff : q.z,
+                         (i + 3 == cd || i + 3 >= Wn) ? 0x7fffffff : q.w};
+        if ((unsigned)(cd - i) < 4u) {
+          q.x = i == cd ? 0 : q.x;
+          q.y = i + 1 == cd ? 0 : q.y;
+          q.z = i + 2 == cd ? 0 : q.z;
+          q.w = i + 3 == cd ? 0 : q.w;
+        }
+        __stcs(out4 + (i >> 2), make_float4(__int_as_float(q.x), __int_as_float(q.y),
+                                            __int_as_float(q.z), __int_as_float(q.w)));
+        const int m4 = min(min(qm.x, qm.y), min(qm.z, qm.w));
+        if (m4 < bval) {  // strict: the earliest column wins among equal values (X8)
+          bval = m4;
+          bidx = T0 + i + (qm.x == m4 ? 0 : qm.y == m4 ? 1 : qm.z == m4 ? 2 : 3);
+        }
       }
       __syncthreads();
     }
+    u64 best = bval == 0x7fffffff ? ~0ull : (((u64)(unsigned)bval << 32) | (unsigned)bidx);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const u64 y = __shfl_xor_sync(0xffffffffu, best, o);
@@ -390,7 +449,7 @@ __global__ void __launch_bounds__(MT2) k_merge_rows(const float *__restrict__ D,
     if (tid == 0) {
       u64 b = wmin[0];
 #pragma unroll
-      for (int i = 1; i < MT2 / 32; ++i) b = wmin[i] < b ? wmin[i] : b;
+      for (int i = 1; i < NTH / 32; ++i) b = wmin[i] < b ? wmin[i] : b;
       keyn[c] = b;
     }
     __syncthreads();
@@ -513,16 +572,23 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
     const int Mn = host_c[1];
     if (Mn >= M || Mn < 1) return cudaErrorUnknown;  // no progress: invariant violated
     if (Mn > 1) {
-      // window: the whole new row if it fits in shared memory, else pieces
-      const int maxW = 56 * 1024;
+      // window: the whole new row if it fits in shared memory, else pieces.
+      // Wide rows: 1024-thread CTAs, one per SM; narrow rows: 256-thread CTAs
+      // so that several rows are in flight per SM (per-row latency dominates).
+      const bool vec = (ld & 3) == 0 && (reinterpret_cast<uintptr_t>(cur) & 15) == 0;
+      const bool wide = Mn > 20 * 1024;
+      const int maxW = wide ? 56 * 1024 : 20 * 1024;
       const int W = std::min<int>((Mn + 3) & ~3, maxW);
       const size_t smem = (size_t)W * 4;
-      cudaFuncSetAttribute(k_merge_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      const int nth = wide ? 1024 : 256;
+      auto kern = wide ? (vec ? k_merge_rows<true, 1024> : k_merge_rows<false, 1024>)
+                       : (vec ? k_merge_rows<true, 256> : k_merge_rows<false, 256>);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       int per_sm = 1;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_merge_rows, MT2, smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nth, smem);
       const int grid = std::min<int>(Mn, sms * std::max(per_sm, 1));
-      k_merge_rows<<<grid, MT2, smem, st>>>(cur, ld, M, pa.Mn, pa.goff, pa.gmem, pa.colsrc,
-                                            pa.cursor, W, next, key[p ^ 1]);
+      kern<<<grid, nth, smem, st>>>(cur, ld, M, pa.Mn, pa.goff, pa.gmem, pa.colsrc, pa.cursor, W, next,
+                                    key[p ^ 1]);
       ++*launches;
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
       cur = next;
