@@ -45,13 +45,16 @@ template <int SHIFT, bool LUT_SMEM, bool COUNTS>
 __global__ void __launch_bounds__(NT, 2) k_dist_tile(DistArgs a, Plan P) {
   constexpr uint32_t DMASK = (1u << SHIFT) - 1u;
   constexpr uint32_t INC = 1u << SHIFT;
+  // SHIFT == 8: accumulate 4 x (s << 8 | D), the byte offset of d(s, D) in the
+  // table (max 4 * (22 << 8 | 242) < 2^16); SHIFT == 10: the index itself.
+  constexpr uint32_t ISCALE = SHIFT == 8 ? 4u : 1u;
   extern __shared__ __align__(16) unsigned char smem[];
   uint32_t *accw = reinterpret_cast<uint32_t *>(smem + P.off_acc);    // [R][NT] packed 2 x u16
   uint32_t *tkey = reinterpret_cast<uint32_t *>(smem + P.off_key);    // [T]
   uint32_t *tmask = reinterpret_cast<uint32_t *>(smem + P.off_mask);  // [T]
   uint16_t *tbase = reinterpret_cast<uint16_t *>(smem + P.off_base);  // [T]
   uint16_t *slot = reinterpret_cast<uint16_t *>(smem + P.off_slot);   // [R*K]
-  uint8_t *plist = smem + P.off_plist;                                // [R*K]
+  uint16_t *plist = reinterpret_cast<uint16_t *>(smem + P.off_plist);  // [R*K] (row << 8 | pos)
   uint32_t *filt = reinterpret_cast<uint32_t *>(smem + P.off_filter); // [FWORDS]
   uint16_t *qent = reinterpret_cast<uint16_t *>(smem + P.off_qdoc);   // [NW][qcap]
   unsigned long long *red = reinterpret_cast<unsigned long long *>(smem + P.off_red);  // [NW][R]
@@ -109,7 +112,7 @@ __global__ void __launch_bounds__(NT, 2) k_dist_tile(DistArgs a, Plan P) {
     for (int it = tid; it < rcount * K; it += NT) {
       const int r = it / K, k = it - r * K;
       const int h = slot[it];
-      plist[tbase[h] + __popc(tmask[h] & ((1u << r) - 1u))] = (uint8_t)k;
+      plist[tbase[h] + __popc(tmask[h] & ((1u << r) - 1u))] = (uint16_t)((r << 8) | k);
     }
     __syncthreads();
 
@@ -158,29 +161,38 @@ __global__ void __launch_bounds__(NT, 2) k_dist_tile(DistArgs a, Plan P) {
           myq[pos++] = (uint16_t)((k << 9) | (col0 + 1u));
         }
         __syncwarp();
-        // ---- drain: all 32 lanes process the warp's candidates -------------
-        for (int base = 0; base < qn; base += 32) {
-          const int i = base + lane;
-          const uint32_t e = i < qn ? myq[i] : 0u;
-          const int k = (int)(e >> 9), col = (int)(e & 511u);
-          const uint32_t doc =
-              i < qn ? __ldg(a.idsT + (int64_t)k * Npad + (c0 + col)) : kReservedDoc;
-          uint32_t h = hash_slot(doc, logT);
-          uint32_t key = tkey[h];
-          while (key != doc && key != kReservedDoc) {
-            h = (h + 1) & (T - 1);
-            key = tkey[h];
+        // ---- drain: all 32 lanes process the warp's candidates; the doc
+        // reloads of DB consecutive rounds are issued together (latency)
+        constexpr int DB = 4;
+        for (int base = 0; base < qn; base += 32 * DB) {
+          uint32_t doc[DB], ent[DB];
+#pragma unroll
+          for (int u = 0; u < DB; ++u) {
+            const int i = base + u * 32 + lane;
+            ent[u] = i < qn ? myq[i] : 0xffffffffu;
+            const int k = (int)(ent[u] >> 9), col = (int)(ent[u] & 511u);
+            doc[u] = i < qn ? __ldg(a.idsT + (int64_t)k * Npad + (c0 + col)) : kReservedDoc;
           }
-          uint32_t m = key == doc ? tmask[h] : 0u;
-          int idx = tbase[h];
-          const uint32_t sh = (uint32_t)(col & 1) * 16u;
-          uint32_t *wp = accw + (col >> 1);
-          while (m) {
-            const int r = __ffs(m) - 1;
-            m &= m - 1u;
-            const int pr = plist[idx++];
-            const uint32_t dp = (uint32_t)(pr > k ? pr - k : k - pr);
-            atomicAdd(wp + r * NT, (INC + dp) << sh);
+#pragma unroll
+          for (int u = 0; u < DB; ++u) {
+            const int k = (int)((ent[u] >> 9) & 31u), col = (int)(ent[u] & 511u);
+            const uint32_t d = doc[u];
+            uint32_t h = hash_slot(d, logT);
+            uint32_t key = tkey[h];
+            while (key != d && key != kReservedDoc) {
+              h = (h + 1) & (T - 1);
+              key = tkey[h];
+            }
+            const int cnt = key == d ? __popc(tmask[h]) : 0;
+            const int idx0 = tbase[h];
+            const uint32_t sh = (uint32_t)(col & 1) * 16u;
+            uint32_t *wp = accw + (col >> 1);
+            for (int z = 0; z < cnt; ++z) {  // rows of the tile holding this doc
+              const uint32_t e = plist[idx0 + z];
+              const int pr = (int)(e & 0xffu);
+              const uint32_t dp = (uint32_t)(pr > k ? pr - k : k - pr);
+              atomicAdd(wp + (e >> 8) * NT, ((INC + dp) * ISCALE) << sh);
+            }
           }
         }
         __syncwarp();
@@ -192,22 +204,30 @@ __global__ void __launch_bounds__(NT, 2) k_dist_tile(DistArgs a, Plan P) {
       const uint32_t j0 = (uint32_t)jb, j1 = (uint32_t)jb + 1u;
       float *orow = a.rows + (r0 - a.row0) * N + jb;
       uint32_t *ap = accw + tid;
-      if (!special && vec_ok && !COUNTS) {
-        // common case: no diagonal, no tail, aligned stores
+      if (!special && vec_ok && !COUNTS && rcount == R) {
+        // common case: full tile, no diagonal, no tail, aligned stores
+        const char *lutb = reinterpret_cast<const char *>(lut);
+        float2 *o = reinterpret_cast<float2 *>(orow);
+        const int64_t step = N / 2;  // float2 units per row (N even here)
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          if (r < rcount) {
-            const uint32_t w = ap[r * NT];
-            ap[r * NT] = 0u;
-            const float d0 = LUT_SMEM ? lut[w & 0xffffu] : __ldg(lut + (w & 0xffffu));
-            const float d1 = LUT_SMEM ? lut[w >> 16] : __ldg(lut + (w >> 16));
-            __stcs(reinterpret_cast<float2 *>(orow + (int64_t)r * N), make_float2(d0, d1));
-            // strict '<' keeps the smallest column among equal distances (X8)
-            const float m = fminf(d0, d1);
-            const bool u = m < bv[r];
-            bj[r] = u ? (d0 <= d1 ? j0 : j1) : bj[r];
-            bv[r] = u ? m : bv[r];
+          const uint32_t w = ap[r * NT];
+          ap[r * NT] = 0u;
+          float d0, d1;
+          if (SHIFT == 8 && LUT_SMEM) {
+            d0 = *reinterpret_cast<const float *>(lutb + (w & 0xffffu));
+            d1 = *reinterpret_cast<const float *>(lutb + (w >> 16));
+          } else {
+            d0 = LUT_SMEM ? lut[(w & 0xffffu) / ISCALE] : __ldg(lut + (w & 0xffffu) / ISCALE);
+            d1 = LUT_SMEM ? lut[(w >> 16) / ISCALE] : __ldg(lut + (w >> 16) / ISCALE);
           }
+          __stcs(o, make_float2(d0, d1));
+          o += step;
+          // strict '<' keeps the smallest column among equal distances (X8)
+          const float m = fminf(d0, d1);
+          const bool u = m < bv[r];
+          bj[r] = u ? (d0 <= d1 ? j0 : j1) : bj[r];
+          bv[r] = u ? m : bv[r];
         }
       } else {
 #pragma unroll
@@ -215,7 +235,7 @@ __global__ void __launch_bounds__(NT, 2) k_dist_tile(DistArgs a, Plan P) {
           if (r < rcount) {
             const uint32_t w = ap[r * NT];
             ap[r * NT] = 0u;
-            const uint32_t p0 = w & 0xffffu, p1 = w >> 16;
+            const uint32_t p0 = (w & 0xffffu) / ISCALE, p1 = (w >> 16) / ISCALE;
             const float d0 = LUT_SMEM ? lut[p0] : __ldg(lut + p0);
             const float d1 = LUT_SMEM ? lut[p1] : __ldg(lut + p1);
             const int64_t gi = r0 + r;
@@ -293,7 +313,7 @@ Plan plan(int K, int shift, int lutSmemEntries) {
   P.off_mask = take((size_t)T * 4, 16);
   P.off_base = take((size_t)T * 2, 16);
   P.off_slot = take((size_t)R * K * 2, 16);
-  P.off_plist = take((size_t)R * K, 16);
+  P.off_plist = take((size_t)R * K * 2, 16);
   P.off_filter = take((size_t)FWORDS * 4, 16);
   P.qcap = 32 * CPT * K;  // every (lane, column, k) can be a candidate
   P.off_qdoc = take((size_t)NW * P.qcap * 2, 16);
