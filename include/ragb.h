@@ -189,18 +189,29 @@ RB_API rb_status rb_index_tree(const rb_index *idx, int32_t *parent, int32_t *le
                                int64_t *prefix_off, uint32_t *prefix_ids, int64_t *path_off,
                                int32_t *path);
 
-/* Context ordering + schedule for the indexed set:
- * ids must be NULL (the indexed contexts, offline mode).  out_ids[M][K]
- * (host): matched prefix then remaining docs in original order; slots past
- * the context length are copied from the input unchanged.  out_prefix_len[M]:
- * length of the inherited prefix.  out_schedule[M]: execution order (input
- * indices): groups by first path element in order of first appearance,
- * path length descending, ties by index (X14).  Any output may be NULL.
- * Errors: RB_EINVAL, RB_ESTATE (online ordering of new contexts is not built
- * yet: ids != NULL). */
+/* Context ordering + schedule (Section 5.1
+ * Section 5.2).
+ * ids == NULL (offline): the indexed contexts; M must equal the number of
+ *   indexed contexts (rb_index_size).  out_ids[M][K] (host): matched prefix
+ *   then remaining docs in original order; slots past a context's length are
+ *   copied from the input unchanged.  out_prefix_len[M]: inherited prefix
+ *   length.  out_schedule[M]: execution order over all indexed contexts.
+ * ids != NULL (online, NEXT-1): M new contexts (host [M][K], lens host [M] or
+ *   NULL) are searched and inserted one after the other (PAPER:371-384:
+ *   greedy descent by minimum Eq. 1 distance against each child's ordered
+ *   context, stop at a leaf or when all eligible children are equidistant;
+ *   readings X15, X20, X21), then ordered; out_schedule is the Section 5.2
+ *   schedule of the batch (indices 0..M-1).  The new contexts become indexed
+ *   contexts N, N+1, ... (rb_index_tree / rb_session_open see them).
+ * Any output may be NULL.  Errors: RB_EINVAL (K or M mismatch, bad length,
+ * reserved DocId), RB_EDUPDOC, RB_ESTATE (linkage skipped). */
 RB_API rb_status rb_order_contexts(rb_index *idx, const uint32_t *ids, const uint8_t *lens, int64_t M,
                                    int32_t K, uint32_t *out_ids, uint8_t *out_prefix_len,
                                    int64_t *out_schedule);
+
+/* Set the Eq. 1 alpha used by online ordering (an index built from a merge
+ * list defaults to 1/200, X1).  Errors: RB_EALPHA. */
+RB_API rb_status rb_index_set_alpha(rb_index *idx, uint32_t alpha_num, uint32_t alpha_den);
 
 /* Open a multi-turn session whose turn 0 is indexed context `row`: the
  * session follows the leaf's stored search path to the first-turn context

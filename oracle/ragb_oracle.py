@@ -411,3 +411,131 @@ def build_index(ids, lens=None, alpha=Fraction(1, 200)):
     sched = schedule(t.path)
     return dict(S=S, D=Dm, d=d, nn_idx=nn_idx, nn_d=nn_d, Z=Z, tree=t, ordered=ordered,
                 prefix_len=plen, schedule=sched)
+
+
+# ------------------------------------------------------------------- NEXT-1
+class OnlineIndex:
+    """NEXT-1: context search, insert and ordering of new
+    contexts against a built index (Section 4.2; PAPER:425-436,
+    Section 5.1), sequential over a batch (SPEC order_batch).
+
+    Search ("greedily descending from the root, selecting at each
+    level the child with the minimum distance ... stops upon reaching a leaf or
+    when all children are equidistant"), with reading X15: distances are the
+    canonical fp32 Eq. 1 values against each child's ordered context; eligible
+    children share at least one doc with the query, and a virtual child must be
+    contained in the query (so every node on the path is a prefix of it,
+    X20); key (d, is_leaf, child index); stop when no child is eligible or when
+    two or more children are eligible and all share the same (d, is_leaf);
+    otherwise descend into the minimum key (a sole eligible child is always
+    descended).
+
+    Insert ("matching an internal node appends the new context as a
+    child, while matching a leaf creates a new internal node with their
+    intersection"), reading X21: a leaf match L under parent P creates a virtual
+    node V with set(L) ∩ set(Q) in L's place (children L, Q) when that
+    intersection extends set(P); otherwise Q becomes a child of P.  V's ordered
+    context is P's followed by the shared docs in L's existing order (L was
+    already served in that order), and L's ordered context is re-derived under
+    V (unchanged when Q contains L).  The new context's order is the matched
+    node's ordered prefix followed by its remaining docs in retrieval order
+    (PAPER:431)."""
+
+    def __init__(self, ctxs, t: Tree, alpha: Fraction):
+        self.alpha = alpha
+        self.children = [list(c) for c in t.children]
+        self.parent = list(t.parent)
+        self.docset = [frozenset(s) for s in t.docset]
+        self.ordered = [list(o) for o in t.ordered]
+        self.leaf_of = list(t.leaf_of)
+        self.docs = [list(c) for c in ctxs]
+        self.leaf_node = list(t.leaf_node)
+
+    def _is_leaf(self, k):
+        return self.leaf_of[k] >= 0
+
+    def _new_node(self, parent, docset, ordered, leaf):
+        k = len(self.parent)
+        self.parent.append(parent)
+        self.children.append([])
+        self.docset.append(frozenset(docset))
+        self.ordered.append(list(ordered))
+        self.leaf_of.append(leaf)
+        return k
+
+    def search(self, q):
+        node, path = 0, []
+        qs = set(q)
+        while not self._is_leaf(node):
+            cands = []
+            for idx, c in enumerate(self.children[node]):
+                s, _ = overlap(q, self.ordered[c])
+                if s == 0:
+                    continue
+                if not self._is_leaf(c) and not self.docset[c] <= qs:
+                    continue
+                cands.append((distance(q, self.ordered[c], self.alpha), self._is_leaf(c), idx, c))
+            if not cands:
+                break
+            if len(cands) >= 2 and all((x[0], x[1]) == (cands[0][0], cands[0][1]) for x in cands):
+                break
+            best = min(cands, key=lambda x: (x[0], x[1], x[2]))
+            path.append(best[2])
+            node = best[3]
+        return node, path
+
+    def order(self, q):
+        """Search + insert one context; returns (ordered docs, prefix length, path)."""
+        q = [int(x) for x in q]
+        node, path = self.search(q)
+        ctx = len(self.docs)
+        self.docs.append(q)
+        if not self._is_leaf(node):
+            parent = node
+        else:
+            L = node
+            P = self.parent[L]
+            inter = set(self.docs[self.leaf_of[L]]) & set(q)
+            if inter == set(self.docset[P]):
+                parent = P
+                path = path[:-1]
+            else:
+                # V keeps L's (already served) order for the shared docs
+                base = len(self.ordered[P])
+                V = self._new_node(P, inter, self.ordered[P] + [x for x in self.ordered[L][base:] if x in inter], -1)
+                pos = self.children[P].index(L)
+                self.children[P][pos] = V
+                self.children[V] = [L]
+                self.parent[L] = V
+                self.ordered[L] = self.ordered[V] + [x for x in self.ordered[L][base:] if x not in inter]
+                parent = V
+        pset = self.docset[parent]
+        ordq = self.ordered[parent] + [x for x in q if x not in pset]
+        k = self._new_node(parent, set(q), ordq, ctx)
+        self.children[parent].append(k)
+        self.leaf_node.append(k)
+        return ordq, len(self.ordered[parent]), self.path_of(ctx)
+
+    def path_of(self, ctx):
+        k = self.leaf_node[ctx]
+        p = []
+        while self.parent[k] != -1:
+            par = self.parent[k]
+            p.append(self.children[par].index(k))
+            k = par
+        return p[::-1]
+
+    def order_batch(self, batch):
+        """Sequential search + insert of a batch (earlier insertions are visible
+        to later items, SPEC order_batch), then the Section 5.2 schedule of the
+        batch's paths."""
+        out = [self.order(q) for q in batch]
+        paths = [self.path_of(len(self.docs) - len(batch) + i) for i in range(len(batch))]
+        return [o for o, _, _ in out], [p for _, p, _ in out], paths, schedule(paths)
+
+
+def traverse_online(idx: OnlineIndex, path):
+    k = 0
+    for step in path:
+        k = idx.children[k][step]
+    return k

@@ -174,6 +174,8 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
   HostIndex &H = idx->H;
   H.N = N;
   H.K = K;
+  H.alpha_num = p->alpha_num;
+  H.alpha_den = p->alpha_den;
   int launches = 0;
   cudaError_t e;
   cudaEvent_t ev[4];
@@ -424,7 +426,7 @@ rb_status rb_index_from_linkage(const uint32_t *ids_host, const uint8_t *lens_ho
 
 rb_status rb_index_size(const rb_index *idx, int64_t *N, int32_t *K) {
   if (!idx) return fail(RB_EINVAL, "NULL index");
-  if (N) *N = idx->H.N;
+  if (N) *N = idx->H.dyn ? ragb::dyn_contexts(idx->H) : idx->H.N;
   if (K) *K = idx->H.K;
   return RB_OK;
 }
@@ -463,6 +465,12 @@ rb_status rb_index_tree_info(const rb_index *idx, int64_t *n_nodes, int64_t *pre
   if (!idx) return fail(RB_EINVAL, "NULL index");
   const HostIndex &H = idx->H;
   if (!H.has_linkage) return fail(RB_ESTATE, "linkage was skipped");
+  if (H.dyn) {
+    if (n_nodes) *n_nodes = ragb::dyn_nodes(H);
+    ragb::dyn_export(H, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, prefix_total,
+                     path_total);
+    return RB_OK;
+  }
   if (n_nodes) *n_nodes = node_count(H);
   if (prefix_total) {
     int64_t t = H.vpre_off[H.V + 1];
@@ -479,6 +487,10 @@ rb_status rb_index_tree(const rb_index *idx, int32_t *parent, int32_t *leaf, int
   if (!idx) return fail(RB_EINVAL, "NULL index");
   const HostIndex &H = idx->H;
   if (!H.has_linkage) return fail(RB_ESTATE, "linkage was skipped");
+  if (H.dyn) {
+    ragb::dyn_export(H, parent, leaf, rep, prefix_off, prefix_ids, path_off, path, nullptr, nullptr);
+    return RB_OK;
+  }
   const int64_t V = H.V, N = H.N, K = H.K;
   if (parent) {
     parent[0] = -1;
@@ -518,15 +530,36 @@ rb_status rb_index_tree(const rb_index *idx, int32_t *parent, int32_t *leaf, int
 rb_status rb_order_contexts(rb_index *idx, const uint32_t *ids, const uint8_t *lens, int64_t M,
                             int32_t K, uint32_t *out_ids, uint8_t *out_prefix_len,
                             int64_t *out_schedule) {
-  (void)lens;
   if (!idx) return fail(RB_EINVAL, "NULL index");
-  const HostIndex &H = idx->H;
-  if (ids) return fail(RB_ESTATE, "online ordering of new contexts is not built yet");
+  HostIndex &H = idx->H;
   if (!H.has_linkage) return fail(RB_ESTATE, "linkage was skipped");
-  if (M != H.N || K != H.K) return fail(RB_EINVAL, "M/K must match the index");
+  if (K != H.K) return fail(RB_EINVAL, "K must match the index");
+  if (ids) {  // online: search + insert + order the new contexts (NEXT-1)
+    if (M < 1) return fail(RB_EINVAL, "M must be >= 1");
+    std::string msg;
+    const rb_status s = ragb::online_order(H, ids, lens, M, K, H.alpha_num, H.alpha_den, out_ids,
+                                           out_prefix_len, out_schedule, &msg);
+    if (s != RB_OK) return fail(s, msg);
+    return RB_OK;
+  }
+  if (H.dyn) {
+    if (M != ragb::dyn_contexts(H)) return fail(RB_EINVAL, "M must match the indexed contexts");
+    ragb::dyn_order_all(H, out_ids, out_prefix_len, out_schedule);
+    return RB_OK;
+  }
+  if (M != H.N) return fail(RB_EINVAL, "M must match the indexed contexts");
   if (out_ids) std::memcpy(out_ids, H.ordered.data(), H.ordered.size() * 4);
   if (out_prefix_len) std::memcpy(out_prefix_len, H.prefix_len.data(), H.prefix_len.size());
   if (out_schedule) std::memcpy(out_schedule, H.schedule.data(), H.schedule.size() * 8);
+  return RB_OK;
+}
+
+rb_status rb_index_set_alpha(rb_index *idx, uint32_t alpha_num, uint32_t alpha_den) {
+  if (!idx) return fail(RB_EINVAL, "NULL index");
+  if (alpha_den == 0 || alpha_den > 1000 || alpha_num > alpha_den)
+    return fail(RB_EALPHA, "alpha must be num/den with 1 <= den <= 1000, num <= den");
+  idx->H.alpha_num = alpha_num;
+  idx->H.alpha_den = alpha_den;
   return RB_OK;
 }
 
@@ -548,6 +581,11 @@ rb_status rb_session_open(const rb_index *idx, int64_t row, rb_session **out) {
   if (!idx || !out) return fail(RB_EINVAL, "NULL argument");
   const HostIndex &H = idx->H;
   if (!H.has_linkage) return fail(RB_ESTATE, "linkage was skipped");
+  if (H.dyn) {
+    if (row < 0 || row >= ragb::dyn_contexts(H)) return fail(RB_EPATH, "row out of range");
+    const auto &o = ragb::dyn_ordered(H, row);
+    return session_from_docs(o.data(), (int32_t)o.size(), out);
+  }
   if (row < 0 || row >= H.N) return fail(RB_EPATH, "row out of range");
   // follow the stored search path from the root
   int64_t node = 0;

@@ -6,6 +6,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <functional>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -83,6 +84,8 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
                         const std::function<void(int64_t)> &on_round);
 
 // ----------------------------------------------------------------- host
+struct DynTree;  // online (mutable) form of the tree, online.cpp
+
 struct HostIndex {
   int64_t N = 0;
   int32_t K = 0;
@@ -108,7 +111,22 @@ struct HostIndex {
   std::vector<uint8_t> prefix_len;  // [N]
   std::vector<int64_t> schedule;    // [N]
   rb_stats stats{};
+  uint32_t alpha_num = 1, alpha_den = 200;  // Eq. 1 alpha of the build (X1)
+  std::shared_ptr<DynTree> dyn;             // set by the first online update
 };
+
+// NEXT-1: online search + insert + ordering of M new contexts (online.cpp).
+rb_status online_order(HostIndex &H, const uint32_t *ids, const uint8_t *lens, int64_t M, int32_t K,
+                       uint32_t an, uint32_t ad, uint32_t *out_ids, uint8_t *out_prefix_len,
+                       int64_t *out_schedule, std::string *msg);
+int64_t dyn_contexts(const HostIndex &H);
+int64_t dyn_nodes(const HostIndex &H);
+void dyn_export(const HostIndex &H, int32_t *parent, int32_t *leaf, int32_t *rep, int64_t *prefix_off,
+                uint32_t *prefix_ids, int64_t *path_off, int32_t *path, int64_t *prefix_total,
+                int64_t *path_total);
+const std::vector<uint32_t> &dyn_ordered(const HostIndex &H, int64_t ctx);
+void dyn_order_all(const HostIndex &H, uint32_t *out_ids, uint8_t *out_prefix_len,
+                   int64_t *out_schedule);
 
 // Sort merges into greedy key order (X9) and validate them; builds tree,
 // orders and schedule (a6-a7).  Returns RB_OK or RB_EINVAL with msg.

@@ -29,6 +29,7 @@ EXPORTED = [
     "rb_build_index_host", "rb_index_from_linkage", "rb_index_size", "rb_index_stats", "rb_index_nn",
     "rb_index_linkage", "rb_index_tree_info", "rb_index_tree", "rb_order_contexts", "rb_session_open",
     "rb_session_open_docs", "rb_dedup_turn", "rb_session_turn", "rb_session_free", "rb_index_free",
+    "rb_index_set_alpha",
 ]
 
 
@@ -83,6 +84,7 @@ def lib():
         "rb_index_tree_info": ([P, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)], i32),
         "rb_index_tree": ([P, P, P, P, P, P, P, P], i32),
         "rb_order_contexts": ([P, P, P, i64, i32, P, P, P], i32),
+        "rb_index_set_alpha": ([P, u32, u32], i32),
         "rb_session_open": ([P, i64, PP], i32),
         "rb_session_open_docs": ([P, i32, PP], i32),
         "rb_dedup_turn": ([P, P, i32, P, ctypes.POINTER(i32), P, P, ctypes.POINTER(i32)], i32),
@@ -177,24 +179,47 @@ class Index:
         parent, leaf, rep = (np.empty(n, dtype=np.int32) for _ in range(3))
         poff = np.empty(n + 1, dtype=np.int64)
         pids = np.empty(pt.value, dtype=np.uint32)
-        qoff = np.empty(self.N + 1, dtype=np.int64)
+        qoff = np.empty(self.size() + 1, dtype=np.int64)
         path = np.empty(qt.value, dtype=np.int32)
         _check(lib().rb_index_tree(self._h, _np_ptr(parent), _np_ptr(leaf), _np_ptr(rep), _np_ptr(poff),
                                    _np_ptr(pids), _np_ptr(qoff), _np_ptr(path)))
         return dict(parent=parent, leaf=leaf, rep=rep, prefix_off=poff, prefix_ids=pids,
                     path_off=qoff, path=path)
 
+    def size(self) -> int:
+        n, k = ctypes.c_int64(), ctypes.c_int32()
+        _check(lib().rb_index_size(self._h, ctypes.byref(n), ctypes.byref(k)))
+        return n.value
+
     def paths(self):
         t = self.tree()
         o, p = t["path_off"], t["path"]
-        return [p[o[i]:o[i + 1]].tolist() for i in range(self.N)]
+        return [p[o[i]:o[i + 1]].tolist() for i in range(len(o) - 1)]
+
+    def set_alpha(self, alpha):
+        an, ad = alpha_rational(alpha)
+        _check(lib().rb_index_set_alpha(self._h, an, ad))
+
+    def order_new(self, ids, lens=None):
+        """NEXT-1: search + insert + order new contexts (host [M, K]); returns
+        (ordered [M, K], prefix_len [M], schedule [M])."""
+        ids = np.ascontiguousarray(ids, dtype=np.uint32)
+        M, K = ids.shape
+        lens_a = None if lens is None else np.ascontiguousarray(lens, dtype=np.uint8)
+        out = np.empty((M, K), dtype=np.uint32)
+        plen = np.empty(M, dtype=np.uint8)
+        sched = np.empty(M, dtype=np.int64)
+        _check(lib().rb_order_contexts(self._h, _np_ptr(ids), _np_ptr(lens_a), M, K, _np_ptr(out),
+                                       _np_ptr(plen), _np_ptr(sched)))
+        return out, plen, sched
 
     def order_contexts(self):
         """Offline prefix-first ordering + schedule of the indexed set."""
-        out = np.empty((self.N, self.K), dtype=np.uint32)
-        plen = np.empty(self.N, dtype=np.uint8)
-        sched = np.empty(self.N, dtype=np.int64)
-        _check(lib().rb_order_contexts(self._h, None, None, self.N, self.K, _np_ptr(out), _np_ptr(plen),
+        n = self.size()
+        out = np.empty((n, self.K), dtype=np.uint32)
+        plen = np.empty(n, dtype=np.uint8)
+        sched = np.empty(n, dtype=np.int64)
+        _check(lib().rb_order_contexts(self._h, None, None, n, self.K, _np_ptr(out), _np_ptr(plen),
                                        _np_ptr(sched)))
         return out, plen, sched
 
