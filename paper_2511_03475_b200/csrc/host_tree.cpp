@@ -23,8 +23,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
-#include <parallel/algorithm>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "internal.h"
@@ -59,7 +59,10 @@ inline bool in_sorted(const uint32_t *s, int n, uint32_t x) {
 int host_threads() {
   static int n = [] {
     if (const char *e = std::getenv("RAGB_HOST_THREADS")) return std::max(1, std::atoi(e));
-    return std::max(1, std::min(16, omp_get_num_procs()));
+    // one core is left to the side sorter / CUDA driver thread: a static OpenMP
+    // schedule with one oversubscribed core stalls every barrier (measured:
+    // 15 threads 8 ms, 16 threads 14-20 ms on a 16-core host at C4)
+    return std::max(1, std::min(15, omp_get_num_procs() - 1));
   }();
   return n;
 }
@@ -209,51 +212,66 @@ rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg) {
   }
   lap("replay tail");
 
-  // ---- collapse (X11): DFS over the raw tree ------------------------------
-  // kept virtual node k (1..V): raw node vraw[k-1], parent node id vpar[k-1].
+  // ---- exported merge order: ascending key (X9), sorted on a side thread
+  //      while the tree is built (the tree reads the replay order) ---------
+  std::vector<MergeKey> zk(nz);
+  std::thread sorter([&] {
+    for (int64_t t = 0; t < nz; ++t) zk[t] = {H.zh[t], H.za[t], H.zb[t], H.zs[t]};
+    std::sort(zk.begin(), zk.end(), key_less);
+  });
+
+  // ---- collapse (X11) -----------------------------------------------------
+  // A raw node is collapsed iff its set equals its raw parent's set (the root
+  // set is empty): the nearest kept ancestor of a collapsed node has the same
+  // set as its raw parent, by induction.  Flags in parallel, then one
+  // top-down pass (parents have larger merge index) numbers the kept nodes
+  // 1..V in decreasing merge index, so every parent precedes its children.
   std::vector<int64_t> vraw;
   std::vector<int32_t> vpar;
   vraw.reserve(nz);
   vpar.reserve(nz);
   H.lparent.assign(N, 0);
   {
-    struct Item {
-      int64_t raw;
-      int32_t kept_parent;
-      int64_t eff;  // raw node holding the effective parent set (-1: empty root set)
-    };
-    std::vector<Item> st;
-    st.reserve(64);
-    st.push_back({top, 0, -1});
-    while (!st.empty()) {
-      const Item it = st.back();
-      st.pop_back();
-      if (it.raw < N) {
-        H.lparent[it.raw] = it.kept_parent;
-        continue;
-      }
+    std::vector<int64_t> rpar(N + nz, -1);
+#pragma omp parallel for num_threads(nth) schedule(static)
+    for (int64_t t = 0; t < nz; ++t) {
+      rpar[rchild[2 * t]] = N + t;
+      rpar[rchild[2 * t + 1]] = N + t;
+    }
+    std::vector<uint8_t> keep(nz);
+#pragma omp parallel for num_threads(nth) schedule(static)
+    for (int64_t t = 0; t < nz; ++t) {
       int n1, n2;
-      const uint32_t *s1 = set_ptr(it.raw, &n1);
+      const uint32_t *s1 = set_ptr(N + t, &n1);
+      const int64_t p = rpar[N + t];
       bool same;
-      if (it.eff < 0) {
+      if (p < 0) {
         same = n1 == 0;
       } else {
-        const uint32_t *s2 = set_ptr(it.eff, &n2);
+        const uint32_t *s2 = set_ptr(p, &n2);
         same = n1 == n2 && std::memcmp(s1, s2, 4 * (size_t)n1) == 0;
       }
-      const int64_t t = it.raw - N;
-      int32_t kp = it.kept_parent;
-      int64_t eff = it.eff;
-      if (!same) {
-        vraw.push_back(it.raw);
-        vpar.push_back(it.kept_parent);
-        kp = (int32_t)vraw.size();
-        eff = it.raw;
+      keep[t] = same ? 0 : 1;
+    }
+    std::vector<int32_t> eff(nz);  // kept node id standing for raw merge t
+    for (int64_t t = nz - 1; t >= 0; --t) {
+      const int64_t p = rpar[N + t];
+      const int32_t pe = p < 0 ? 0 : eff[p - N];
+      if (keep[t]) {
+        vraw.push_back(N + t);
+        vpar.push_back(pe);
+        eff[t] = (int32_t)vraw.size();
+      } else {
+        eff[t] = pe;
       }
-      st.push_back({rchild[2 * t + 1], kp, eff});
-      st.push_back({rchild[2 * t], kp, eff});
+    }
+#pragma omp parallel for num_threads(nth) schedule(static)
+    for (int64_t i = 0; i < N; ++i) {
+      const int64_t p = rpar[i];
+      H.lparent[i] = p < 0 ? 0 : eff[p - N];
     }
   }
+  (void)top;
   const int64_t V = (int64_t)vraw.size();
   lap("collapse");
 
@@ -281,38 +299,46 @@ rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg) {
   }
   lap("children");
 
-  // ---- virtual nodes: ordered prefixes (X10) and paths, top-down ----------
-  // DFS creation order puts every parent before its children.
+  // ---- virtual nodes: ordered prefixes (X10) and paths ---------------------
+  // prefix(k) = prefix(parent) ++ sorted(set(k) \ set(parent)) has |set(k)|
+  // entries; each node writes its own by walking up its ancestors (depth <=
+  // K + 1 after the collapse), so the nodes are filled in parallel.
   H.V = V;
   H.vparent.assign(vpar.begin(), vpar.end());
   H.vrep.resize(V);
   H.vpre_off.assign(V + 2, 0);  // by node id 0..V (root: empty)
-  H.vpre.clear();
-  H.vpre.reserve((size_t)V * 4 + 16);
   std::vector<int64_t> vpath_off(V + 2, 0);
-  std::vector<int32_t> vpath;
-  vpath.reserve((size_t)V * 6 + 16);
   std::vector<int32_t> depth(V + 1, 0);
   for (int64_t k = 1; k <= V; ++k) {
-    const int32_t p = vpar[k - 1];
+    int nk;
+    set_ptr(vraw[k - 1], &nk);
     H.vrep[k - 1] = rep_of[k];
-    // prefix = prefix(parent) ++ sorted(set(k) \ set(parent))
-    const int64_t p0 = H.vpre_off[p], p1 = H.vpre_off[p + 1];
-    for (int64_t z = p0; z < p1; ++z) H.vpre.push_back(H.vpre[z]);
-    int nk, np = 0;
-    const uint32_t *sk = set_ptr(vraw[k - 1], &nk);
-    const uint32_t *sp = p > 0 ? set_ptr(vraw[p - 1], &np) : nullptr;
-    int q = 0;
-    for (int x = 0; x < nk; ++x) {  // both sorted: merge-difference
-      while (q < np && sp[q] < sk[x]) ++q;
-      if (q < np && sp[q] == sk[x]) continue;
-      H.vpre.push_back(sk[x]);
+    depth[k] = depth[vpar[k - 1]] + 1;
+    H.vpre_off[k + 1] = H.vpre_off[k] + nk;
+    vpath_off[k + 1] = vpath_off[k] + depth[k];
+  }
+  H.vpre.resize(H.vpre_off[V + 1]);
+  std::vector<int32_t> vpath(vpath_off[V + 1]);
+#pragma omp parallel for num_threads(nth) schedule(dynamic, 512)
+  for (int64_t k = 1; k <= V; ++k) {
+    int32_t chain[260];
+    int nc = 0;
+    for (int32_t x = (int32_t)k; x > 0; x = vpar[x - 1]) chain[nc++] = x;
+    uint32_t *o = H.vpre.data() + H.vpre_off[k];
+    int32_t *pp = vpath.data() + vpath_off[k];
+    for (int c = nc - 1; c >= 0; --c) {  // top-down
+      const int32_t x = chain[c], px = vpar[x - 1];
+      int nx, np = 0;
+      const uint32_t *sx = set_ptr(vraw[x - 1], &nx);
+      const uint32_t *sp = px > 0 ? set_ptr(vraw[px - 1], &np) : nullptr;
+      int q = 0;
+      for (int z = 0; z < nx; ++z) {  // both sorted: merge-difference
+        while (q < np && sp[q] < sx[z]) ++q;
+        if (q < np && sp[q] == sx[z]) continue;
+        *o++ = sx[z];
+      }
+      *pp++ = child_idx[x];
     }
-    H.vpre_off[k + 1] = (int64_t)H.vpre.size();
-    depth[k] = depth[p] + 1;
-    for (int64_t z = vpath_off[p]; z < vpath_off[p + 1]; ++z) vpath.push_back(vpath[z]);
-    vpath.push_back(child_idx[k]);
-    vpath_off[k + 1] = (int64_t)vpath.size();
   }
   lap("virtual");
 
@@ -367,20 +393,12 @@ rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg) {
   }
   lap("schedule");
 
-  // ---- exported merge order: ascending key (X9) ---------------------------
-  {
-    std::vector<MergeKey> zk(nz);
-    for (int64_t t = 0; t < nz; ++t) zk[t] = {H.zh[t], H.za[t], H.zb[t], H.zs[t]};
-    if (nth > 1 && nz > 4096)
-      __gnu_parallel::sort(zk.begin(), zk.end(), key_less);
-    else
-      std::sort(zk.begin(), zk.end(), key_less);
-    for (int64_t t = 0; t < nz; ++t) {
-      H.za[t] = zk[t].a;
-      H.zb[t] = zk[t].b;
-      H.zh[t] = zk[t].h;
-      H.zs[t] = zk[t].size;
-    }
+  sorter.join();
+  for (int64_t t = 0; t < nz; ++t) {
+    H.za[t] = zk[t].a;
+    H.zb[t] = zk[t].b;
+    H.zh[t] = zk[t].h;
+    H.zs[t] = zk[t].size;
   }
   lap("sort merges");
   return RB_OK;

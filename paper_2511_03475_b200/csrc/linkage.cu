@@ -55,6 +55,7 @@ struct PrepArgs {
   int *rep_n, *sz_n;
   int *Mn;
   int *level;  // [0] level list length, [1] h bits
+  int *cstat;  // clique diagnostics: starts, batches, picks, candidates, level n, clk/1k (warp0, pass)
 };
 
 struct BlockScratch {
@@ -184,20 +185,31 @@ __global__ void k_level_adj(PrepArgs a, uint32_t *__restrict__ adj) {
 // an h-neighbour and absorbs its smallest h-neighbour; the merged cluster stays
 // at h only from vertices at h from both (max(h, h') = h iff h' = h), so the
 // candidate set shrinks by intersection; then the next vertex.  Candidate and
-// alive sets are bitsets over list positions in shared memory; each step is
-// one AND pass over an adjacency row (one word per thread) plus a block-wide
-// find-first with a single barrier (double-buffered warp minima).
-__global__ void __launch_bounds__(PT, 1) k_level_cliques(PrepArgs a,
+// alive sets are bitsets over list positions in shared memory.
+// Batching: warp 0 takes the next (up to) 32 candidates p_1 < ... < p_32 of C;
+// the sequential process picks p_1, then each p_j adjacent to every earlier
+// pick (C restricted to (p_1, p_32] is exactly p_2..p_32), which is a shuffle
+// chain over the 32x32 adjacency bits.  One block pass then folds the picks'
+// adjacency rows into C above p_32.  Warp 0 only records the picks (list
+// positions, in greedy order); the merge rows (reps, cumulative sizes,
+// leaders) are written afterwards by the whole block with a segmented scan.
+constexpr int CT = 512;  // threads of k_level_cliques (128 registers for the pick chain)
+__global__ void __launch_bounds__(CT, 1) k_level_cliques(PrepArgs a,
                                                          const uint32_t *__restrict__ adj) {
   extern __shared__ uint32_t bits[];  // [2][W]: alive, candidates
-  __shared__ int s_first[2][PT / 32];
+  __shared__ int s_first[2][CT / 32];
+  __shared__ int s_p[64];     // next candidates (list positions), ascending
+  __shared__ int s_pick[32];  // picks of the batch (list positions)
+  __shared__ int s_npick, s_last, s_nseq;
+  __shared__ int s_sv[CT / 32], s_sf[CT / 32];
   const int n = a.level[0];
   if (n < 2) return;
   const float hf = __uint_as_float((unsigned)a.level[1]);
   const int W = (n + 31) >> 5;
   uint32_t *A = bits, *C = bits + W;
+  int *seq = a.candA, *seqs = a.candB;  // pick list position, its clique's start position
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  for (int w = tid; w < W; w += PT) {
+  for (int w = tid; w < W; w += CT) {
     const int rem = n - w * 32;
     A[w] = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
   }
@@ -206,51 +218,194 @@ __global__ void __launch_bounds__(PT, 1) k_level_cliques(PrepArgs a,
   // C[w] = f(w) for w >= w0; returns the first set bit position (or INT_MAX)
   auto pass = [&](int w0, auto f) {
     int first = 0x7fffffff;
-    for (int w = w0 + tid; w < W; w += PT) {
+    for (int w = w0 + tid; w < W; w += CT) {
       const uint32_t c = f(w);
       C[w] = c;
-      if (c && first == 0x7fffffff) first = w * 32 + __ffs(c) - 1;
+      first = (c != 0u && first == 0x7fffffff) ? w * 32 + __ffs(c) - 1 : first;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
     if (lane == 0) s_first[parity][wid] = first;
     __syncthreads();
-    int m = s_first[parity][lane];
+    int m = lane < CT / 32 ? s_first[parity][lane] : 0x7fffffff;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
     parity ^= 1;
     return m;
   };
-  int sza = 0;
+  int nseq = 0;  // warp 0: picks recorded so far
+  long long st_starts = 0, st_batches = 0, st_picks = 0, st_cands = 0, st_w0 = 0, st_pass = 0;
   for (int ia = 0; ia < n; ++ia) {
     if (!((A[ia >> 5] >> (ia & 31)) & 1u)) continue;  // absorbed earlier (uniform)
-    const int v = a.list[ia];
     const int w0 = ia >> 5;
     const uint32_t gt = (ia & 31) == 31 ? 0u : (0xffffffffu << ((ia & 31) + 1));
     const uint32_t *row = adj + (int64_t)ia * W;
-    int b = pass(w0, [&](int w) { return __ldg(row + w) & A[w] & (w == w0 ? gt : 0xffffffffu); });
-    sza = a.sz[v];
-    while (b < 0x7fffffff) {
-      const int vb = a.list[b];
-      sza += a.sz[vb];
-      if (tid == 0) {
-        const int pos = atomicAdd(a.zcount, 1);
-        a.za[pos] = a.rep[v];
-        a.zb[pos] = a.rep[vb];
-        a.zh[pos] = hf;
-        a.zs[pos] = sza;
-        a.leader[vb] = v;
+    ++st_starts;
+    // the first batch reads adj(ia) & A above ia directly; later ones read C
+    bool first = true;
+    int cur = ia;
+    while (true) {
+      long long c0 = clock64();
+      ++st_batches;
+      if (wid == 0) {
+        // -- collect the next <= 32 candidates; lane l covers 16 consecutive
+        //    words of each 512-word chunk (all loads in flight) --------------
+        int got = 0;
+        for (int wpos = cur >> 5; got < 32 && wpos < W; wpos += 512) {
+          const int wq = wpos + lane * 16;
+          uint32_t c[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            const int w = wq + u;
+            uint32_t x = 0u;
+            if (w < W) x = first ? (__ldg(row + w) & A[w] & (w == w0 ? gt : 0xffffffffu)) : C[w];
+            c[u] = x;
+          }
+          int cnt = 0;
+#pragma unroll
+          for (int u = 0; u < 16; ++u) cnt += __popc(c[u]);
+          int incl = cnt;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            incl += lane >= o ? y : 0;
+          }
+          int slot = got + incl - cnt;
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            uint32_t x = c[u];
+            while (x != 0u && slot < 32) {
+              s_p[slot++] = (wq + u) * 32 + __ffs(x) - 1;
+              x &= x - 1u;
+            }
+          }
+          got += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        __syncwarp();
+        const int k = min(got, 32);
+        int npick = 0;
+        if (k > 0) {
+          const int pi = lane < k ? s_p[lane] : 0;
+          // -- m bit j (j < lane): p_j adjacent to p_lane ----------------------
+          const uint32_t *arow = adj + (int64_t)pi * W;
+          uint32_t wd[31];
+#pragma unroll
+          for (int j = 0; j < 31; ++j) wd[j] = (j < lane && lane < k) ? __ldg(arow + (s_p[j] >> 5)) : 0u;
+          uint32_t m = 0u;
+#pragma unroll
+          for (int j = 0; j < 31; ++j) m |= ((wd[j] >> (s_p[j] & 31)) & 1u) << j;
+          // -- the pick chain: p_1, then the smallest remaining candidate
+          //    adjacent to every pick so far (rem = lanes adjacent to all picks)
+          uint32_t ch = 1u;
+          uint32_t rem = __ballot_sync(0xffffffffu, lane < k && (m & 1u));
+          while (rem != 0u) {
+            const int j = __ffs(rem) - 1;
+            ch |= 1u << j;
+            rem &= __ballot_sync(0xffffffffu, (m >> j) & 1u) & ~((2u << j) - 1u);
+          }
+          const bool picked = lane < k && ((ch >> lane) & 1u);
+          npick = __popc(ch);
+          const int rank = __popc(ch & ((1u << lane) - 1u));
+          if (picked) {
+            seq[nseq + rank] = pi;
+            seqs[nseq + rank] = ia;
+            atomicAnd(&A[pi >> 5], ~(1u << (pi & 31)));
+            s_pick[rank] = pi;
+          }
+        }
+        nseq += npick;
+        st_picks += npick;
+        st_cands += k;
+        if (lane == 0) {
+          s_npick = npick;
+          s_last = got > 32 || (got == 32 && k > 0) ? s_p[31] : -1;
+        }
       }
-      // the thread owning word b/32 clears b's alive bit before the next pass reads it
-      const int wb = b >> 5;
-      if (tid == wb % PT) A[wb] &= ~(1u << (b & 31));
-      const uint32_t *rb = adj + (int64_t)b * W;
-      const uint32_t above = (b & 31) == 31 ? 0u : (0xffffffffu << ((b & 31) + 1));
-      // candidates up to b are already excluded (b was the first set bit)
-      b = pass(wb, [&](int w) { return C[w] & __ldg(rb + w) & (w == wb ? above : 0xffffffffu); });
+      __syncthreads();
+      st_w0 += clock64() - c0;
+      c0 = clock64();
+      const int last = s_last;
+      if (last < 0) break;  // every candidate was considered (uniform)
+      const int npick = s_npick;
+      const int wl = last >> 5;
+      const uint32_t above = (last & 31) == 31 ? 0u : (0xffffffffu << ((last & 31) + 1));
+      const bool fst = first;
+      cur = pass(wl, [&](int w) {
+        uint32_t c = fst ? (__ldg(row + w) & A[w]) : C[w];
+        c &= w == wl ? above : 0xffffffffu;
+        for (int t = 0; t < npick; ++t) c &= __ldg(adj + (int64_t)s_pick[t] * W + w);
+        return c;
+      });
+      st_pass += clock64() - c0;
+      first = false;
+      if (cur == 0x7fffffff) break;
     }
-    if (tid == w0 % PT) A[w0] &= ~(1u << (ia & 31));
     __syncthreads();
+  }
+  if (tid == 0) s_nseq = nseq;
+  __syncthreads();
+  // -- emit the merges: zs = size of the clique after this pick (segmented
+  //    inclusive scan of member sizes within a clique, plus the start's size)
+  const int ns = s_nseq;
+  const int zbase = *a.zcount;
+  int carry = 0;
+  for (int c0 = 0; c0 < ns; c0 += CT) {
+    const int k = c0 + tid;
+    int v = 0, f = 0, vb = 0, va = 0, st = -1;
+    if (k < ns) {
+      st = seqs[k];
+      vb = a.list[seq[k]];
+      va = a.list[st];
+      v = a.sz[vb];
+      f = (k == 0 || seqs[k - 1] != st) ? 1 : 0;
+    }
+    // segmented inclusive scan (flag starts a new segment)
+    int sv = v, sf = f;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int yv = __shfl_up_sync(0xffffffffu, sv, o);
+      const int yf = __shfl_up_sync(0xffffffffu, sf, o);
+      sv = (lane >= o && !sf) ? sv + yv : sv;
+      sf = lane >= o ? (sf | yf) : sf;
+    }
+    if (lane == 31) {
+      s_sv[wid] = sv;
+      s_sf[wid] = sf;
+    }
+    __syncthreads();
+    // prefix over earlier warps of this chunk, then the previous chunks' carry
+    int pv = carry, pf = 0;
+    for (int q = 0; q < wid; ++q) {
+      pv = s_sf[q] ? s_sv[q] : pv + s_sv[q];
+      pf |= s_sf[q];
+    }
+    (void)pf;
+    const int incl = sf ? sv : sv + pv;
+    if (k < ns) {
+      a.za[zbase + k] = a.rep[va];
+      a.zb[zbase + k] = a.rep[vb];
+      a.zh[zbase + k] = hf;
+      a.zs[zbase + k] = a.sz[va] + incl;
+      a.leader[vb] = va;
+    }
+    const int last_in = min(CT, ns - c0) - 1;
+    __syncthreads();
+    if (tid == last_in) s_sv[0] = incl;
+    __syncthreads();
+    carry = s_sv[0];
+    __syncthreads();
+  }
+  if (tid == 0) {
+    *a.zcount = zbase + ns;
+    if (a.cstat) {
+      a.cstat[0] = (int)st_starts;
+      a.cstat[1] = (int)st_batches;
+      a.cstat[2] = (int)st_picks;
+      a.cstat[3] = (int)st_cands;
+      a.cstat[4] = n;
+      a.cstat[5] = (int)(st_w0 >> 10);
+      a.cstat[6] = (int)(st_pass >> 10);
+    }
   }
 }
 
@@ -353,7 +508,7 @@ __global__ void __launch_bounds__(NTH) k_merge_rows(const float *__restrict__ D,
       if (VEC) {
         const float4 *__restrict__ r4 = reinterpret_cast<const float4 *>(row0);
         const int4 *__restrict__ c4 = reinterpret_cast<const int4 *>(colmap);
-        constexpr int UV = 2;
+        constexpr int UV = 4;
         for (int qb = (s0 >> 2) + tid; qb * 4 < M; qb += NTH * UV) {
           int4 t4[UV];
           float4 v4[UV];
@@ -511,6 +666,7 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
   pa.zcount = counters;
   pa.Mn = counters + 1;
   pa.level = counters + 2;
+  pa.cstat = counters + 4;
 
   const float *cur = rows;
   int64_t ld = N;
@@ -525,7 +681,10 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
   int prev_z = 0;
   int zdone = 0;
   while (M > 1) {
-    if (trace) cudaEventRecord(tev[0], st);
+    if (trace) {
+      cudaMemsetAsync(counters + 4, 0, 8 * sizeof(int), st);
+      cudaEventRecord(tev[0], st);
+    }
     pa.D = cur;
     pa.ld = ld;
     pa.M = M;
@@ -541,14 +700,14 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
       const size_t smem = 2 * (size_t)((M + 31) / 32) * 4;
       if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_level_cliques, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      k_level_cliques<<<1, PT, smem, st>>>(pa, adj);
+      k_level_cliques<<<1, CT, smem, st>>>(pa, adj);
     }
     k_prep_compact<<<1, PT, 0, st>>>(pa);
     *launches += 4;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (trace) cudaEventRecord(tev[1], st);
-    int host_c[2];
-    if ((e = cudaMemcpyAsync(host_c, counters, sizeof(host_c), cudaMemcpyDeviceToHost, st)) !=
+    int host_c[12] = {0};
+    if ((e = cudaMemcpyAsync(host_c, counters, (trace ? 12 : 2) * sizeof(int), cudaMemcpyDeviceToHost, st)) !=
         cudaSuccess)
       return e;
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
@@ -601,8 +760,11 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
       float a = 0, b = 0;
       cudaEventElapsedTime(&a, tev[0], tev[1]);
       cudaEventElapsedTime(&b, tev[1], tev[2]);
-      std::fprintf(stderr, "[ragb linkage] round %d M=%d Mn=%d merges=%d prep=%.3fms merge=%.3fms\n",
-                   out->rounds, M, Mn, host_c[0] - prev_z, a, b);
+      std::fprintf(stderr,
+                   "[ragb linkage] round %d M=%d Mn=%d merges=%d prep=%.3fms merge=%.3fms | level n=%d "
+                   "starts=%d batches=%d picks=%d cands=%d kclk w0=%d pass=%d\n",
+                   out->rounds, M, Mn, host_c[0] - prev_z, a, b, host_c[8], host_c[4], host_c[5],
+                   host_c[6], host_c[7], host_c[9], host_c[10]);
       prev_z = host_c[0];
     }
     p ^= 1;
