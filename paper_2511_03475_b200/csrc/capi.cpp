@@ -107,6 +107,8 @@ ScratchLayout ScratchLayout::make(int64_t N, int32_t K, bool keep_rows, bool lin
     L.zb = take(o, (size_t)N * 4);
     L.zh = take(o, (size_t)N * 4);
     L.zs = take(o, (size_t)N * 4);
+    L.amask = take(o, (size_t)(N / 32 + 1) * 4);
+    L.mlist = take(o, (size_t)N * 4);
     // compacted matrices: at most (N-1) rows with a leading dimension padded to 4
     const size_t mat = (size_t)(N - 1) * (size_t)((N + 2) & ~3ll) * 4;
     L.matA = take(o, mat);

@@ -31,7 +31,7 @@ inline int64_t padded_cols(int64_t N) { return round_up(N, kChunk); }
 // Byte layout of the caller-owned scratch buffer (all offsets 256-aligned).
 struct ScratchLayout {
   size_t err, idsT, nnkey, stage_ids, stage_lens, lut, key0, key1, rep0, rep1, sz0, sz1, leader, aux0, aux1, aux2, aux3, aux4,
-      alive, za, zb, zh, zs, counters, matA, matB, total;
+      alive, za, zb, zh, zs, amask, mlist, counters, matA, matB, total;
   static ScratchLayout make(int64_t N, int32_t K, bool keep_rows, bool linkage);
 };
 

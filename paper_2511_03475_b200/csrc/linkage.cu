@@ -37,6 +37,8 @@ namespace {
 
 typedef unsigned long long u64;
 constexpr int PT = 1024;  // threads of the single-CTA round-prep kernel
+constexpr u64 kDead = ~0ull;  // row key of a row merged away by an in-place round
+constexpr int kInplaceMaxM = 48 * 1024;  // in-place rounds keep a whole row in shared memory
 
 struct PrepArgs {
   const float *D;
@@ -131,9 +133,10 @@ __global__ void __launch_bounds__(PT, 1) k_prep_mark(PrepArgs a) {
     const u64 kx = a.key[x];
     const unsigned hx = (unsigned)(kx >> 32);
     const int y = (int)(kx & 0xffffffffu);
-    int lead = x;
-    a.alive[x] = (hx == h) ? 1 : 0;
-    if (hx > h && (int)(a.key[y] & 0xffffffffu) == x) {
+    const bool dead = kx == kDead;  // row merged away by an in-place round
+    int lead = dead ? -1 : x;
+    a.alive[x] = (!dead && hx == h) ? 1 : 0;
+    if (!dead && hx > h && (int)(a.key[y] & 0xffffffffu) == x) {
       if (y < x) {
         lead = y;
       } else {
@@ -193,6 +196,120 @@ __global__ void k_level_adj(PrepArgs a, uint32_t *__restrict__ adj) {
 // adjacency rows into C above p_32.  Warp 0 only records the picks (list
 // positions, in greedy order); the merge rows (reps, cumulative sizes,
 // leaders) are written afterwards by the whole block with a segmented scan.
+// Warp-resident variant (n <= 32 * 32 * WPL): one warp holds the alive and
+// candidate bitsets in registers (lane l owns words [l*WPL, (l+1)*WPL)), so a
+// batch costs no block barrier: collect the next <= 32 candidates, their
+// mutual adjacency bits, the pick chain, then fold the picks' adjacency rows
+// into C above the last candidate.  For n <= 1024 the adjacency (n x 32
+// words) is staged in shared memory first.  Returns the number of picks
+// (lane-uniform); picks go to seq/seqs in greedy order.
+template <int WPL>
+__device__ int cliques_warp(const PrepArgs &a, const uint32_t *adj, int n, int W, int *s_p, int *seq,
+                            int *seqs) {
+  const int lane = threadIdx.x & 31;
+  const int base = lane * WPL;
+  uint32_t A[WPL], C[WPL];
+#pragma unroll
+  for (int u = 0; u < WPL; ++u) {
+    const int w = base + u, rem = n - w * 32;
+    A[u] = w < W ? (rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u)) : 0u;
+  }
+  int nseq = 0;
+  for (int ia = 0; ia < n; ++ia) {
+    const int wi = ia >> 5, own = wi / WPL, ui = wi - own * WPL;
+    uint32_t aw = 0u;
+#pragma unroll
+    for (int u = 0; u < WPL; ++u) aw = u == ui ? A[u] : aw;
+    aw = __shfl_sync(0xffffffffu, aw, own);
+    if (!((aw >> (ia & 31)) & 1u)) continue;  // absorbed earlier
+    const uint32_t gt = (ia & 31) == 31 ? 0u : (0xffffffffu << ((ia & 31) + 1));
+    const uint32_t *row = adj + (int64_t)ia * W;
+#pragma unroll
+    for (int u = 0; u < WPL; ++u) {
+      const int w = base + u;
+      uint32_t x = w < W ? row[w] : 0u;
+      x &= A[u];
+      x = w < wi ? 0u : (w == wi ? (x & gt) : x);
+      C[u] = x;
+    }
+    while (true) {
+      // -- collect the first <= 32 candidates -------------------------------
+      int cnt = 0;
+#pragma unroll
+      for (int u = 0; u < WPL; ++u) cnt += __popc(C[u]);
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        incl += lane >= o ? y : 0;
+      }
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      if (total == 0) break;
+      int slot = incl - cnt;
+#pragma unroll
+      for (int u = 0; u < WPL; ++u) {
+        uint32_t x = C[u];
+        while (x != 0u && slot < 32) {
+          s_p[slot++] = (base + u) * 32 + __ffs(x) - 1;
+          x &= x - 1u;
+        }
+      }
+      __syncwarp();
+      const int k = min(total, 32);
+      const int pi = lane < k ? s_p[lane] : 0;
+      // -- m bit j (j < lane): p_j adjacent to p_lane ------------------------
+      const uint32_t *arow = adj + (int64_t)pi * W;
+      uint32_t wd[31];
+#pragma unroll
+      for (int j = 0; j < 31; ++j) wd[j] = (j < lane && lane < k) ? arow[s_p[j] >> 5] : 0u;
+      uint32_t m = 0u;
+#pragma unroll
+      for (int j = 0; j < 31; ++j) m |= ((wd[j] >> (s_p[j] & 31)) & 1u) << j;
+      // -- pick chain --------------------------------------------------------
+      uint32_t ch = 1u;
+      uint32_t rem = __ballot_sync(0xffffffffu, lane < k && (m & 1u));
+      while (rem != 0u) {
+        const int j = __ffs(rem) - 1;
+        ch |= 1u << j;
+        rem &= __ballot_sync(0xffffffffu, (m >> j) & 1u) & ~((2u << j) - 1u);
+      }
+      const int rank = __popc(ch & ((1u << lane) - 1u));
+      if (lane < k && ((ch >> lane) & 1u)) {
+        seq[nseq + rank] = pi;
+        seqs[nseq + rank] = ia;
+      }
+      nseq += __popc(ch);
+      // -- picks leave the alive set ------------------------------------------
+      for (uint32_t pm = ch; pm != 0u; pm &= pm - 1u) {
+        const int pj = s_p[__ffs(pm) - 1];
+        const int wj = pj >> 5, oj = wj / WPL, uj = wj - oj * WPL;
+        const uint32_t clr = lane == oj ? ~(1u << (pj & 31)) : 0xffffffffu;
+#pragma unroll
+        for (int u = 0; u < WPL; ++u) A[u] &= u == uj ? clr : 0xffffffffu;
+      }
+      if (total <= 32) break;  // every candidate was considered
+      // -- C &= adj(pick) for every pick, above the last candidate ------------
+      const int last = s_p[31], wl = last >> 5;
+      const uint32_t above = (last & 31) == 31 ? 0u : (0xffffffffu << ((last & 31) + 1));
+      for (uint32_t pm = ch; pm != 0u; pm &= pm - 1u) {
+        const uint32_t *prow = adj + (int64_t)s_p[__ffs(pm) - 1] * W;
+#pragma unroll
+        for (int u = 0; u < WPL; ++u) C[u] &= base + u < W ? prow[base + u] : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < WPL; ++u) {
+        const int w = base + u;
+        C[u] = w < wl ? 0u : (w == wl ? (C[u] & above) : C[u]);
+      }
+      __syncwarp();  // s_p is rewritten by the next collection
+    }
+  }
+  return nseq;
+}
+// Above 4096 vertices the per-batch fold (picks x WPL loads per lane) makes
+// the single warp slower than the block-wide passes (measured at n = 16082).
+constexpr int kWarpCliqueMaxN = 32 * 32 * 4;
+
 constexpr int CT = 512;  // threads of k_level_cliques (128 registers for the pick chain)
 __global__ void __launch_bounds__(CT, 1) k_level_cliques(PrepArgs a,
                                                          const uint32_t *__restrict__ adj) {
@@ -235,6 +352,15 @@ __global__ void __launch_bounds__(CT, 1) k_level_cliques(PrepArgs a,
   };
   int nseq = 0;  // warp 0: picks recorded so far
   long long st_starts = 0, st_batches = 0, st_picks = 0, st_cands = 0, st_w0 = 0, st_pass = 0;
+  if (n <= kWarpCliqueMaxN) {
+    if (n <= 1024) {  // stage the adjacency (n x W <= 32K words) in shared memory
+      for (int i = tid; i < n * W; i += CT) bits[i] = __ldg(adj + i);
+      __syncthreads();
+      if (wid == 0) nseq = cliques_warp<1>(a, bits, n, W, s_p, seq, seqs);
+    } else if (wid == 0) {
+      nseq = cliques_warp<4>(a, adj, n, W, s_p, seq, seqs);
+    }
+  } else
   for (int ia = 0; ia < n; ++ia) {
     if (!((A[ia >> 5] >> (ia & 31)) & 1u)) continue;  // absorbed earlier (uniform)
     const int w0 = ia >> 5;
@@ -433,6 +559,7 @@ __global__ void __launch_bounds__(PT, 1) k_prep_compact(PrepArgs a) {
   __syncthreads();
   for (int x = tid; x < M; x += PT) {
     const int l = a.leader[x];
+    if (l < 0) continue;  // dead row
     const int g = a.newidx[l];
     atomicAdd(&a.cnt[g], 1);
     atomicAdd(&a.sz_n[g], a.sz[x]);
@@ -449,19 +576,21 @@ __global__ void __launch_bounds__(PT, 1) k_prep_compact(PrepArgs a) {
     base += tot;
   }
   if (tid == 0) {
-    a.goff[Mn] = M;
+    a.goff[Mn] = base;  // live rows (dead rows of in-place rounds are in no group)
     *a.Mn = Mn;
   }
   __syncthreads();
   for (int x = tid; x < M; x += PT) {
-    const int g = a.newidx[a.leader[x]];
+    const int l = a.leader[x];
+    if (l < 0) continue;
+    const int g = a.newidx[l];
     a.gmem[a.goff[g] + atomicAdd(&a.cursor[g], 1)] = x;
   }
   __syncthreads();
   // old column -> new column; new column -> its leader (smallest old member)
   for (int x = tid; x < M; x += PT) {
     const int l = a.leader[x];
-    const int g = a.newidx[l];
+    const int g = l < 0 ? -1 : a.newidx[l];
     a.colsrc[x] = g;
     if (l == x) a.cursor[g] = x;  // cursor is free after the scatter: first_old
   }
@@ -611,6 +740,204 @@ __global__ void __launch_bounds__(NTH) k_merge_rows(const float *__restrict__ D,
   }
 }
 
+// ---------------------------------------------------------------------------
+// In-place rounds.  When a round merges few clusters, rewriting the whole
+// compacted matrix costs (M^2 + Mn^2) floats while only the merged rows and
+// columns change.  Then the matrix keeps its size: rows merged away get the
+// key kDead and a cleared bit in the alive mask, the surviving (smallest)
+// member of each group gets the merged row, its column is rewritten from that
+// row (the matrix is symmetric), and only rows whose nearest neighbour was in
+// a merged group are rescanned (any other row's nearest neighbour is unchanged:
+// complete-linkage values only grow, X7, and the group keeps the smallest
+// index, X8).  Column order is unchanged, so column order == rep order still.
+
+// S0: per-row flags; multi-member groups -> mlist; members other than the
+// survivor -> dead; the survivor's size.
+__global__ void k_inplace_prep(PrepArgs a, int M, uint32_t *__restrict__ amask, int *__restrict__ mlist,
+                               int *__restrict__ nmulti, int *__restrict__ sz, u64 *__restrict__ key) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < M; x += gridDim.x * blockDim.x) {
+    const int l = a.leader[x];
+    uint8_t chg = 0;
+    if (l >= 0) {
+      const int g = a.newidx[l];
+      if (a.goff[g + 1] - a.goff[g] >= 2) {
+        chg = 1;
+        if (x != l) {
+          key[x] = kDead;
+          atomicAnd(&amask[x >> 5], ~(1u << (x & 31)));
+        } else {
+          mlist[atomicAdd(nmulti, 1)] = g;
+          sz[x] = a.sz_n[g];
+        }
+      }
+    }
+    a.alive[x] = chg;  // "in a merged group" (the level flags are free by now)
+  }
+}
+
+// S1: one CTA per merged group: the survivor's new row in shared memory,
+// row(L)[c] = max over members m of D[m][c]; then the entries at the other
+// merged groups' survivors, row(L)[L_h] = max over x in h of row(L)[x]; the
+// diagonal; write back and the row's nearest neighbour over live columns.
+template <int NTH>
+__global__ void __launch_bounds__(NTH, 2) k_inplace_rows(PrepArgs a, float *__restrict__ D, int64_t ld, int M,
+                                                      const uint32_t *__restrict__ amask,
+                                                      const int *__restrict__ mlist,
+                                                      const int *__restrict__ nmulti_p, u64 *__restrict__ key) {
+  extern __shared__ __align__(16) float row[];  // [M rounded up to 4]
+  __shared__ u64 wmin[NTH / 32];
+  const int nmulti = *nmulti_p;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int M4 = (M + 3) >> 2;
+  for (int gi = blockIdx.x; gi < nmulti; gi += gridDim.x) {
+    const int g = mlist[gi];
+    const int rb = a.goff[g], re = a.goff[g + 1];
+    const int L = a.cursor[g];  // first_old: the survivor
+    for (int q = tid; q < M4; q += NTH) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int r = rb; r < re; ++r) {
+        const float4 x = __ldcs(reinterpret_cast<const float4 *>(D + (int64_t)a.gmem[r] * ld) + q);
+        v.x = fmaxf(v.x, x.x);
+        v.y = fmaxf(v.y, x.y);
+        v.z = fmaxf(v.z, x.z);
+        v.w = fmaxf(v.w, x.w);
+      }
+      reinterpret_cast<float4 *>(row)[q] = v;
+    }
+    __syncthreads();
+    for (int hi = tid; hi < nmulti; hi += NTH) {
+      const int h = mlist[hi];
+      if (h == g) continue;
+      float v = 0.f;
+      for (int r = a.goff[h]; r < a.goff[h + 1]; ++r) v = fmaxf(v, row[a.gmem[r]]);
+      row[a.cursor[h]] = v;
+    }
+    __syncthreads();
+    if (tid == 0) row[L] = 0.f;
+    __syncthreads();
+    u64 best = ~0ull;
+    float4 *out = reinterpret_cast<float4 *>(D + (int64_t)L * ld);
+    for (int q = tid; q < M4; q += NTH) {
+      const float4 v = reinterpret_cast<const float4 *>(row)[q];
+      __stcs(out + q, v);
+      const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int c = 4 * q + k;
+        const bool live = c < M && c != L && ((amask[c >> 5] >> (c & 31)) & 1u);
+        const u64 kk = ((u64)__float_as_uint(vv[k]) << 32) | (unsigned)c;
+        best = (live && kk < best) ? kk : best;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const u64 y = __shfl_xor_sync(0xffffffffu, best, o);
+      best = y < best ? y : best;
+    }
+    if (lane == 0) wmin[w] = best;
+    __syncthreads();
+    if (tid == 0) {
+      u64 b = wmin[0];
+#pragma unroll
+      for (int i = 1; i < NTH / 32; ++i) b = wmin[i] < b ? wmin[i] : b;
+      key[L] = b;
+    }
+    __syncthreads();
+  }
+}
+
+// S2: columns from rows (symmetry): D[r][L] = D[L][r] for every live row r.
+// Work items = (merged group, 1024-row chunk); each thread moves 4 rows
+// (coalesced loads, scattered 4-byte stores).  Few, long-lived CTAs: with one
+// short CTA per item the block scheduler, not the stores, set the pace.
+__global__ void __launch_bounds__(256) k_inplace_cols(PrepArgs a, float *__restrict__ D, int64_t ld, int M,
+                                                      const uint32_t *__restrict__ amask,
+                                                      const int *__restrict__ mlist,
+                                                      const int *__restrict__ nmulti_p) {
+  const int nmulti = *nmulti_p;
+  const int nchunk = (M + 1023) >> 10;
+  const int64_t items = (int64_t)nmulti * nchunk;
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const int gi = (int)(it / nchunk), ch = (int)(it - (int64_t)gi * nchunk);
+    const int L = a.cursor[mlist[gi]];
+    const float *src = D + (int64_t)L * ld;
+    float v[4];
+    int rr[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int r = (ch << 10) + u * 256 + (int)threadIdx.x;
+      rr[u] = (r < M && ((amask[r >> 5] >> (r & 31)) & 1u)) ? r : -1;
+      v[u] = rr[u] >= 0 ? __ldg(src + r) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (rr[u] >= 0) D[(int64_t)rr[u] * ld + L] = v[u];
+  }
+}
+
+// S3a: one thread per live row r outside the merged groups whose nearest
+// neighbour t was in a merged group g with survivor L: the new value d(r, L)
+// (column L was rewritten by S2) is >= the old d(r, t); if equal, (d, L) is
+// the new key without a scan (L <= t, every other entry is unchanged or
+// larger); otherwise r goes to the rescan list.
+__global__ void k_inplace_check(PrepArgs a, const float *__restrict__ D, int64_t ld, int M,
+                                u64 *__restrict__ key, int *__restrict__ rlist, int *__restrict__ nres) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < M; r += gridDim.x * blockDim.x) {
+    const u64 kr = key[r];
+    if (kr == kDead || a.alive[r]) continue;  // dead, or a survivor (done in S1)
+    const int t = (int)(kr & 0xffffffffu);
+    if (!a.alive[t]) continue;  // neighbour not merged: unchanged
+    const int Lg = a.leader[t];
+    const unsigned v = __float_as_uint(D[(int64_t)r * ld + Lg]);
+    if (v == (unsigned)(kr >> 32))
+      key[r] = ((u64)v << 32) | (unsigned)Lg;
+    else
+      rlist[atomicAdd(nres, 1)] = r;
+  }
+}
+
+// S3b: full rescans of the listed rows over the live columns.
+template <int NTH>
+__global__ void __launch_bounds__(NTH) k_inplace_rescan(const float *__restrict__ D, int64_t ld, int M,
+                                                        const uint32_t *__restrict__ amask,
+                                                        const int *__restrict__ rlist,
+                                                        const int *__restrict__ nres_p, u64 *__restrict__ key) {
+  __shared__ u64 wmin[NTH / 32];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int M4 = (M + 3) >> 2;
+  const int nres = *nres_p;
+  for (int i = blockIdx.x; i < nres; i += gridDim.x) {
+    const int r = rlist[i];
+    u64 best = ~0ull;
+    const float4 *src = reinterpret_cast<const float4 *>(D + (int64_t)r * ld);
+    for (int q = tid; q < M4; q += NTH) {
+      const float4 v = __ldcs(src + q);
+      const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int c = 4 * q + k;
+        const bool live = c < M && c != r && ((amask[c >> 5] >> (c & 31)) & 1u);
+        const u64 kk = ((u64)__float_as_uint(vv[k]) << 32) | (unsigned)c;
+        best = (live && kk < best) ? kk : best;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const u64 y = __shfl_xor_sync(0xffffffffu, best, o);
+      best = y < best ? y : best;
+    }
+    if (lane == 0) wmin[w] = best;
+    __syncthreads();
+    if (tid == 0) {
+      u64 b = wmin[0];
+#pragma unroll
+      for (int i2 = 1; i2 < NTH / 32; ++i2) b = wmin[i2] < b ? wmin[i2] : b;
+      key[r] = b;
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void k_init_state(int *rep, int *sz, int64_t N) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < N) {
@@ -668,19 +995,27 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
   pa.level = counters + 2;
   pa.cstat = counters + 4;
 
-  const float *cur = rows;
+  float *cur = rows;
   int64_t ld = N;
-  int M = (int)N;
+  int M = (int)N;   // rows of the current matrix (live + dead)
+  int live = (int)N;  // live clusters
+  bool mask_ok = false;  // alive mask valid for the current matrix
+  uint32_t *amask = at<uint32_t>(scratch, L.amask);
+  int *mlist = at<int>(scratch, L.mlist);
+  int *nmulti = counters + 12;
   int p = 0;
   float *next = matA;
   // RAGB_TRACE=1: per-round timing on stderr (diagnostics only).
   const bool trace = std::getenv("RAGB_TRACE") != nullptr;
+  // RAGB_INPLACE=0 / 1: never / always take in-place rounds (testing); unset: cost model
+  const char *ipm = std::getenv("RAGB_INPLACE");
+  const int inplace_mode = ipm ? std::atoi(ipm) : 2;
   cudaEvent_t tev[3];
   if (trace)
     for (auto &x : tev) cudaEventCreate(&x);
-  int prev_z = 0;
+  int zprev = 0;
   int zdone = 0;
-  while (M > 1) {
+  while (live > 1) {
     if (trace) {
       cudaMemsetAsync(counters + 4, 0, 8 * sizeof(int), st);
       cudaEventRecord(tev[0], st);
@@ -697,7 +1032,8 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
     uint32_t *adj = reinterpret_cast<uint32_t *>(next);  // free until the merge writes it
     k_level_adj<<<sms * 4, 256, 0, st>>>(pa, adj);
     {
-      const size_t smem = 2 * (size_t)((M + 31) / 32) * 4;
+      const size_t m1 = std::min<size_t>((size_t)M, 1024);
+      const size_t smem = std::max(2 * (size_t)((M + 31) / 32), m1 * ((m1 + 31) / 32)) * 4;
       if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_level_cliques, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       k_level_cliques<<<1, CT, smem, st>>>(pa, adj);
@@ -729,8 +1065,30 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
       }
     }
     const int Mn = host_c[1];
-    if (Mn >= M || Mn < 1) return cudaErrorUnknown;  // no progress: invariant violated
-    if (Mn > 1) {
+    if (Mn >= live || Mn < 1) return cudaErrorUnknown;  // no progress: invariant violated
+    const int merges_round = host_c[0] - zprev;
+    zprev = host_c[0];
+    // in place when the merged rows, the rewritten columns (one scattered
+    // 4-byte store per row and merge, ~30 row-equivalents per merge measured)
+    // and the rescans cost less than rewriting the matrix (~live + Mn^2/M rows)
+    const bool inplace = Mn > 1 && cur != rows && M <= kInplaceMaxM && inplace_mode != 0 &&
+                         (inplace_mode == 1 || 32.0 * merges_round < (double)live + (double)Mn * Mn / M);
+    if (inplace) {
+      if (!mask_ok) {
+        if ((e = cudaMemsetAsync(amask, 0xff, (size_t)(M / 32 + 1) * 4, st)) != cudaSuccess) return e;
+        mask_ok = true;
+      }
+      if ((e = cudaMemsetAsync(nmulti, 0, 8, st)) != cudaSuccess) return e;  // nmulti, nres
+      k_inplace_prep<<<sms * 2, 256, 0, st>>>(pa, M, amask, mlist, nmulti, sz[p], key[p]);
+      const size_t smem = (size_t)((M + 3) & ~3) * 4;
+      cudaFuncSetAttribute(k_inplace_rows<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      k_inplace_rows<512><<<sms * 2, 512, smem, st>>>(pa, cur, ld, M, amask, mlist, nmulti, key[p]);
+      k_inplace_cols<<<sms * 8, 256, 0, st>>>(pa, cur, ld, M, amask, mlist, nmulti);
+      k_inplace_check<<<(M + 255) / 256, 256, 0, st>>>(pa, cur, ld, M, key[p], pa.cnt, nmulti + 1);  // cnt: free after the compaction map
+      k_inplace_rescan<256><<<sms * 4, 256, 0, st>>>(cur, ld, M, amask, pa.cnt, nmulti + 1, key[p]);
+      *launches += 5;
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    } else if (Mn > 1) {
       // window: the whole new row if it fits in shared memory, else pieces.
       // Wide rows: 1024-thread CTAs, one per SM; narrow rows: 256-thread CTAs
       // so that several rows are in flight per SM (per-row latency dominates).
@@ -753,6 +1111,7 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
       cur = next;
       next = (next == matA) ? matB : matA;
       ld = ((int64_t)Mn + 3) & ~3ll;  // padded leading dimension of the new matrix
+      mask_ok = false;
     }
     if (trace) {
       cudaEventRecord(tev[2], st);
@@ -761,14 +1120,16 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
       cudaEventElapsedTime(&a, tev[0], tev[1]);
       cudaEventElapsedTime(&b, tev[1], tev[2]);
       std::fprintf(stderr,
-                   "[ragb linkage] round %d M=%d Mn=%d merges=%d prep=%.3fms merge=%.3fms | level n=%d "
+                   "[ragb linkage] round %d M=%d live=%d Mn=%d merges=%d %s prep=%.3fms merge=%.3fms | level n=%d "
                    "starts=%d batches=%d picks=%d cands=%d kclk w0=%d pass=%d\n",
-                   out->rounds, M, Mn, host_c[0] - prev_z, a, b, host_c[8], host_c[4], host_c[5],
-                   host_c[6], host_c[7], host_c[9], host_c[10]);
-      prev_z = host_c[0];
+                   out->rounds, M, live, Mn, merges_round, inplace ? "inplace" : "compact", a, b, host_c[8],
+                   host_c[4], host_c[5], host_c[6], host_c[7], host_c[9], host_c[10]);
     }
-    p ^= 1;
-    M = Mn;
+    if (!inplace) {
+      p ^= 1;
+      M = Mn;
+    }
+    live = Mn;
   }
   if (trace)
     for (auto &x : tev) cudaEventDestroy(x);
