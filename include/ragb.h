@@ -230,6 +230,25 @@ RB_API rb_status rb_dedup_turn(rb_session *s, const uint32_t *ids, int32_t n, ui
                                int32_t *n_novel, uint32_t *ref_doc, int32_t *ref_turn,
                                int32_t *n_ref);
 
+/* The session's cumulative context: the turn-0 context followed by every
+ * turn's novel docs in the order they were prefilled ("appended to a copy of
+ * the first-turn context state"; X18).  out: host [cap] or NULL
+ * (then only *n is set).  Errors: RB_ESESSION, RB_EINVAL (cap < *n). */
+RB_API rb_status rb_session_context(const rb_session *s, uint32_t *out, int32_t cap, int32_t *n);
+
+/* NEXT-2: a batch of follow-up turns over many sessions.
+ * Row i (host ids [M][K], lens [M] or NULL = K) is the next turn of session
+ * sessions[turn_session[i]]; rows of one session are applied in row order,
+ * distinct sessions are independent (processed in parallel on the host).
+ * Per row the result equals rb_dedup_turn: novel [M][K] (first n_novel[i]
+ * valid), ref_doc / ref_turn [M][K] (first n_ref[i] valid).  All rows are
+ * validated before any session changes.  Errors: RB_EINVAL, RB_ESESSION
+ * (index out of range or NULL handle), RB_EDUPDOC. */
+RB_API rb_status rb_dedup_batch(rb_session *const *sessions, int64_t S, const int64_t *turn_session,
+                                const uint32_t *ids, const uint8_t *lens, int64_t M, int32_t K,
+                                uint32_t *novel, int32_t *n_novel, uint32_t *ref_doc, int32_t *ref_turn,
+                                int32_t *n_ref);
+
 /* Current turn number of a session (0 right after open). */
 RB_API rb_status rb_session_turn(const rb_session *s, int32_t *turn);
 

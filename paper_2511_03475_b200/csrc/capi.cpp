@@ -25,6 +25,7 @@ struct rb_index {
 
 struct rb_session {
   std::unordered_map<uint32_t, int32_t> seen;  // doc -> turn first prefilled
+  std::vector<uint32_t> ctx;                   // turn-0 context ++ novel docs
   int32_t turn = 0;
 };
 
@@ -575,6 +576,7 @@ static rb_status session_from_docs(const uint32_t *docs, int32_t n, rb_session *
       return fail(RB_EDUPDOC, "duplicate DocId in turn-0 context");
     }
   }
+  s->ctx.assign(docs, docs + n);
   *out = s;
   return RB_OK;
 }
@@ -629,9 +631,59 @@ rb_status rb_dedup_turn(rb_session *s, const uint32_t *ids, int32_t n, uint32_t 
     }
   }
   for (int32_t k = 0; k < nn; ++k) s->seen.emplace(novel[k], turn);
+  s->ctx.insert(s->ctx.end(), novel, novel + nn);
   s->turn = turn;
   *n_novel = nn;
   *n_ref = nr;
+  return RB_OK;
+}
+
+rb_status rb_session_context(const rb_session *s, uint32_t *out, int32_t cap, int32_t *n) {
+  if (!s) return fail(RB_ESESSION, "NULL session");
+  if (!n) return fail(RB_EINVAL, "NULL output");
+  *n = (int32_t)s->ctx.size();
+  if (out) {
+    if (cap < *n) return fail(RB_EINVAL, "output capacity too small");
+    std::memcpy(out, s->ctx.data(), s->ctx.size() * 4);
+  }
+  return RB_OK;
+}
+
+rb_status rb_dedup_batch(rb_session *const *sessions, int64_t S, const int64_t *turn_session,
+                         const uint32_t *ids, const uint8_t *lens, int64_t M, int32_t K, uint32_t *novel,
+                         int32_t *n_novel, uint32_t *ref_doc, int32_t *ref_turn, int32_t *n_ref) {
+  if (M < 0 || K < 1 || K > 255 || (M > 0 && (!sessions || !turn_session || !ids || !novel || !n_novel ||
+                                               !ref_doc || !ref_turn || !n_ref)))
+    return fail(RB_EINVAL, "bad argument");
+  // validate everything before any state changes
+  for (int64_t i = 0; i < M; ++i) {
+    const int64_t si = turn_session[i];
+    if (si < 0 || si >= S || !sessions[si]) return fail(RB_ESESSION, "row " + std::to_string(i) + ": bad session");
+    const int L = lens ? lens[i] : K;
+    if (L < 0 || L > K) return fail(RB_EINVAL, "row " + std::to_string(i) + ": length not in [0, K]");
+    const uint32_t *r = ids + i * K;
+    for (int k = 1; k < L; ++k)
+      for (int q = 0; q < k; ++q)
+        if (r[q] == r[k]) return fail(RB_EDUPDOC, "row " + std::to_string(i) + ": duplicate DocId");
+  }
+  // rows grouped by session (stable: a session's turns keep their order);
+  // sessions are independent, so the groups run in parallel
+  std::vector<int64_t> off(S + 1, 0), order(M);
+  for (int64_t i = 0; i < M; ++i) ++off[turn_session[i] + 1];
+  for (int64_t q = 0; q < S; ++q) off[q + 1] += off[q];
+  {
+    std::vector<int64_t> fill(off.begin(), off.end() - 1);
+    for (int64_t i = 0; i < M; ++i) order[fill[turn_session[i]]++] = i;
+  }
+#pragma omp parallel for schedule(dynamic, 64) num_threads(ragb::host_threads())
+  for (int64_t q = 0; q < S; ++q) {
+    for (int64_t z = off[q]; z < off[q + 1]; ++z) {
+      const int64_t i = order[z];
+      const int L = lens ? lens[i] : K;
+      rb_dedup_turn(sessions[q], ids + i * K, L, novel + i * K, n_novel + i, ref_doc + i * K, ref_turn + i * K,
+                    n_ref + i);
+    }
+  }
   return RB_OK;
 }
 

@@ -29,7 +29,7 @@ EXPORTED = [
     "rb_build_index_host", "rb_index_from_linkage", "rb_index_size", "rb_index_stats", "rb_index_nn",
     "rb_index_linkage", "rb_index_tree_info", "rb_index_tree", "rb_order_contexts", "rb_session_open",
     "rb_session_open_docs", "rb_dedup_turn", "rb_session_turn", "rb_session_free", "rb_index_free",
-    "rb_index_set_alpha",
+    "rb_index_set_alpha", "rb_session_context", "rb_dedup_batch",
 ]
 
 
@@ -85,6 +85,8 @@ def lib():
         "rb_index_tree": ([P, P, P, P, P, P, P, P], i32),
         "rb_order_contexts": ([P, P, P, i64, i32, P, P, P], i32),
         "rb_index_set_alpha": ([P, u32, u32], i32),
+        "rb_session_context": ([P, P, i32, ctypes.POINTER(i32)], i32),
+        "rb_dedup_batch": ([P, i64, P, P, P, i64, i32, P, P, P, P, P], i32),
         "rb_session_open": ([P, i64, PP], i32),
         "rb_session_open_docs": ([P, i32, PP], i32),
         "rb_dedup_turn": ([P, P, i32, P, ctypes.POINTER(i32), P, P, ctypes.POINTER(i32)], i32),
@@ -265,6 +267,33 @@ class Session:
         _check(lib().rb_dedup_turn(self._h, _np_ptr(d), n, _np_ptr(novel), ctypes.byref(nn_), _np_ptr(rdoc),
                                    _np_ptr(rturn), ctypes.byref(nr)))
         return novel[:nn_.value].copy(), rdoc[:nr.value].copy(), rturn[:nr.value].copy()
+
+    def context(self) -> np.ndarray:
+        """Cumulative context: turn-0 docs ++ every turn's novel docs."""
+        n = ctypes.c_int32()
+        _check(lib().rb_session_context(self._h, None, 0, ctypes.byref(n)))
+        out = np.empty(max(n.value, 1), dtype=np.uint32)
+        _check(lib().rb_session_context(self._h, _np_ptr(out), n.value, ctypes.byref(n)))
+        return out[:n.value].copy()
+
+
+def dedup_batch(sessions, turn_session, ids, lens=None):
+    """NEXT-2: row i is the next turn of sessions[turn_session[i]]; returns
+    (novel [M,K], n_novel [M], ref_doc [M,K], ref_turn [M,K], n_ref [M])."""
+    ids = np.ascontiguousarray(ids, dtype=np.uint32)
+    M, K = ids.shape
+    ts = np.ascontiguousarray(turn_session, dtype=np.int64)
+    lens_a = None if lens is None else np.ascontiguousarray(lens, dtype=np.uint8)
+    handles = (ctypes.c_void_p * max(len(sessions), 1))(*[s._h.value if hasattr(s._h, "value") else s._h
+                                                          for s in sessions])
+    novel = np.empty((M, K), dtype=np.uint32)
+    rdoc = np.empty((M, K), dtype=np.uint32)
+    rturn = np.empty((M, K), dtype=np.int32)
+    nn_ = np.empty(M, dtype=np.int32)
+    nr = np.empty(M, dtype=np.int32)
+    _check(lib().rb_dedup_batch(handles, len(sessions), _np_ptr(ts), _np_ptr(ids), _np_ptr(lens_a), M, K,
+                                _np_ptr(novel), _np_ptr(nn_), _np_ptr(rdoc), _np_ptr(rturn), _np_ptr(nr)))
+    return novel, nn_, rdoc, rturn, nr
 
 
 def index_from_linkage(ids, a, b, h, size, lens=None) -> Index:

@@ -248,3 +248,57 @@ def test_full_size_configs(name):
     # tree/order: host step re-run from the device merge order == library result
     idx2 = F.index_from_linkage(w.ids, a, b, h, s)
     assert np.array_equal(idx2.order_contexts()[0], out)
+
+
+@pytest.mark.parametrize("mode", ["0", "1"])
+@pytest.mark.parametrize("case", ["C2", "var", "ties"])
+def test_round_strategy(mode, case, monkeypatch):
+    """Linkage rounds in place (RAGB_INPLACE=1, forced wherever allowed) or
+    always compacting (0) give the oracle's merge order (the strategy is an
+    implementation choice, X7-X9 fix the result)."""
+    monkeypatch.setenv("RAGB_INPLACE", mode)
+    if case == "C2":
+        check_full(config("C2").ids, counts=False)
+    elif case == "var":
+        w = generate(2500, 12, 6000, 31, len_min=2)
+        check_full(w.ids, w.lens, counts=False)
+    else:  # tie-heavy: tiny pool, short lists -> many equal heights and cliques
+        w = generate(3000, 4, 300, 32)
+        check_full(w.ids, counts=False)
+
+
+def test_round_strategy_full_size(monkeypatch):
+    """At C4 size (level cliques above 4096 vertices, block path) the merge
+    order and the document order do not depend on the round strategy."""
+    ids = config("C4").ids
+    t = torch.from_numpy(ids.view(np.int32)).cuda()
+    res = []
+    for mode in ("0", "2"):
+        monkeypatch.setenv("RAGB_INPLACE", mode)
+        idx, ws = F.build_index(t)
+        res.append((idx.linkage(), idx.order_contexts()))
+        del idx, ws
+        torch.cuda.empty_cache()
+    for x, y in zip(res[0][0] + res[0][1], res[1][0] + res[1][1]):
+        assert np.array_equal(x, y)
+
+
+def test_multiturn_cumulative_index():
+    """NEXT-2: sessions' cumulative contexts (turn-0 ++ novel docs) are
+    variable-length (X4); their index on the GPU equals the oracle's."""
+    w = generate(6000, 10, 9000, 12, turns=4)
+    t0 = {int(w.session[i]): i for i in range(w.N) if w.turn[i] == 0}
+    sids = sorted(t0)
+    pos = {s: q for q, s in enumerate(sids)}
+    sess = [F.Session.from_docs(w.ids[t0[s]]) for s in sids]
+    follow = sorted((int(w.turn[i]), i) for i in range(w.N) if w.turn[i] > 0)
+    rows = np.array([i for _, i in follow], dtype=np.int64)
+    F.dedup_batch(sess, np.array([pos[int(w.session[i])] for i in rows]), w.ids[rows])
+    ctxs = [s.context() for s in sess]
+    Kc = max(len(c) for c in ctxs)
+    ids = np.zeros((len(ctxs), Kc), dtype=np.uint32)
+    lens = np.array([len(c) for c in ctxs], dtype=np.uint8)
+    for q, c in enumerate(ctxs):
+        ids[q, :len(c)] = c
+    assert lens.max() > 10
+    check_full(ids, lens, counts=False)
