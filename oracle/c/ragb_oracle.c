@@ -230,3 +230,81 @@ int ro_linkage_nnchain(float *d, int64_t N, int32_t *za, int32_t *zb, float *zh,
   free(active); free(size); free(chain); free(Z);
   return 0;
 }
+
+/* NEXT-3 ("iteratively merge the closest pair, creating
+ * a virtual node whose context is the sorted intersection", read as SPEC:177):
+ * the merged cluster is represented by the ascending sorted intersection of
+ * its two representatives; cluster distance = Eq. 1 between representatives
+ * (positions = list index).  Greedy: each step merges the active pair with the
+ * smallest key (d, min rep, max rep) (X8); the survivor keeps the smaller rep.
+ * Plain O(N^2) scan per step over a full matrix; merges in greedy order.
+ * ctx: [N][K] contexts (row-major; lens[i] or K docs); d: [N][N] Eq. 1 matrix of
+ * the contexts (overwritten). */
+int ro_linkage_intersection(const uint32_t *ids, const uint8_t *lens, int64_t N, int32_t K, uint32_t an,
+                            uint32_t ad, float *d, int32_t *za, int32_t *zb, float *zh, int32_t *zsize) {
+  if (N < 1 || K < 1 || K > 255 || ad == 0) return -1;
+  uint32_t *ctx = (uint32_t *)malloc((size_t)N * K * 4);
+  int *len = (int *)malloc((size_t)N * sizeof(int));
+  int *size = (int *)malloc((size_t)N * sizeof(int));
+  unsigned char *act = (unsigned char *)malloc((size_t)N);
+  if (!ctx || !len || !size || !act) return -2;
+  for (int64_t i = 0; i < N; ++i) {
+    len[i] = lens ? lens[i] : K;
+    for (int k = 0; k < len[i]; ++k) ctx[i * K + k] = ids[i * K + k];
+    size[i] = 1;
+    act[i] = 1;
+  }
+  for (int64_t t = 0; t + 1 < N; ++t) {
+    int64_t ba = -1, bb = -1;
+    float bh = 0.0f;
+    for (int64_t i = 0; i < N; ++i) {
+      if (!act[i]) continue;
+      for (int64_t j = i + 1; j < N; ++j) {
+        if (!act[j]) continue;
+        float v = d[i * N + j];
+        if (ba < 0 || v < bh) { /* strict: the first (i, j) in index order wins ties */
+          ba = i;
+          bb = j;
+          bh = v;
+        }
+      }
+    }
+    /* representative of the merged cluster: sorted intersection */
+    uint32_t tmp[256];
+    int n = 0;
+    for (int p = 0; p < len[ba]; ++p)
+      for (int q = 0; q < len[bb]; ++q)
+        if (ctx[ba * K + p] == ctx[bb * K + q]) tmp[n++] = ctx[ba * K + p];
+    for (int x = 1; x < n; ++x) { /* insertion sort, ascending DocId */
+      uint32_t v = tmp[x];
+      int y = x;
+      while (y > 0 && tmp[y - 1] > v) {
+        tmp[y] = tmp[y - 1];
+        --y;
+      }
+      tmp[y] = v;
+    }
+    for (int x = 0; x < n; ++x) ctx[ba * K + x] = tmp[x];
+    len[ba] = n;
+    act[bb] = 0;
+    size[ba] += size[bb];
+    za[t] = (int32_t)ba;
+    zb[t] = (int32_t)bb;
+    zh[t] = bh;
+    zsize[t] = size[ba];
+    for (int64_t j = 0; j < N; ++j) { /* the survivor's new distances */
+      if (!act[j] || j == ba) continue;
+      uint32_t s, D;
+      overlap_pair(ctx + ba * K, len[ba], ctx + j * K, len[j], &s, &D);
+      uint32_t m = (uint32_t)(len[ba] > len[j] ? len[ba] : len[j]);
+      float v = ro_eq1(s, D, m, an, ad);
+      d[ba * N + j] = v;
+      d[j * N + ba] = v;
+    }
+  }
+  free(ctx);
+  free(len);
+  free(size);
+  free(act);
+  return 0;
+}

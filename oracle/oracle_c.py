@@ -42,6 +42,7 @@ def lib():
         L.ro_row_nn.argtypes = [P, i64, i64, i64, P, P]
         L.ro_row_nn.restype = ctypes.c_int
         L.ro_linkage_nnchain.argtypes = [P, i64, P, P, P, P]
+        L.ro_linkage_intersection.argtypes = [P, P, i64, i32, u32, u32, P, P, P, P, P]
         L.ro_linkage_nnchain.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -99,4 +100,22 @@ def linkage(d):
     rc = lib().ro_linkage_nnchain(_p(d), N, _p(a), _p(b), _p(h), _p(sz))
     if rc != 0:
         raise ValueError(f"ro_linkage_nnchain rc={rc}")
+    return a, b, h, sz
+
+
+def linkage_intersection(ids, lens, alpha_num, alpha_den):
+    """NEXT-3 greedy intersection-representative linkage (merge order)."""
+    ids = np.ascontiguousarray(ids, dtype=np.uint32)
+    N, K = ids.shape
+    lens_a = None if lens is None else np.ascontiguousarray(lens, dtype=np.uint8)
+    d = pairwise_rows(ids, lens_a, alpha_num, alpha_den)
+    d = np.array(d, dtype=np.float32, order="C", copy=True)
+    a = np.empty(max(N - 1, 0), dtype=np.int32)
+    b = np.empty_like(a)
+    h = np.empty(max(N - 1, 0), dtype=np.float32)
+    sz = np.empty_like(a)
+    rc = lib().ro_linkage_intersection(_p(ids), _p(lens_a) if lens_a is not None else None, N, K, alpha_num,
+                                       alpha_den, _p(d), _p(a), _p(b), _p(h), _p(sz))
+    if rc != 0:
+        raise ValueError(f"ro_linkage_intersection rc={rc}")
     return a, b, h, sz

@@ -224,6 +224,37 @@ def linkage_nn_chain(d: np.ndarray):
     return Z
 
 
+def linkage_intersection(ctxs, alpha: Fraction):
+    """NEXT-3: "iteratively merge the closest pair,
+    creating a virtual node whose context is the sorted intersection" read as
+    SPEC:177 — the merged cluster is represented by the ascending sorted
+    intersection of its two representatives, and cluster distance is Eq. 1
+     between representatives (positions = index in the list:
+    retrieval order for a leaf, ascending DocId for a virtual node).  Greedy
+    with the X8 key (d, min rep, max rep); the survivor keeps the smaller rep.
+    The linkage is not reducible (a later merge can be lower), so the merge
+    list is in merge order, not sorted by height.  Brute force: every step
+    recomputes every active pair — small N only."""
+    rep_ctx = {i: list(c) for i, c in enumerate(ctxs)}
+    size = {i: 1 for i in rep_ctx}
+    Z = []
+    while len(rep_ctx) > 1:
+        keys = sorted(rep_ctx)
+        best = None
+        for x in range(len(keys)):
+            for y in range(x + 1, len(keys)):
+                a, b = keys[x], keys[y]
+                k = (distance(rep_ctx[a], rep_ctx[b], alpha), a, b)
+                if best is None or k < best:
+                    best = k
+        h, a, b = best
+        rep_ctx[a] = sorted(set(rep_ctx[a]) & set(rep_ctx[b]))
+        del rep_ctx[b]
+        size[a] += size.pop(b)
+        Z.append((a, b, np.float32(h), size[a]))
+    return Z
+
+
 def cluster_height(d: np.ndarray, A, B) -> np.float32:
     """Complete-linkage distance by its definition: max over member pairs."""
     return np.float32(max(d[a, b] for a in A for b in B))

@@ -120,3 +120,75 @@ def test_medium_c_vs_numpy_chain():
     w = generate(600, 10, 3000, 3)
     d = oc.pairwise_rows(w.ids, None, 1, 200)
     assert c_linkage(d) == z_tuples(o.linkage_nn_chain(d))
+
+
+# --------------------------------------------------------------- NEXT-3 oracle
+def _reps_from_members(ctxs, members):
+    """Representative of a cluster from its member leaves: the leaf itself
+    (retrieval order) for a singleton, else the ascending sorted intersection
+    of all member sets (associativity of the pairwise rule)."""
+    if len(members) == 1:
+        return list(ctxs[next(iter(members))])
+    s = set(ctxs[next(iter(members))])
+    for m in members:
+        s &= set(ctxs[m])
+    return sorted(s)
+
+
+def test_intersection_fig4(golden):
+    ctxs = golden["fig4_build"]["contexts"]
+    Z = o.linkage_intersection(ctxs, A200)
+    assert [(a, b, s) for a, b, _, s in Z] == [(0, 1, 2), (0, 2, 3)]
+    assert Z[0][2] == np.float32(403 / 1200)   # C1, C2 (PAPER:337)
+    # C3 vs the virtual node {1,2}: s=1, positions 1 / 0, m=3 -> 1-1/3+1/200 = 403/600
+    assert Z[1][2] == o.rn32(Fraction(403, 600))
+
+
+def test_intersection_identical_unsorted():
+    # identical leaves are at 0; a virtual node is the SORTED set, which is at
+    # alpha*footrule/K > 0 from an unsorted leaf: leaves pair up first
+    ctxs = [[3, 1, 2]] * 4
+    Z = o.linkage_intersection(ctxs, A200)
+    assert [(a, b, float(h), s) for a, b, h, s in Z] == [(0, 1, 0.0, 2), (2, 3, 0.0, 2), (0, 2, 0.0, 4)]
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_intersection_python_vs_c(seed):
+    rng = np.random.default_rng(seed)
+    N = int(rng.integers(2, 36))
+    K = int(rng.integers(2, 8))
+    w = generate(N, K, int(rng.integers(K + 1, 4 * K + 8)), 1000 + seed)
+    lens = None
+    if seed % 3 == 0:
+        lens = rng.integers(1, K + 1, size=N).astype(np.uint8)
+    ctxs = o.validate(w.ids, lens)
+    Zp = o.linkage_intersection(ctxs, A200)
+    a, b, h, s = oc.linkage_intersection(w.ids, lens, 1, 200)
+    assert [(x[0], x[1], x[3]) for x in Zp] == list(zip(a.tolist(), b.tolist(), s.tolist()))
+    assert np.array_equal(np.array([x[2] for x in Zp], dtype=np.float32).view(np.uint32), h.view(np.uint32))
+    # definition check: replay; every merge is the minimum key over the active
+    # clusters, with distances recomputed from the member leaves
+    members = {i: {i} for i in range(N)}
+    for (ma, mb, mh, ms) in Zp:
+        best = min((o.distance(_reps_from_members(ctxs, members[x]), _reps_from_members(ctxs, members[y]), A200), x, y)
+                   for x in members for y in members if x < y)
+        assert best == (mh, ma, mb)
+        members[ma] |= members.pop(mb)
+        assert len(members[ma]) == ms
+
+
+def test_intersection_is_not_reducible():
+    """Some run has a later merge lower than an earlier one, which
+    complete linkage never has: the two readings are really different."""
+    found = False
+    for seed in range(30):
+        w = generate(24, 5, 30, 2000 + seed)
+        a, b, h, s = oc.linkage_intersection(w.ids, None, 1, 200)
+        if np.any(np.diff(h) < 0):
+            found = True
+            ctxs = o.validate(w.ids)
+            t = o.build_tree(ctxs, list(zip(a.tolist(), b.tolist(), h.tolist(), s.tolist())))
+            for i in range(24):  # the tree still replays
+                assert o.traverse(t, t.path[i]) == t.leaf_node[i]
+            break
+    assert found
