@@ -63,8 +63,15 @@ enum rb_status_code {
 
 /* Linkage: the paper says only "iteratively merge the closest pair"
  * (PAPER:335).  X7: complete linkage on the Eq. 1 matrix, tie key
- * (d, min rep, max rep), rep = smallest leaf index (X8). */
-enum rb_linkage { RB_LINK_COMPLETE = 0 };
+ * (d, min rep, max rep), rep = smallest leaf index (X8); merges exported in
+ * ascending key order (X9).
+ * RB_LINK_INTERSECTION (NEXT-3, the SPEC:177 reading): a merged cluster is
+ * represented by the ascending sorted intersection of its two representatives
+ * ("a virtual node whose context is the sorted intersection") and
+ * cluster distances are Eq. 1 between representatives; same tie key.  It is
+ * not reducible (heights can decrease), so merges are computed sequentially
+ * (N-1 greedy steps on the device) and exported in merge order. */
+enum rb_linkage { RB_LINK_COMPLETE = 0, RB_LINK_INTERSECTION = 1 };
 
 enum rb_flags {
   RB_EMIT_COUNTS = 1u << 0,   /* also write s_ij (uint8) and the positional sum

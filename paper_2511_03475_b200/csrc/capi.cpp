@@ -64,7 +64,8 @@ rb_status check_params(int64_t N, int32_t K, const rb_params *p, int64_t *row0, 
     const uint64_t n = p->alpha_num, d = p->alpha_den;
     if (n * 1000 < d || n * 100 > d) return fail(RB_EALPHA, "alpha outside [0.001, 0.01]");
   }
-  if (p->linkage != RB_LINK_COMPLETE) return fail(RB_EINVAL, "unknown linkage");
+  if (p->linkage != RB_LINK_COMPLETE && p->linkage != RB_LINK_INTERSECTION)
+    return fail(RB_EINVAL, "unknown linkage");
   *row0 = p->row0;
   *nrows = p->nrows < 0 ? N - p->row0 : p->nrows;
   if (*row0 < 0 || *nrows < 1 || *row0 + *nrows > N) return fail(RB_EINVAL, "bad row range");
@@ -111,7 +112,8 @@ ScratchLayout ScratchLayout::make(int64_t N, int32_t K, bool keep_rows, bool lin
     L.amask = take(o, (size_t)(N / 32 + 1) * 4);
     L.mlist = take(o, (size_t)N * 4);
     // compacted matrices: at most (N-1) rows with a leading dimension padded to 4
-    const size_t mat = (size_t)(N - 1) * (size_t)((N + 2) & ~3ll) * 4;
+    // (also holds an N x N copy for the intersection linkage with RB_KEEP_ROWS)
+    const size_t mat = std::max((size_t)(N - 1) * (size_t)((N + 2) & ~3ll), (size_t)N * N) * 4;
     L.matA = take(o, mat);
     L.matB = keep_rows ? take(o, mat) : 0;
   }
@@ -279,7 +281,25 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
   // ---- a5 (device) with the a6 replay pipelined on a host worker ------------
   ragb::LinkageOut lo;
   ragb::TreeBuild T;
-  if (linkage) {
+  const bool intersection = linkage && p->linkage == RB_LINK_INTERSECTION;
+  if (intersection) {  // NEXT-3: sequential greedy merges in one cooperative kernel
+    H.za.assign(N - 1, 0);
+    H.zb.assign(N - 1, 0);
+    H.zh.assign(N - 1, 0.0f);
+    H.zs.assign(N - 1, 0);
+    H.sort_merges = false;
+    float *mat = rows_dev;
+    if (keep_rows && N > 1) {
+      mat = reinterpret_cast<float *>(sc + L.matA);
+      RB_CUDA(cudaMemcpyAsync(mat, rows_dev, (size_t)N * N * 4, cudaMemcpyDeviceToDevice, st), "copy rows");
+    }
+    RB_CUDA(ragb::run_linkage_intersection(mat, N, N, K, Npad, idsT, lens_d, da.nnkey, p->alpha_num,
+                                           p->alpha_den, scratch_dev, L, st, H.za.data(), H.zb.data(),
+                                           H.zh.data(), H.zs.data(), &launches),
+            "intersection linkage");
+    lo.rounds = (int)(N - 1);
+    ragb::host_begin(H, T);
+  } else if (linkage) {
     H.za.assign(N - 1, 0);
     H.zb.assign(N - 1, 0);
     H.zh.assign(N - 1, 0.0f);

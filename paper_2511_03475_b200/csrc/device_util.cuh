@@ -7,6 +7,31 @@
 
 namespace ragb {
 
+// Correctly rounded fp32 of num/den (X6).  num, den < 2^24: both exact in
+// fp32 and IEEE division is correctly rounded.  Otherwise den < 2^29 holds for
+// every admissible input (ad <= 1000, m, s <= 255), and RN32(RN64(q)) == RN32(q)
+// because |q - midpoint| >= 1/(den*2^(24-e)) > ulp64(q)/2.
+__device__ __forceinline__ float rn32_ratio(uint64_t num, uint64_t den) {
+  if (((num | den) >> 24) == 0) return __fdiv_rn((float)(uint32_t)num, (float)(uint32_t)den);
+  return __double2float_rn(__ddiv_rn((double)num, (double)den));
+}
+
+// Eq. 1 from exact counts, branch-free in s: the quotient is evaluated with
+// s clamped to >= 1 and replaced by 1.0f (X3) when s == 0.  A data-dependent
+// `if (s == 0)` inside the finalize loop made the sm_100a build fault
+// intermittently (a lane split off its warp while the loop counter lives in a
+// warp-shared uniform register), so every
+// per-lane decision in the finalize is a select.
+__device__ __forceinline__ float eq1_from_counts(uint32_t s, uint32_t D, uint32_t m, uint32_t an,
+                                                 uint32_t ad) {
+  const uint32_t ss = s > 0u ? s : 1u;
+  const uint64_t num = (uint64_t)(m - ss) * ad * ss + (uint64_t)an * D * m;
+  const uint64_t den = (uint64_t)ad * m * ss;
+  const float q = rn32_ratio(num, den);
+  return s == 0u ? 1.0f : q;
+}
+
+
 // Multiplicative hash of a DocId into a 2^logT table.
 __device__ __forceinline__ uint32_t hash_slot(uint32_t x, int logT) {
   return (x * 0x9E3779B1u) >> (32 - logT);

@@ -214,8 +214,9 @@ rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg) {
 
   // ---- exported merge order: ascending key (X9), sorted on a side thread
   //      while the tree is built (the tree reads the replay order) ---------
-  std::vector<MergeKey> zk(nz);
+  std::vector<MergeKey> zk(H.sort_merges ? nz : 0);
   std::thread sorter([&] {
+    if (!H.sort_merges) return;  // non-reducible linkage: keep the merge order
     for (int64_t t = 0; t < nz; ++t) zk[t] = {H.zh[t], H.za[t], H.zb[t], H.zs[t]};
     std::sort(zk.begin(), zk.end(), key_less);
   });
@@ -394,7 +395,7 @@ rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg) {
   lap("schedule");
 
   sorter.join();
-  for (int64_t t = 0; t < nz; ++t) {
+  for (int64_t t = 0; t < (int64_t)zk.size(); ++t) {
     H.za[t] = zk[t].a;
     H.zb[t] = zk[t].b;
     H.zh[t] = zk[t].h;

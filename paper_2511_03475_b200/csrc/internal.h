@@ -78,6 +78,15 @@ struct LinkageOut {
 // dependency-respecting order, round by round; on_round(upto) is called after
 // each round with the number of merges available so far (used to pipeline the
 // host tree build with the device rounds; may be empty).
+// NEXT-3: intersection-representative linkage (ilinkage.cu); rows [N][ld] are
+// updated in place, ctxT [K][Npad] holds the contexts (updated in place),
+// merges come back to the host arrays in greedy (merge) order.
+cudaError_t run_linkage_intersection(float *rows, int64_t ld, int64_t N, int32_t K, int64_t Npad,
+                                     uint32_t *ctxT, const uint8_t *lens, unsigned long long *nnkey,
+                                     uint32_t an, uint32_t ad, void *scratch, const ScratchLayout &L,
+                                     cudaStream_t st, int32_t *za, int32_t *zb, float *zh, int32_t *zs,
+                                     int *launches);
+
 cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void *scratch,
                         const ScratchLayout &L, bool keep_rows, cudaStream_t st, int32_t *za,
                         int32_t *zb, float *zh, int32_t *zs, LinkageOut *out, int *launches,
@@ -111,7 +120,8 @@ struct HostIndex {
   std::vector<uint8_t> prefix_len;  // [N]
   std::vector<int64_t> schedule;    // [N]
   rb_stats stats{};
-  uint32_t alpha_num = 1, alpha_den = 200;  // Eq. 1 alpha of the build (X1)
+  uint32_t alpha_num = 1, alpha_den = 200;
+  bool sort_merges = true;  // complete linkage: export ascending key (X9); intersection: merge order
   std::shared_ptr<DynTree> dyn;             // set by the first online update
 };
 

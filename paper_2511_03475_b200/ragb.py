@@ -20,6 +20,7 @@ LIB_PATH = os.path.join(_PKG, "lib", f"libragb_{os.environ['RAGB_LIB']}.so" if o
 RB_OK, RB_EINVAL, RB_EDUPDOC, RB_EALPHA, RB_ENOMEM, RB_ECUDA, RB_ENCCL, RB_EPATH, RB_ESESSION, \
     RB_ESTATE = 0, -1, -2, -3, -4, -5, -6, -7, -8, -9
 RB_EMIT_COUNTS, RB_ALPHA_ANY, RB_KEEP_ROWS, RB_SKIP_LINKAGE = 1, 2, 4, 8
+RB_LINK_COMPLETE, RB_LINK_INTERSECTION = 0, 1
 
 STATUS_NAMES = {0: "RB_OK", -1: "RB_EINVAL", -2: "RB_EDUPDOC", -3: "RB_EALPHA", -4: "RB_ENOMEM",
                 -5: "RB_ECUDA", -6: "RB_ENCCL", -7: "RB_EPATH", -8: "RB_ESESSION", -9: "RB_ESTATE"}
@@ -123,10 +124,11 @@ def alpha_rational(alpha) -> tuple[int, int]:
     return f.numerator, f.denominator
 
 
-def make_params(alpha=(1, 200), flags=0, stream=None, row0=0, nrows=-1) -> Params:
+def make_params(alpha=(1, 200), flags=0, stream=None, row0=0, nrows=-1, linkage=RB_LINK_COMPLETE) -> Params:
     p = Params()
     _check(lib().rb_params_init(ctypes.byref(p)))
     p.alpha_num, p.alpha_den = alpha_rational(alpha)
+    p.linkage = linkage
     p.flags = flags
     p.stream = stream
     p.row0 = row0
@@ -333,7 +335,7 @@ def _stream_ptr(stream):
 
 
 def build_index(ids, lens=None, *, alpha=(1, 200), flags=0, row0=0, nrows=-1, stream=None,
-                workspace: Workspace | None = None):
+                workspace: Workspace | None = None, linkage=RB_LINK_COMPLETE):
     """Build the context index from device ids (torch.int32/uint32 CUDA tensor [N, K]).
 
     Returns (Index, Workspace); workspace.rows holds the distance rows (unless
@@ -345,7 +347,7 @@ def build_index(ids, lens=None, *, alpha=(1, 200), flags=0, row0=0, nrows=-1, st
         raise TypeError("ids must be int32/uint32 (bit pattern of uint32 DocIds)")
     ids = ids.contiguous()
     N, K = ids.shape
-    p = make_params(alpha, flags, _stream_ptr(stream), row0, nrows)
+    p = make_params(alpha, flags, _stream_ptr(stream), row0, nrows, linkage)
     ws = workspace or Workspace(N, K, p, device=ids.device)
     if lens is not None:
         lens = lens.contiguous()
@@ -360,11 +362,11 @@ def build_index(ids, lens=None, *, alpha=(1, 200), flags=0, row0=0, nrows=-1, st
 
 
 def build_index_host(ids, lens=None, *, alpha=(1, 200), flags=0, stream=None,
-                     workspace: Workspace | None = None):
+                     workspace: Workspace | None = None, linkage=RB_LINK_COMPLETE):
     """End-to-end entry: ids/lens are host numpy arrays; H2D happens inside."""
     ids = np.ascontiguousarray(ids, dtype=np.uint32)
     N, K = ids.shape
-    p = make_params(alpha, flags, _stream_ptr(stream))
+    p = make_params(alpha, flags, _stream_ptr(stream), linkage=linkage)
     ws = workspace or Workspace(N, K, p)
     lens_a = None if lens is None else np.ascontiguousarray(lens, dtype=np.uint8)
     out = ctypes.c_void_p()

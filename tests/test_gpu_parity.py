@@ -302,3 +302,45 @@ def test_multiturn_cumulative_index():
         ids[q, :len(c)] = c
     assert lens.max() > 10
     check_full(ids, lens, counts=False)
+
+
+def check_intersection(ids, lens=None, flags=F.RB_KEEP_ROWS):
+    """NEXT-3: device intersection-representative linkage vs the C oracle
+    (merge order, heights bit-exact), then the tree / order / schedule the
+    merges imply (build_tree replays merges in merge order)."""
+    N, K = ids.shape
+    idx, ws = dev_build(ids, lens, flags=flags, linkage=F.RB_LINK_INTERSECTION)
+    a, b, h, s = idx.linkage()
+    za, zb, zh, zs = oc.linkage_intersection(ids, lens, 1, 200)
+    assert np.array_equal(a, za) and np.array_equal(b, zb) and np.array_equal(s, zs)
+    assert np.array_equal(h.view(np.uint32), zh.view(np.uint32))
+    ctxs = o.validate(ids, lens)
+    t = o.build_tree(ctxs, list(zip(za.tolist(), zb.tolist(), zh.tolist(), zs.tolist())))
+    assert idx.paths() == t.path
+    ordered, plen = o.offline_order(ctxs, t)
+    out, pl, sc = idx.order_contexts()
+    for i in range(N):
+        L = K if lens is None else int(lens[i])
+        assert out[i, :L].tolist() == ordered[i]
+    assert pl.tolist() == plen and sc.tolist() == o.schedule(t.path)
+    if flags & F.RB_KEEP_ROWS:  # the distance rows are untouched
+        dref = oc.pairwise_rows(ids, lens, 1, 200)
+        assert np.array_equal(ws.rows.cpu().numpy().view(np.uint32), dref.view(np.uint32))
+
+
+def test_intersection_fig4(golden):
+    ids = np.array(golden["fig4_build"]["contexts"], dtype=np.uint32)
+    check_intersection(ids)
+
+
+@pytest.mark.parametrize("N,K,V,seed", [(64, 5, 200, 1), (1, 4, 10, 2), (2, 4, 10, 3), (37, 3, 20, 4),
+                                        (500, 8, 1500, 5), (1500, 10, 4000, 6), (700, 4, 80, 7)])
+def test_intersection_linkage(N, K, V, seed):
+    w = generate(N, K, V, seed)
+    check_intersection(w.ids)
+
+
+def test_intersection_variable_lengths_and_consumed_rows():
+    w = generate(900, 12, 2500, 8, len_min=2)
+    check_intersection(w.ids, w.lens)
+    check_intersection(w.ids, w.lens, flags=0)
