@@ -63,45 +63,79 @@ def workload_desc(name, w):
 
 # ------------------------------------------------------------------ clocks
 class Clocks:
-    def __init__(self, index):
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+    """SM clocks and throttle reasons sampled DURING the timed region.  In-process
+    NVML on a thread (a polling nvidia-smi process competed with the host
+    stage for CPU and driver locks and slowed the measured build by ~20%);
+    nvidia-smi is the fallback when NVML is unavailable."""
+
+    NAMES = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+             "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+             "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+             "sw_power_cap": "nvmlClocksEventReasonSwPowerCap"}
+
+    def __init__(self, index, period_s=0.05):
+        import threading
+        self.sm, self.mx, self.reasons = [], [], set()
+        self.stop_ev = threading.Event()
         self.p = None
+        self.t = None
         try:
-            self.p = subprocess.Popen(
-                ["nvidia-smi", f"--id={index}",
-                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
-        except FileNotFoundError:
-            self.p = None
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            bits = {nm: getattr(pynvml, attr) for nm, attr in self.NAMES.items()}
+
+            def loop():
+                while not self.stop_ev.is_set():
+                    try:
+                        self.sm.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+                        self.mx.append(float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)))
+                        r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.reasons.update(nm for nm, b in bits.items() if r & b)
+                    except pynvml.NVMLError:
+                        pass
+                    self.stop_ev.wait(period_s)
+
+            self.t = threading.Thread(target=loop, daemon=True)
+            self.t.start()
+        except Exception:  # no NVML: nvidia-smi fallback
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            try:
+                self.p = subprocess.Popen(
+                    ["nvidia-smi", f"--id={index}",
+                     "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                     "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                     "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                     "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+            except FileNotFoundError:
+                self.p = None
 
     def stop(self):
-        if self.p is None:
+        if self.t is not None:
+            self.stop_ev.set()
+            self.t.join()
+        elif self.p is not None:
+            self.p.terminate()
+            self.p.wait()
+            self.f.flush()
+            self.f.seek(0)
+            for line in self.f.read().splitlines():
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 8:
+                    continue
+                try:
+                    self.sm.append(float(parts[0]))
+                    self.mx.append(float(parts[1]))
+                except ValueError:
+                    continue
+                for nm, v in zip(self.NAMES, parts[4:8]):
+                    if v.lower() in ("active", "1"):
+                        self.reasons.add(nm)
+            os.unlink(self.f.name)
+        if not self.sm:
             return None
-        self.p.terminate()
-        self.p.wait()
-        self.f.flush()
-        self.f.seek(0)
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.f.read().splitlines():
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[4:8]):
-                if v.lower() in ("active", "1"):
-                    reasons.add(nm)
-        os.unlink(self.f.name)
-        if not sm:
-            return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "samples": len(sm),
-                "reasons": sorted(reasons)}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": max(self.mx), "samples": len(self.sm),
+                "reasons": sorted(self.reasons), "sampler": "nvml" if self.t is not None else "nvidia-smi"}
 
 
 # ------------------------------------------------------------------ oracle timing
@@ -240,14 +274,29 @@ def run_ours(args, ws, rank, local):
     hbm = peaks.get("hbm_gbs")
     peak_src = "measured (MEASURED_PEAKS.json hbm_gbs, copy)" if hbm else "fallback 6650 GB/s (B200_PROFILING.md)"
     hbm = hbm or 6650.0
-    # dominant kernel: the distance kernel (a2-a4) vs the linkage (a5)
+    # rooflines: the distance kernel (a2-a4) and the linkage compaction kernel
+    # (a5, k_merge_rows: every launch reads the live rows of the old matrix and
+    # writes the new one); "roofline" is the one with the larger step share
     dist_bytes = 4.0 * N * N + 4.0 * N * K   # full fp32 rows written + ids read (algorithmic)
     dist_gbs = dist_bytes / (mean["distance_ms"] * 1e-3) / 1e9
     traffic = load_traffic(args.config)
-    roofline = {"kernel": "k_dist_tile (a2-a4, distance rows + fused row NN)", "bound": "hbm", "achieved": dist_gbs, "peak": hbm,
-                "unit": "GB/s", "frac": dist_gbs / hbm, "traffic": traffic, "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": dist_bytes,
-                "share_of_step": mean["distance_ms"] / ms}
+    roof_dist = {"kernel": "k_dist_tile (a2-a4, distance rows + fused row NN)", "bound": "hbm",
+                 "achieved": dist_gbs, "peak": hbm, "unit": "GB/s", "frac": dist_gbs / hbm,
+                 "traffic": traffic.get("k_dist_tile") if traffic else None, "peak_source": peak_src,
+                 "algorithmic_bytes_per_launch": dist_bytes, "launches_per_step": 1,
+                 "share_of_step": mean["distance_ms"] / ms}
+    mb = mean["merge_bytes"] / max(mean["merge_launches"], 1)
+    merge_gbs = mean["merge_bytes"] / (mean["merge_ms"] * 1e-3) / 1e9 if mean["merge_ms"] > 0 else 0.0
+    roof_merge = {"kernel": "k_merge_rows (a5, linkage compaction rounds)", "bound": "hbm",
+                  "achieved": merge_gbs, "peak": hbm, "unit": "GB/s", "frac": merge_gbs / hbm,
+                  "traffic": traffic.get("k_merge_rows") if traffic else None, "peak_source": peak_src,
+                  "algorithmic_bytes_per_launch": mb, "launches_per_step": mean["merge_launches"],
+                  "algorithmic_bytes_note": "4 B x (live old rows^2 + new rows^2) per launch, averaged",
+                  "share_of_step": mean["merge_ms"] / ms}
+    if roof_merge["share_of_step"] >= roof_dist["share_of_step"]:
+        roofline, roofline_other = roof_merge, roof_dist
+    else:
+        roofline, roofline_other = roof_dist, roof_merge
     line = {
         "metric": f"context-pair distances/s (index build, N={N}, K={K})",
         "value": pairs * ws / (ms * 1e-3),
@@ -263,6 +312,7 @@ def run_ours(args, ws, rank, local):
         "distance_pairs_per_s": pairs / (mean["distance_ms"] * 1e-3),
         "linkage_rounds": mean["linkage_rounds"],
         "roofline": roofline,
+        "roofline_other": roofline_other,
         "e2e": {"value": pairs * ws / (e2e_ms * 1e-3), "unit": "context-pairs/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": int(N * K * 4),
                 "d2h_bytes_per_step": int(N * 8 + 16 * (N - 1) + 8)},
@@ -289,9 +339,9 @@ def load_peaks():
 
 
 def load_traffic(cfg):
-    """dram read+write bytes per launch of the distance kernel from the committed
-    ncu --set full capture (profiles/), or None."""
-    path = os.path.join(ROOT, "profiles", "ncu_distance_traffic.json")
+    """dram read+write bytes per launch (per kernel) from the committed
+    ncu --set full captures under profiles/, or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
             d = json.load(f)

@@ -103,6 +103,9 @@ typedef struct rb_stats {
   int32_t kernel_launches;/* kernels launched by this call                         */
   int64_t n_virtual;      /* virtual (intersection) nodes kept after collapse      */
   int64_t max_depth;      /* maximum leaf path length                              */
+  float merge_ms;         /* CUDA-event time of the linkage compaction launches    */
+  int32_t merge_launches; /* number of compaction launches                         */
+  double merge_bytes;     /* their algorithmic bytes (live rows read, rows written)*/
 } rb_stats;
 
 typedef struct rb_index rb_index;

@@ -363,6 +363,9 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
   cudaEventElapsedTime(&ms, ev[2], ev[3]);
   H.stats.linkage_ms = ms;
   H.stats.linkage_rounds = lo.rounds;
+  H.stats.merge_ms = lo.merge_ms;
+  H.stats.merge_launches = lo.merge_launches;
+  H.stats.merge_bytes = lo.merge_bytes;
   H.stats.kernel_launches = launches;
 
   // ---- a6-a7: tree, orders, schedule (host) --------------------------------

@@ -71,6 +71,9 @@ cudaError_t launch_distance(const DistArgs &a, cudaStream_t st, int *launches);
 
 struct LinkageOut {
   int rounds = 0;
+  float merge_ms = 0.f;     // CUDA-event time of the compaction (k_merge_rows) launches
+  int merge_launches = 0;
+  double merge_bytes = 0;   // their algorithmic bytes: live old rows read + new rows written
 };
 
 // a5: complete linkage on the full rows (rows ld = N) starting from the fused

@@ -29,6 +29,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <functional>
+#include <vector>
 
 #include "internal.h"
 
@@ -1015,6 +1016,7 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
     for (auto &x : tev) cudaEventCreate(&x);
   int zprev = 0;
   int zdone = 0;
+  std::vector<cudaEvent_t> mev;  // [start, end] per compaction launch (merge_ms)
   while (live > 1) {
     if (trace) {
       cudaMemsetAsync(counters + 4, 0, 8 * sizeof(int), st);
@@ -1104,8 +1106,17 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
       int per_sm = 1;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nth, smem);
       const int grid = std::min<int>(Mn, sms * std::max(per_sm, 1));
+      cudaEvent_t me[2];
+      cudaEventCreate(&me[0]);
+      cudaEventCreate(&me[1]);
+      cudaEventRecord(me[0], st);
       kern<<<grid, nth, smem, st>>>(cur, ld, M, pa.Mn, pa.goff, pa.gmem, pa.colsrc, pa.cursor, W, next,
                                     key[p ^ 1]);
+      cudaEventRecord(me[1], st);
+      mev.push_back(me[0]);
+      mev.push_back(me[1]);
+      out->merge_bytes += 4.0 * ((double)live * live + (double)Mn * Mn);
+      ++out->merge_launches;
       ++*launches;
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
       cur = next;
@@ -1133,6 +1144,13 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
   }
   if (trace)
     for (auto &x : tev) cudaEventDestroy(x);
+  cudaStreamSynchronize(st);
+  for (size_t i = 0; i + 1 < mev.size(); i += 2) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, mev[i], mev[i + 1]);
+    out->merge_ms += ms;
+  }
+  for (auto &x : mev) cudaEventDestroy(x);
   if (zdone != N - 1) return cudaErrorUnknown;
   return cudaSuccess;
 }
