@@ -262,6 +262,51 @@ RB_API rb_status rb_dedup_batch(rb_session *const *sessions, int64_t S, const in
 /* Current turn number of a session (0 right after open). */
 RB_API rb_status rb_session_turn(const rb_session *s, int32_t *turn);
 
+/* ---- NEXT-4: cache events and a prefix-cache simulator --------------------
+ * Index update under cache events (Section 4.1 "Index
+ * update": a min-heap of active nodes by last access time; evicted tokens are
+ * "removed from the least recently used nodes by decrementing their token
+ * counts"; SPEC apply_cache_event).  kind RB_CACHE_APPENDED(path, n): n tokens
+ * cached at the node reached by path (host [path_len] child indices, as in
+ * rb_index_tree paths), access refreshed; RB_CACHE_ACCESSED(path): access
+ * refreshed; RB_CACHE_EVICTED(n): tokens taken from the nodes holding tokens
+ * in ascending (last access, node id), zero-clamped; a node left with no
+ * tokens and no children is detached from its parent (its later siblings'
+ * child indices shift by one), and so are ancestors left empty.  *taken (or
+ * NULL) receives the tokens actually evicted.  Detached contexts report an
+ * empty path; rb_index_tree reports parent -1 for detached nodes.
+ * Errors: RB_EPATH (invalid path), RB_EINVAL (n < 0, unknown kind), RB_ESTATE. */
+enum rb_cache_event_kind { RB_CACHE_APPENDED = 0, RB_CACHE_ACCESSED = 1, RB_CACHE_EVICTED = 2 };
+RB_API rb_status rb_index_cache_event(rb_index *idx, int32_t kind, const int32_t *path, int32_t path_len,
+                                      int64_t n_tokens, int64_t *taken);
+
+/* Per-node cache state after cache events: seq_len (host [n_nodes] or NULL;
+ * -1 for a detached node) and last access stamps (host [n_nodes] or NULL);
+ * n_nodes from rb_index_tree_info.  Errors: RB_ESTATE (no event applied). */
+RB_API rb_status rb_index_cache_state(const rb_index *idx, int64_t *seq_len, int64_t *last_access);
+
+/* Document-granularity prefix cache standing in for the inference engine
+ * (Section 2.1 "prefix cache ... trie-based implementation";
+ * SPEC cache_sim): a trie over DocId edges with a token budget.  A request's
+ * hit is its longest cached prefix, the rest is inserted, and
+ * least-recently-used leaves outside the request's path are evicted until the
+ * budget holds (ties: older node first).  Errors: RB_EINVAL (capacity <= 0,
+ * request larger than the capacity, token count <= 0), RB_EDUPDOC. */
+typedef struct rb_cache rb_cache;
+RB_API rb_status rb_cache_create(int64_t capacity_tokens, rb_cache **out);
+/* One request: docs host [n] in prefill order, doc_tokens host [n] or NULL (1
+ * token per doc); outputs hit / miss / evicted tokens. */
+RB_API rb_status rb_cache_prefill(rb_cache *c, const uint32_t *docs, int32_t n, const int32_t *doc_tokens,
+                                  int64_t *hit, int64_t *miss, int64_t *evicted);
+/* M requests (host ids [M][K], lens [M] or NULL) served in `order` (host [M],
+ * e.g. rb_order_contexts' schedule; NULL = input order), tokens_per_doc each;
+ * per-request outputs host [M] indexed by request. */
+RB_API rb_status rb_cache_prefill_batch(rb_cache *c, const uint32_t *ids, const uint8_t *lens,
+                                        const int64_t *order, int64_t M, int32_t K, int32_t tokens_per_doc,
+                                        int64_t *hit, int64_t *miss, int64_t *evicted);
+RB_API rb_status rb_cache_resident(const rb_cache *c, int64_t *tokens);
+RB_API void rb_cache_free(rb_cache *c);
+
 RB_API void rb_session_free(rb_session *s);
 RB_API void rb_index_free(rb_index *idx);
 

@@ -570,3 +570,175 @@ def traverse_online(idx: OnlineIndex, path):
     for step in path:
         k = idx.children[k][step]
     return k
+
+
+# ------------------------------------------------------------------ NEXT-4
+class PrefixCache:
+    """NEXT-4: document-granularity prefix cache standing in
+    for the inference engine (§2.1 "prefix cache that stores KV
+    caches from prior prompts", "trie-based implementation organizes tokens
+    hierarchically"; SPEC cache_sim).  A trie of DocId edges; a request's hit
+    is its longest cached prefix ("only the longest common prefix
+    ... can be reused"); the rest is inserted; least-recently-used leaves that
+    are not on the request's path are evicted until the token budget holds
+    (ties: older node first).  Tokens per doc default to 1."""
+
+    def __init__(self, capacity, tokens=None):
+        if capacity <= 0:
+            raise OracleError("capacity must be positive")
+        self.cap = capacity
+        self.tok = tokens or {}
+        self.children = [{}]     # node -> {doc: child}
+        self.parent = [-1]
+        self.doc = [None]
+        self.stamp = [0]
+        self.alive = [True]
+        self.clock = 0
+        self.resident = 0
+
+    def _t(self, d):
+        return self.tok.get(d, 1)
+
+    def prefill(self, docs):
+        """Returns (hit_tokens, miss_tokens, evicted_tokens)."""
+        docs = [int(x) for x in docs]
+        if len(set(docs)) != len(docs):
+            raise OracleError("duplicate DocId in request")
+        total = sum(self._t(d) for d in docs)
+        if total > self.cap:
+            raise OracleError("request exceeds capacity by %d" % (total - self.cap))
+        self.clock += 1
+        node, k = 0, 0
+        path = [0]
+        while k < len(docs) and docs[k] in self.children[node]:
+            node = self.children[node][docs[k]]
+            self.stamp[node] = self.clock
+            path.append(node)
+            k += 1
+        hit = sum(self._t(d) for d in docs[:k])
+        miss = total - hit
+        need = self.resident + miss - self.cap
+        evicted = 0
+        onpath = set(path)
+        while need > 0:
+            leaves = [v for v in range(1, len(self.parent)) if self.alive[v] and not self.children[v]
+                      and v not in onpath]
+            v = min(leaves, key=lambda x: (self.stamp[x], x))
+            self.alive[v] = False
+            del self.children[self.parent[v]][self.doc[v]]
+            t = self._t(self.doc[v])
+            self.resident -= t
+            evicted += t
+            need -= t
+        for d in docs[k:]:
+            v = len(self.parent)
+            self.children.append({})
+            self.parent.append(node)
+            self.doc.append(d)
+            self.stamp.append(self.clock)
+            self.alive.append(True)
+            self.children[node][d] = v
+            self.resident += self._t(d)
+            node = v
+        return hit, miss, evicted
+
+
+def prefix_cache_list_model(capacity, requests, tokens=None):
+    """Independent reference for PrefixCache (SPEC cache_sim "brute-force
+    reference simulator with an explicit list-of-prefixes model"): the cache
+    is the set of resident prefixes (tuples) with their last-use stamp;
+    eviction removes the least recently used prefix that no other resident
+    prefix extends and that the request does not contain.  O(N^2)."""
+    tok = tokens or {}
+    t = lambda d: tok.get(d, 1)
+    res = {}  # prefix tuple -> (stamp, creation)
+    clock, created, out = 0, 0, []
+    for req in requests:
+        req = tuple(int(x) for x in req)
+        clock += 1
+        k = 0
+        while k < len(req) and req[:k + 1] in res:
+            k += 1
+        for j in range(1, k + 1):
+            res[req[:j]] = (clock, res[req[:j]][1])
+        hit = sum(t(d) for d in req[:k])
+        miss = sum(t(d) for d in req[k:])
+        resident = sum(t(p[-1]) for p in res)
+        evicted = 0
+        while resident + miss > capacity:
+            cands = [p for p in res if not any(q[:len(p)] == p and len(q) > len(p) for q in res)
+                     and not (len(p) <= len(req) and req[:len(p)] == p)]
+            p = min(cands, key=lambda x: res[x])
+            del res[p]
+            resident -= t(p[-1])
+            evicted += t(p[-1])
+        for j in range(k + 1, len(req) + 1):
+            created += 1
+            res[req[:j]] = (clock, created)
+        out.append((hit, miss, evicted))
+    return out
+
+
+class CacheIndex:
+    """NEXT-4: index update under cache events (§4.1 "Index
+    update": "maintains a min-heap tracking all active nodes by last access
+    time", "removed from the least recently used nodes by decrementing their
+    token counts"; SPEC apply_cache_event).  Per node seq_len and last access;
+    Appended(path, n) adds n tokens and refreshes; Accessed(path) refreshes;
+    Evicted(n) takes tokens from nodes with seq_len > 0 in ascending
+    (last_access, creation order); a node reaching 0 with no children is
+    detached from its parent, and parents left with no children and seq_len 0
+    are deleted recursively (child indices of later siblings shift)."""
+
+    def __init__(self, children):
+        self.children = [list(c) for c in children]
+        self.parent = [-1] * len(children)
+        for p, cs in enumerate(children):
+            for c in cs:
+                self.parent[c] = p
+        self.seq = [0] * len(children)
+        self.last = [0] * len(children)
+        self.gone = [False] * len(children)
+        self.clock = 0
+
+    def node_at(self, path):
+        k = 0
+        for i in path:
+            if i < 0 or i >= len(self.children[k]):
+                raise OracleError("invalid path")
+            k = self.children[k][i]
+        return k
+
+    def appended(self, path, n):
+        if n < 0:
+            raise OracleError("negative token count")
+        k = self.node_at(path)
+        self.clock += 1
+        self.seq[k] += n
+        self.last[k] = self.clock
+
+    def accessed(self, path):
+        k = self.node_at(path)
+        self.clock += 1
+        self.last[k] = self.clock
+
+    def evicted(self, n):
+        if n < 0:
+            raise OracleError("negative token count")
+        taken = 0
+        while n > 0:
+            live = [k for k in range(len(self.seq)) if not self.gone[k] and self.seq[k] > 0]
+            if not live:
+                break
+            k = min(live, key=lambda x: (self.last[x], x))
+            d = min(n, self.seq[k])
+            self.seq[k] -= d
+            n -= d
+            taken += d
+            x = k
+            while x > 0 and self.seq[x] == 0 and not self.children[x]:
+                p = self.parent[x]
+                self.children[p].remove(x)
+                self.gone[x] = True
+                x = p
+        return taken

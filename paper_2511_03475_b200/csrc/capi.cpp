@@ -125,6 +125,9 @@ ScratchLayout ScratchLayout::make(int64_t N, int32_t K, bool keep_rows, bool lin
 
 extern "C" {
 
+// error helper for the other host translation units (hidden: not an rb_ entry)
+rb_status ragb_fail_msg(rb_status code, const char *msg) { return fail(code, msg); }
+
 const char *rb_version(void) { return "ragb 0.1.0 (sm_100a)"; }
 
 const char *rb_last_error(void) { return g_err.c_str(); }
@@ -714,6 +717,23 @@ rb_status rb_session_turn(const rb_session *s, int32_t *turn) {
   if (!s) return fail(RB_ESESSION, "NULL session");
   if (!turn) return fail(RB_EINVAL, "NULL output");
   *turn = s->turn;
+  return RB_OK;
+}
+
+rb_status rb_index_cache_event(rb_index *idx, int32_t kind, const int32_t *path, int32_t path_len,
+                               int64_t n_tokens, int64_t *taken) {
+  if (!idx) return fail(RB_EINVAL, "NULL index");
+  if (!idx->H.has_linkage) return fail(RB_ESTATE, "linkage was skipped");
+  if (path_len < 0) return fail(RB_EINVAL, "negative path length");
+  std::string msg;
+  const rb_status s = ragb::dyn_cache_event(idx->H, kind, path, path_len, n_tokens, taken, &msg);
+  return s == RB_OK ? s : fail(s, msg);
+}
+
+rb_status rb_index_cache_state(const rb_index *idx, int64_t *seq_len, int64_t *last_access) {
+  if (!idx) return fail(RB_EINVAL, "NULL index");
+  if (!idx->H.dyn) return fail(RB_ESTATE, "no cache events applied yet");
+  ragb::dyn_cache_state(idx->H, seq_len, last_access);
   return RB_OK;
 }
 

@@ -137,6 +137,9 @@ int64_t dyn_nodes(const HostIndex &H);
 void dyn_export(const HostIndex &H, int32_t *parent, int32_t *leaf, int32_t *rep, int64_t *prefix_off,
                 uint32_t *prefix_ids, int64_t *path_off, int32_t *path, int64_t *prefix_total,
                 int64_t *path_total);
+rb_status dyn_cache_event(HostIndex &H, int kind, const int32_t *path, int32_t path_len, int64_t n,
+                          int64_t *taken, std::string *msg);
+void dyn_cache_state(const HostIndex &H, int64_t *seq_len, int64_t *last_access);
 const std::vector<uint32_t> &dyn_ordered(const HostIndex &H, int64_t ctx);
 void dyn_order_all(const HostIndex &H, uint32_t *out_ids, uint8_t *out_prefix_len,
                    int64_t *out_schedule);

@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cstring>
 #include <memory>
+#include <set>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -58,6 +59,13 @@ struct DynTree {
   std::vector<std::vector<uint32_t>> docs; // context -> docs in retrieval order
   // per-node inverted index doc -> child positions (large fan-out nodes only)
   std::unordered_map<int32_t, std::unordered_map<uint32_t, std::vector<int32_t>>> inv;
+  // NEXT-4 cache state: cached tokens and last access per node, LRU order of
+  // the nodes holding tokens, nodes detached by evictions
+  std::vector<int64_t> seq;
+  std::vector<uint64_t> last;
+  std::vector<uint8_t> gone;
+  std::set<std::pair<uint64_t, int32_t>> lru;
+  uint64_t clock = 0;
 };
 
 static DynTree *dyn_from_offline(const HostIndex &H) {
@@ -107,6 +115,11 @@ static int32_t dyn_new_node(DynTree &T, int32_t parent, std::vector<uint32_t> se
   T.ord.push_back(std::move(ord));
   T.leaf.push_back(leaf);
   T.cidx.push_back(0);
+  if (!T.seq.empty()) {
+    T.seq.push_back(0);
+    T.last.push_back(0);
+    T.gone.push_back(0);
+  }
   return k;
 }
 
@@ -375,13 +388,89 @@ void dyn_order_all(const HostIndex &H, uint32_t *out_ids, uint8_t *out_prefix_le
     std::unordered_map<int32_t, int64_t> grank;
     std::vector<std::pair<std::pair<int64_t, int64_t>, int64_t>> key(n);
     for (int64_t i = 0; i < n; ++i) {
-      const int32_t g = paths[i][0];
+      const int32_t g = paths[i].empty() ? -1 - (int32_t)i : paths[i][0];  // evicted: own group
       auto it = grank.find(g);
       const int64_t r = it == grank.end() ? (grank[g] = (int64_t)grank.size()) : it->second;
       key[i] = {{r, -(int64_t)paths[i].size()}, i};
     }
     std::sort(key.begin(), key.end());
     for (int64_t i = 0; i < n; ++i) out_schedule[i] = key[i].second;
+  }
+}
+
+// NEXT-4: index update under cache events (Section 4.1 "Index
+// update": "maintains a min-heap tracking all active nodes by last access
+// time" and evicted tokens are "removed from the least recently used nodes by
+// decrementing their token counts"; SPEC apply_cache_event).  kind 0
+// Appended(path, n): n tokens cached at the node, access refreshed; kind 1
+// Accessed(path): access refreshed; kind 2 Evicted(n): tokens taken from the
+// nodes holding tokens in ascending (last access, node id); a node left with
+// no tokens and no children is detached from its parent (later siblings'
+// child indices shift), and so are its ancestors left empty.
+rb_status dyn_cache_event(HostIndex &H, int kind, const int32_t *path, int32_t path_len, int64_t n,
+                          int64_t *taken, std::string *msg) {
+  if (!H.dyn) H.dyn = std::shared_ptr<DynTree>(dyn_from_offline(H));
+  DynTree &T = *H.dyn;
+  if (T.seq.size() != T.parent.size()) {
+    T.seq.resize(T.parent.size(), 0);
+    T.last.resize(T.parent.size(), 0);
+    T.gone.resize(T.parent.size(), 0);
+  }
+  if (n < 0) {
+    *msg = "negative token count";
+    return RB_EINVAL;
+  }
+  if (taken) *taken = 0;
+  if (kind == 0 || kind == 1) {
+    int32_t node = 0;
+    for (int32_t i = 0; i < path_len; ++i) {
+      if (!path || path[i] < 0 || path[i] >= (int32_t)T.kids[node].size()) {
+        *msg = "invalid path";
+        return RB_EPATH;
+      }
+      node = T.kids[node][path[i]];
+    }
+    if (T.seq[node] > 0) T.lru.erase({T.last[node], node});
+    if (kind == 0) T.seq[node] += n;
+    T.last[node] = ++T.clock;
+    if (T.seq[node] > 0) T.lru.insert({T.last[node], node});
+    return RB_OK;
+  }
+  if (kind != 2) {
+    *msg = "unknown cache event";
+    return RB_EINVAL;
+  }
+  int64_t got = 0;
+  while (n > 0 && !T.lru.empty()) {
+    const int32_t k = T.lru.begin()->second;
+    const int64_t d = std::min<int64_t>(n, T.seq[k]);
+    T.seq[k] -= d;
+    n -= d;
+    got += d;
+    if (T.seq[k] > 0) continue;
+    T.lru.erase(T.lru.begin());
+    for (int32_t x = k; x > 0 && T.seq[x] == 0 && T.kids[x].empty();) {
+      const int32_t p = T.parent[x];
+      auto &pk = T.kids[p];
+      const int32_t pos = T.cidx[x];
+      pk.erase(pk.begin() + pos);
+      for (size_t z = (size_t)pos; z < pk.size(); ++z) T.cidx[pk[z]] = (int32_t)z;
+      T.inv.erase(p);  // child positions changed: rebuilt on demand
+      T.gone[x] = 1;
+      T.parent[x] = -1;
+      x = p;
+    }
+  }
+  if (taken) *taken = got;
+  return RB_OK;
+}
+
+void dyn_cache_state(const HostIndex &H, int64_t *seq_len, int64_t *last_access) {
+  const DynTree &T = *H.dyn;
+  for (size_t k = 0; k < T.parent.size(); ++k) {
+    const bool has = k < T.seq.size();
+    if (seq_len) seq_len[k] = has ? (T.gone[k] ? -1 : T.seq[k]) : 0;
+    if (last_access) last_access[k] = has ? (int64_t)T.last[k] : 0;
   }
 }
 

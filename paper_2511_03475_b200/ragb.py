@@ -21,6 +21,7 @@ RB_OK, RB_EINVAL, RB_EDUPDOC, RB_EALPHA, RB_ENOMEM, RB_ECUDA, RB_ENCCL, RB_EPATH
     RB_ESTATE = 0, -1, -2, -3, -4, -5, -6, -7, -8, -9
 RB_EMIT_COUNTS, RB_ALPHA_ANY, RB_KEEP_ROWS, RB_SKIP_LINKAGE = 1, 2, 4, 8
 RB_LINK_COMPLETE, RB_LINK_INTERSECTION = 0, 1
+RB_CACHE_APPENDED, RB_CACHE_ACCESSED, RB_CACHE_EVICTED = 0, 1, 2
 
 STATUS_NAMES = {0: "RB_OK", -1: "RB_EINVAL", -2: "RB_EDUPDOC", -3: "RB_EALPHA", -4: "RB_ENOMEM",
                 -5: "RB_ECUDA", -6: "RB_ENCCL", -7: "RB_EPATH", -8: "RB_ESESSION", -9: "RB_ESTATE"}
@@ -31,6 +32,8 @@ EXPORTED = [
     "rb_index_linkage", "rb_index_tree_info", "rb_index_tree", "rb_order_contexts", "rb_session_open",
     "rb_session_open_docs", "rb_dedup_turn", "rb_session_turn", "rb_session_free", "rb_index_free",
     "rb_index_set_alpha", "rb_session_context", "rb_dedup_batch",
+    "rb_index_cache_event", "rb_index_cache_state", "rb_cache_create", "rb_cache_prefill",
+    "rb_cache_prefill_batch", "rb_cache_resident", "rb_cache_free",
 ]
 
 
@@ -89,6 +92,13 @@ def lib():
         "rb_index_set_alpha": ([P, u32, u32], i32),
         "rb_session_context": ([P, P, i32, ctypes.POINTER(i32)], i32),
         "rb_dedup_batch": ([P, i64, P, P, P, i64, i32, P, P, P, P, P], i32),
+        "rb_index_cache_event": ([P, i32, P, i32, i64, ctypes.POINTER(i64)], i32),
+        "rb_index_cache_state": ([P, P, P], i32),
+        "rb_cache_create": ([i64, PP], i32),
+        "rb_cache_prefill": ([P, P, i32, P, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)], i32),
+        "rb_cache_prefill_batch": ([P, P, P, P, i64, i32, i32, P, P, P], i32),
+        "rb_cache_resident": ([P, ctypes.POINTER(i64)], i32),
+        "rb_cache_free": ([P], None),
         "rb_session_open": ([P, i64, PP], i32),
         "rb_session_open_docs": ([P, i32, PP], i32),
         "rb_dedup_turn": ([P, P, i32, P, ctypes.POINTER(i32), P, P, ctypes.POINTER(i32)], i32),
@@ -200,6 +210,22 @@ class Index:
         t = self.tree()
         o, p = t["path_off"], t["path"]
         return [p[o[i]:o[i + 1]].tolist() for i in range(len(o) - 1)]
+
+    def cache_event(self, kind, path=(), n_tokens=0) -> int:
+        """NEXT-4: Appended / Accessed / Evicted; returns the
+        tokens evicted (Evicted) or 0."""
+        pa = np.ascontiguousarray(list(path), dtype=np.int32)
+        taken = ctypes.c_int64()
+        _check(lib().rb_index_cache_event(self._h, kind, _np_ptr(pa) if len(pa) else None, len(pa), n_tokens,
+                                          ctypes.byref(taken)))
+        return taken.value
+
+    def cache_state(self):
+        n = len(self.tree()["parent"])
+        seq = np.empty(n, dtype=np.int64)
+        last = np.empty(n, dtype=np.int64)
+        _check(lib().rb_index_cache_state(self._h, _np_ptr(seq), _np_ptr(last)))
+        return seq, last
 
     def set_alpha(self, alpha):
         an, ad = alpha_rational(alpha)
@@ -375,3 +401,44 @@ def build_index_host(ids, lens=None, *, alpha=(1, 200), flags=0, stream=None,
                                      ctypes.c_void_p(ws.rows.data_ptr()), ctypes.c_void_p(ws.scratch.data_ptr()),
                                      ws.scratch.numel(), ctypes.byref(out)))
     return Index(out), ws
+
+
+class PrefixCache:
+    """NEXT-4: document-granularity prefix cache."""
+
+    def __init__(self, capacity_tokens: int):
+        h = ctypes.c_void_p()
+        _check(lib().rb_cache_create(int(capacity_tokens), ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.rb_cache_free(h)
+            self._h = None
+
+    def prefill(self, docs, doc_tokens=None):
+        d = np.ascontiguousarray(docs, dtype=np.uint32)
+        t = None if doc_tokens is None else np.ascontiguousarray(doc_tokens, dtype=np.int32)
+        hit, miss, ev = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().rb_cache_prefill(self._h, _np_ptr(d), d.shape[0], _np_ptr(t), ctypes.byref(hit),
+                                      ctypes.byref(miss), ctypes.byref(ev)))
+        return hit.value, miss.value, ev.value
+
+    def prefill_batch(self, ids, lens=None, order=None, tokens_per_doc=1):
+        ids = np.ascontiguousarray(ids, dtype=np.uint32)
+        M, K = ids.shape
+        lens_a = None if lens is None else np.ascontiguousarray(lens, dtype=np.uint8)
+        ord_a = None if order is None else np.ascontiguousarray(order, dtype=np.int64)
+        hit = np.empty(M, dtype=np.int64)
+        miss = np.empty(M, dtype=np.int64)
+        ev = np.empty(M, dtype=np.int64)
+        _check(lib().rb_cache_prefill_batch(self._h, _np_ptr(ids), _np_ptr(lens_a), _np_ptr(ord_a), M, K,
+                                            tokens_per_doc, _np_ptr(hit), _np_ptr(miss), _np_ptr(ev)))
+        return hit, miss, ev
+
+    @property
+    def resident(self) -> int:
+        r = ctypes.c_int64()
+        _check(lib().rb_cache_resident(self._h, ctypes.byref(r)))
+        return r.value
