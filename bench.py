@@ -10,10 +10,12 @@ value = N(N-1)/2 context pairs per build x builds / time (all ranks).
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                   [--config C4] [--no-cpu-baseline]
 
-Multi-GPU (torchrun, one process per GPU): every rank builds the index of its
-own batch (seed + rank) — independent problems, no data-path collective;
-scaling "weak".  Timing: CUDA events on the launching stream, barrier +
-synchronize on both sides, max over ranks.
+Multi-GPU (torchrun, one process per GPU; default --multi sharded): ONE index
+of the same N contexts, rows of the N x N matrix sharded over the GPUs, the
+member rows of every compaction round read from the owning GPU over peer
+memory (§8(e)); scaling "strong".  --multi replicas: every rank builds the
+index of its own batch (seed + rank), scaling "weak".  Timing: CUDA events on
+the launching stream, barrier + synchronize on both sides, max over ranks.
 """
 from __future__ import annotations
 
@@ -44,6 +46,9 @@ def parse():
     ap.add_argument("--config", default="C4")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=8192, help="contexts in the oracle sample")
+    ap.add_argument("--multi", default="sharded", choices=["sharded", "replicas"],
+                    help="N>1: one index with rows sharded over the GPUs (strong scaling), or one "
+                         "independent build per GPU (weak scaling)")
     return ap.parse_args()
 
 
@@ -204,19 +209,32 @@ def run_ours(args, ws, rank, local):
     from paper_2511_03475_b200 import ragb
     from synth.workload import CONFIGS, config
 
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    w = config(args.config) if ws == 1 else config(args.config, seed=CONFIGS[args.config]["seed"] + 1000 * rank)
+    sharded = ws > 1 and args.multi == "sharded"
+    replicas = ws > 1 and not sharded
+    w = config(args.config, seed=CONFIGS[args.config]["seed"] + 1000 * rank) if replicas else config(args.config)
     N, K = w.ids.shape
     pairs = N * (N - 1) / 2
     ids_dev = torch.from_numpy(w.ids.view(np.int32)).to(dev)
     stream = torch.cuda.current_stream(dev)
     p = ragb.make_params(flags=0, stream=ctypes_stream(stream))
-    wsp = ragb.Workspace(N, K, p, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    if sharded:
+        # one index, rows of the N x N matrix sharded over the ws GPUs (§8(e))
+        db = ragb.DistBuilder(ws, N, K, rank=rank, local=False, device=dev)
+
+        def build(ids):
+            return db.build(ids, stream=stream)
+    else:
+        wsp = ragb.Workspace(N, K, p, device=dev)
+
+        def build(ids):
+            return ragb.build_index(ids, workspace=wsp, stream=stream)[0]
 
     def step():
-        idx, _ = ragb.build_index(ids_dev, workspace=wsp, stream=stream)
+        idx = build(ids_dev)
         idx.order_contexts()
         return idx
 
@@ -239,33 +257,36 @@ def run_ours(args, ws, rank, local):
     clocks = clk.stop()
     ms = e0.elapsed_time(e1) / args.steps
     if ws > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = allreduce_max(ms, dev)
         dist.barrier()
 
     # ---- end-to-end through the public API with host buffers -------------
-    ids_pin = torch.from_numpy(w.ids.view(np.int32)).pin_memory().numpy().view(np.uint32)
-    for _ in range(1):
-        idx, _ = ragb.build_index_host(ids_pin, workspace=wsp, stream=stream)
-        idx.order_contexts()
+    ids_pin = torch.from_numpy(w.ids.view(np.int32)).pin_memory()
+
+    def e2e_step():
+        if sharded:  # host ids -> this rank's device, then the sharded build
+            ids_d = ids_pin.to(dev, non_blocking=True)
+            idx = db.build(ids_d, stream=stream)
+        else:
+            idx, _ = ragb.build_index_host(ids_pin.numpy().view(np.uint32), workspace=wsp, stream=stream)
+        out, plen, sched = idx.order_contexts()
+        nn_i, nn_d = idx.nn()
+        za = idx.linkage()
+        return idx
+
+    e2e_step()
     torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
     t0 = time.perf_counter()
     e0.record(stream)
     for _ in range(args.steps):
-        idx, _ = ragb.build_index_host(ids_pin, workspace=wsp, stream=stream)
-        out, plen, sched = idx.order_contexts()
-        nn_i, nn_d = idx.nn()
-        za = idx.linkage()
+        idx = e2e_step()
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = max(e0.elapsed_time(e1), (time.perf_counter() - t0) * 1e3) / args.steps
     if ws > 1:
-        t = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+        e2e_ms = allreduce_max(e2e_ms, dev)
 
     if rank != 0:
         return
@@ -277,7 +298,8 @@ def run_ours(args, ws, rank, local):
     # rooflines: the distance kernel (a2-a4) and the linkage compaction kernel
     # (a5, k_merge_rows: every launch reads the live rows of the old matrix and
     # writes the new one); "roofline" is the one with the larger step share
-    dist_bytes = 4.0 * N * N + 4.0 * N * K   # full fp32 rows written + ids read (algorithmic)
+    rows_here = -(-N // ws) if sharded else N  # rows of the distance matrix this rank writes
+    dist_bytes = 4.0 * rows_here * N + 4.0 * N * K   # fp32 rows written + ids read (algorithmic)
     dist_gbs = dist_bytes / (mean["distance_ms"] * 1e-3) / 1e9
     traffic = load_traffic(args.config)
     roof_dist = {"kernel": "k_dist_tile (a2-a4, distance rows + fused row NN)", "bound": "hbm",
@@ -299,21 +321,23 @@ def run_ours(args, ws, rank, local):
         roofline, roofline_other = roof_dist, roof_merge
     line = {
         "metric": f"context-pair distances/s (index build, N={N}, K={K})",
-        "value": pairs * ws / (ms * 1e-3),
+        "value": pairs * (1 if sharded else ws) / (ms * 1e-3),
         "unit": "context-pairs/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if sharded else "weak", "vs_baseline": None,
         "dtype": "u32+f32", "data": "synthetic",
-        "config": {"workload": workload_desc(args.config, w) + (f"; rank r uses seed+1000r" if ws > 1 else ""),
+        "config": {"workload": workload_desc(args.config, w) + ("; rank r uses seed+1000r" if replicas else ""),
                    "l2": "256 MB flush write between builds; per-build working set 80 GB >> 126 MB L2",
-                   "parallelism": f"{ws} independent index builds (one per GPU)"},
+                   "parallelism": (f"one index, rows sharded over {ws} GPUs (peer-memory exchange)" if sharded
+                                   else f"{ws} independent index builds (one per GPU)")},
         "build_time_ms": ms,
         "stages_ms": {k: mean[k] for k in ("validate_ms", "distance_ms", "linkage_ms", "host_ms", "total_ms")},
         "distance_pairs_per_s": pairs / (mean["distance_ms"] * 1e-3),
         "linkage_rounds": mean["linkage_rounds"],
         "roofline": roofline,
         "roofline_other": roofline_other,
-        "e2e": {"value": pairs * ws / (e2e_ms * 1e-3), "unit": "context-pairs/s", "ms_per_step": e2e_ms,
+        "e2e": {"value": pairs * (1 if sharded else ws) / (e2e_ms * 1e-3), "unit": "context-pairs/s",
+                "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": int(N * K * 4),
                 "d2h_bytes_per_step": int(N * 8 + 16 * (N - 1) + 8)},
         "gpu_launches": int(sum(s["kernel_launches"] for s in stats)),
@@ -323,6 +347,16 @@ def run_ours(args, ws, rank, local):
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(w, min(args.cpu_sample, N))
     print(json.dumps(line), flush=True)
+
+
+def allreduce_max(x, dev):
+    """Max over ranks (device tensor with NCCL, host tensor with gloo)."""
+    import torch
+    import torch.distributed as dist
+    on_dev = dist.get_backend() == "nccl"
+    t = torch.tensor([x], dtype=torch.float64, device=dev if on_dev else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 def ctypes_stream(stream):
@@ -360,8 +394,11 @@ def main():
                 return
         else:
             import torch
-            torch.cuda.set_device(local)
-            dist.init_process_group("nccl")
+            # one process per GPU; more ranks than GPUs (a one-GPU check of the
+            # multi-process path) share devices and fall back to gloo plumbing
+            ngpu = max(torch.cuda.device_count(), 1)
+            torch.cuda.set_device(local % ngpu)
+            dist.init_process_group("nccl" if ws <= ngpu else "gloo")
     if args.impl == "reference":
         run_reference(args, ws, rank)
         return

@@ -307,6 +307,36 @@ RB_API rb_status rb_cache_prefill_batch(rb_cache *c, const uint32_t *ids, const 
 RB_API rb_status rb_cache_resident(const rb_cache *c, int64_t *tokens);
 RB_API void rb_cache_free(rb_cache *c);
 
+/* ---- §8(e): one index built by `world` GPUs, rows sharded ----------------
+ * Rank q computes rows [q*S, min((q+1)*S, N)) of the Eq. 1 matrix (S =
+ * ceil(N/world)) and, every linkage round, the new rows it owns of the
+ * compacted matrix, reading member rows from the rank that holds them over
+ * peer memory (CUDA IPC, NVLink/NVSwitch); the O(N) round state (keys, level
+ * cliques, compaction map) is replicated and the merges are identical on all
+ * ranks (north_star "rows of the N x N matrix shard naturally across the 8
+ * GPUs of one box").  One process per GPU: local_ranks = 1; every rank
+ * attaches its buffers, exports a handle blob, imports every other rank's
+ * blob (exchanged by the caller, e.g. torch.distributed), then all ranks call
+ * rb_build_index_dist together.  local_ranks = world (rank 0): all ranks in
+ * this process on the current device (validation of the sharded algorithm
+ * on one GPU).  Buffers per rank: rows [S][N] floats and scratch, sizes from
+ * rb_dist_workspace_size.  Complete linkage only.  A rank that never arrives
+ * at a barrier makes the others fail with RB_ECUDA after ~20 s (no hang). */
+typedef struct rb_dist rb_dist;
+#define RB_DIST_HANDLE_BYTES 256
+RB_API rb_status rb_dist_create(int32_t world, int32_t rank, int32_t local_ranks, rb_dist **out);
+RB_API rb_status rb_dist_workspace_size(int32_t world, int64_t N, int32_t K, size_t *rows_bytes,
+                                        size_t *scratch_bytes);
+RB_API rb_status rb_dist_attach(rb_dist *d, int32_t rank, float *rows_dev, void *scratch_dev,
+                                size_t scratch_bytes);
+RB_API rb_status rb_dist_export(const rb_dist *d, void *blob, size_t blob_bytes);
+RB_API rb_status rb_dist_import(rb_dist *d, const void *blob, size_t blob_bytes);
+/* ids_dev [N][K] / lens_dev [N] on this rank's device (the same contexts on
+ * every rank).  Errors as rb_build_index, RB_ESTATE (buffers missing). */
+RB_API rb_status rb_build_index_dist(rb_dist *d, const uint32_t *ids_dev, const uint8_t *lens_dev, int64_t N,
+                                     int32_t K, const rb_params *p, rb_index **out);
+RB_API void rb_dist_free(rb_dist *d);
+
 RB_API void rb_session_free(rb_session *s);
 RB_API void rb_index_free(rb_index *idx);
 

@@ -19,10 +19,6 @@
 using ragb::HostIndex;
 using ragb::ScratchLayout;
 
-struct rb_index {
-  HostIndex H;
-};
-
 struct rb_session {
   std::unordered_map<uint32_t, int32_t> seen;  // doc -> turn first prefilled
   std::vector<uint32_t> ctx;                   // turn-0 context ++ novel docs

@@ -166,3 +166,8 @@ void host_replay(HostIndex &H, TreeBuild &T, int64_t upto);
 rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg);
 
 }  // namespace ragb
+
+// the C-ABI handle (capi.cpp, dist.cu)
+struct rb_index {
+  ragb::HostIndex H;
+};

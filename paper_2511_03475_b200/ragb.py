@@ -34,6 +34,8 @@ EXPORTED = [
     "rb_index_set_alpha", "rb_session_context", "rb_dedup_batch",
     "rb_index_cache_event", "rb_index_cache_state", "rb_cache_create", "rb_cache_prefill",
     "rb_cache_prefill_batch", "rb_cache_resident", "rb_cache_free",
+    "rb_dist_create", "rb_dist_workspace_size", "rb_dist_attach", "rb_dist_export", "rb_dist_import",
+    "rb_build_index_dist", "rb_dist_free",
 ]
 
 
@@ -99,6 +101,13 @@ def lib():
         "rb_cache_prefill_batch": ([P, P, P, P, i64, i32, i32, P, P, P], i32),
         "rb_cache_resident": ([P, ctypes.POINTER(i64)], i32),
         "rb_cache_free": ([P], None),
+        "rb_dist_create": ([i32, i32, i32, PP], i32),
+        "rb_dist_workspace_size": ([i32, i64, i32, ctypes.POINTER(sz), ctypes.POINTER(sz)], i32),
+        "rb_dist_attach": ([P, i32, P, P, sz], i32),
+        "rb_dist_export": ([P, P, sz], i32),
+        "rb_dist_import": ([P, P, sz], i32),
+        "rb_build_index_dist": ([P, P, P, i64, i32, ctypes.POINTER(Params), PP], i32),
+        "rb_dist_free": ([P], None),
         "rb_session_open": ([P, i64, PP], i32),
         "rb_session_open_docs": ([P, i32, PP], i32),
         "rb_dedup_turn": ([P, P, i32, P, ctypes.POINTER(i32), P, P, ctypes.POINTER(i32)], i32),
@@ -442,3 +451,66 @@ class PrefixCache:
         r = ctypes.c_int64()
         _check(lib().rb_cache_resident(self._h, ctypes.byref(r)))
         return r.value
+
+
+RB_DIST_HANDLE_BYTES = 256
+
+
+class DistBuilder:
+    """§8(e): one index built by `world` GPUs with the distance rows sharded.
+
+    local=True: all ranks in this process on the current device (validation
+    of the sharded algorithm on one GPU).  local=False: one process per GPU
+    (torchrun); the handle blobs are exchanged with torch.distributed.
+    """
+
+    def __init__(self, world: int, N: int, K: int, rank: int = 0, local: bool = False, device="cuda"):
+        import torch
+        self.world, self.N, self.K, self.rank, self.local = world, N, K, rank, local
+        h = ctypes.c_void_p()
+        _check(lib().rb_dist_create(world, rank, world if local else 1, ctypes.byref(h)))
+        self._h = h
+        rb, sb = ctypes.c_size_t(), ctypes.c_size_t()
+        _check(lib().rb_dist_workspace_size(world, N, K, ctypes.byref(rb), ctypes.byref(sb)))
+        ranks = range(world) if local else [rank]
+        self.rows, self.scratch = {}, {}
+        for q in ranks:
+            self.rows[q] = torch.empty(max(rb.value // 4, 1), dtype=torch.float32, device=device)
+            self.scratch[q] = torch.empty(sb.value, dtype=torch.uint8, device=device)
+            _check(lib().rb_dist_attach(self._h, q, ctypes.c_void_p(self.rows[q].data_ptr()),
+                                        ctypes.c_void_p(self.scratch[q].data_ptr()), sb.value))
+        if not local and world > 1:
+            import torch.distributed as dist
+            blob = ctypes.create_string_buffer(RB_DIST_HANDLE_BYTES)
+            _check(lib().rb_dist_export(self._h, blob, RB_DIST_HANDLE_BYTES))
+            blobs = [None] * world
+            dist.all_gather_object(blobs, bytes(blob.raw))
+            for b in blobs:
+                buf = ctypes.create_string_buffer(b, RB_DIST_HANDLE_BYTES)
+                _check(lib().rb_dist_import(self._h, buf, RB_DIST_HANDLE_BYTES))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.rb_dist_free(h)
+            self._h = None
+
+    def build(self, ids, lens=None, *, alpha=(1, 200), flags=0, stream=None) -> Index:
+        import torch
+        ids = ids.contiguous()
+        N, K = ids.shape
+        assert (N, K) == (self.N, self.K)
+        p = make_params(alpha, flags, _stream_ptr(stream))
+        out = ctypes.c_void_p()
+        _check(lib().rb_build_index_dist(self._h, ctypes.c_void_p(ids.data_ptr()),
+                                         None if lens is None else ctypes.c_void_p(lens.contiguous().data_ptr()),
+                                         N, K, ctypes.byref(p), ctypes.byref(out)))
+        return Index(out)
+
+
+def torch_cuda_available() -> bool:
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False

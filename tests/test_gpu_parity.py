@@ -344,3 +344,50 @@ def test_intersection_variable_lengths_and_consumed_rows():
     w = generate(900, 12, 2500, 8, len_min=2)
     check_intersection(w.ids, w.lens)
     check_intersection(w.ids, w.lens, flags=0)
+
+
+def _dist_vs_single(ids, lens, world):
+    t = torch.from_numpy(np.ascontiguousarray(ids).view(np.int32)).cuda()
+    tl = None if lens is None else torch.from_numpy(np.ascontiguousarray(lens, dtype=np.uint8)).cuda()
+    db = F.DistBuilder(world, ids.shape[0], ids.shape[1], local=True)
+    di = db.build(t, tl)
+    res_d = (di.linkage(), di.nn(), di.order_contexts(), di.paths())
+    del db, di
+    torch.cuda.empty_cache()
+    si, ws = F.build_index(t, tl)
+    res_s = (si.linkage(), si.nn(), si.order_contexts(), si.paths())
+    del si, ws
+    torch.cuda.empty_cache()
+    for x, y in zip(res_d[0] + res_d[1] + res_d[2], res_s[0] + res_s[1] + res_s[2]):
+        assert np.array_equal(np.asarray(x).view(np.uint8), np.asarray(y).view(np.uint8))
+    assert res_d[3] == res_s[3]
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+def test_row_sharded_build_matches_single_gpu(world):
+    """§8(e): the row-sharded build (ranks simulated in one process on one GPU,
+    member rows read through the peer tables) gives the single-GPU (and so the
+    oracle's) merge order, NN, document order, schedule and paths."""
+    _dist_vs_single(config("C2").ids, None, world)
+    w = generate(2053, 12, 5000, 77, len_min=3)
+    _dist_vs_single(w.ids, w.lens, world)
+    w = generate(1500, 4, 200, 78)  # tie-heavy: large level cliques
+    _dist_vs_single(w.ids, None, world)
+
+
+def test_row_sharded_tiny_and_vs_oracle():
+    w = generate(5, 4, 12, 3)
+    _dist_vs_single(w.ids, None, 8)  # fewer rows than ranks
+    w = config("C1")
+    t = torch.from_numpy(w.ids.view(np.int32)).cuda()
+    di = F.DistBuilder(3, w.N, w.K, local=True).build(t)
+    Z = oc.linkage(oc.pairwise_rows(w.ids, None, 1, 200))
+    a, b, h, s = di.linkage()
+    assert np.array_equal(a, Z[0]) and np.array_equal(b, Z[1]) and np.array_equal(s, Z[3])
+    assert np.array_equal(h.view(np.uint32), Z[2].view(np.uint32))
+
+
+def test_row_sharded_full_size_C4():
+    """C4 with 8 ranks' shards on one device (~130 GB): identical to the
+    single-GPU build."""
+    _dist_vs_single(config("C4").ids, None, 8)
