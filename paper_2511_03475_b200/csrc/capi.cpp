@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <condition_variable>
 #include <mutex>
 #include <thread>
@@ -86,6 +87,8 @@ ScratchLayout ScratchLayout::make(int64_t N, int32_t K, bool keep_rows, bool lin
     int64_t entries;
     distance_lut_layout(K, true, &stride, &entries);
     L.lut = take(o, (size_t)std::max<int64_t>(entries, 1) * 4);
+    L.lutc = take(o, (size_t)std::max<int64_t>(entries, 1) * 4);
+    L.vals = take(o, (size_t)std::max<int64_t>(entries, 1) * 4);
   }
   if (linkage && N > 1) {
     L.key0 = L.nnkey;
@@ -98,9 +101,10 @@ ScratchLayout ScratchLayout::make(int64_t N, int32_t K, bool keep_rows, bool lin
     L.aux0 = take(o, (size_t)N * 4);
     L.aux1 = take(o, (size_t)(N + 1) * 4);
     L.aux2 = take(o, (size_t)N * 4);
-    L.aux3 = take(o, (size_t)(N + 4) * 4);
+    L.aux3 = take(o, (size_t)(N + 8) * 4);
     L.aux4 = take(o, (size_t)2 * N * 4);
     L.alive = take(o, (size_t)N);
+    L.pmap = take(o, (size_t)(N + 8) * 8);
     L.za = take(o, (size_t)N * 4);
     L.zb = take(o, (size_t)N * 4);
     L.zh = take(o, (size_t)N * 4);
@@ -110,7 +114,11 @@ ScratchLayout ScratchLayout::make(int64_t N, int32_t K, bool keep_rows, bool lin
     // compacted matrices: at most (N-1) rows with a leading dimension padded to 4
     // (also holds an N x N copy for the intersection linkage with RB_KEEP_ROWS)
     const size_t mat = std::max((size_t)(N - 1) * (size_t)((N + 2) & ~3ll), (size_t)N * N) * 4;
-    L.matA = take(o, mat);
+    // code mode: two code matrices of max(N x N, (N-1) x round_up(N, 8)) in the same region
+    const size_t cmat = (std::max((size_t)N * N, (size_t)(N - 1) * (size_t)((N + 7) & ~7ll)) * 2 + 255) & ~(size_t)255;
+    L.matA = take(o, std::max(mat, 2 * cmat));
+    L.codes = L.matA;
+    L.mat16 = L.matA + cmat;
     L.matB = keep_rows ? take(o, mat) : 0;
   }
   L.total = (o + kAlign - 1) / kAlign * kAlign;
@@ -257,6 +265,12 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
   da.D_out = (p->flags & RB_EMIT_COUNTS) ? D_dev : nullptr;
   da.nnkey = reinterpret_cast<unsigned long long *>(sc + L.nnkey);
   da.lut = nullptr;
+  // complete linkage on 16-bit value codes whenever the tile
+  // path's Eq. 1 table exists; RAGB_CODES=0 keeps the fp32 matrices (testing)
+  const char *cenv = std::getenv("RAGB_CODES");
+  const bool code_mode = linkage && p->linkage == RB_LINK_COMPLETE && N > 1 &&
+                         ragb::tile_path_ok(K, lens_d == nullptr) && !(cenv && std::atoi(cenv) == 0);
+  ragb::CodeMode cm{};
   {
     int stride;
     int64_t entries;
@@ -267,6 +281,19 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
                                    &launches),
               "eq1 table");
       da.lut = lut;
+      if (code_mode) {
+        uint32_t *lutc = reinterpret_cast<uint32_t *>(sc + L.lutc);
+        float *vals = reinterpret_cast<float *>(sc + L.vals);
+        int *ncode = reinterpret_cast<int *>(sc + L.err + 16);
+        RB_CUDA(ragb::launch_code_table(lut, K, stride, entries, lutc, vals, ncode, st, &launches), "code table");
+        da.lutc = lutc;
+        da.vals = vals;
+        da.codes = reinterpret_cast<uint16_t *>(sc + L.codes);
+        cm.codes = da.codes;
+        cm.mat16 = reinterpret_cast<uint16_t *>(sc + L.mat16);
+        cm.vals = vals;
+        cm.ncode = ncode;
+      }
     }
   }
   RB_CUDA(ragb::launch_distance(da, st, &launches), "distance kernel");
@@ -323,7 +350,7 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
       }
     });
     const cudaError_t le = ragb::run_linkage(
-        rows_dev, N, da.nnkey, scratch_dev, L, keep_rows, st, H.za.data(), H.zb.data(),
+        rows_dev, N, da.nnkey, scratch_dev, L, keep_rows, code_mode ? &cm : nullptr, st, H.za.data(), H.zb.data(),
         H.zh.data(), H.zs.data(), &lo, &launches, [&](int64_t upto) {
           {
             std::lock_guard<std::mutex> lk(mu);

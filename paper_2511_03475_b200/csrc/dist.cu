@@ -74,7 +74,7 @@ struct DistLayout {
     L.aux0 = take(o, (size_t)N * 4);
     L.aux1 = take(o, (size_t)(N + 1) * 4);
     L.aux2 = take(o, (size_t)N * 4);
-    L.aux3 = take(o, (size_t)(N + 4) * 4);
+    L.aux3 = take(o, (size_t)(N + 8) * 4);
     L.aux4 = take(o, (size_t)2 * N * 4);
     L.alive = take(o, (size_t)N);
     L.za = take(o, (size_t)N * 4);
@@ -617,12 +617,13 @@ rb_status build_index_dist(rb_dist *d, const uint32_t *ids_d, const uint8_t *len
       const int64_t ldn = ((int64_t)Mn + 3) & ~3ll;
       const bool vec = (ld & 3) == 0;
       const bool wide = Mn > 20 * 1024;
-      const int maxW = wide ? 56 * 1024 : 20 * 1024;
+      const int maxW = wide ? 56 * 1024 : 20 * 1024;  // window of 32-bit slots (fp32 matrices)
       const int W = std::min<int>((Mn + 3) & ~3, maxW);
       const size_t smem = (size_t)W * 4;
       const int nth = wide ? 1024 : 256;
-      auto kern = wide ? (vec ? k_merge_rows<true, 1024, PeerRows> : k_merge_rows<false, 1024, PeerRows>)
-                       : (vec ? k_merge_rows<true, 256, PeerRows> : k_merge_rows<false, 256, PeerRows>);
+      typedef PeerRows<float> PR;
+      auto kern = wide ? (vec ? k_merge_rows<true, 1024, float, PR> : k_merge_rows<false, 1024, float, PR>)
+                       : (vec ? k_merge_rows<true, 256, float, PR> : k_merge_rows<false, 256, float, PR>);
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       int per_sm = 1;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nth, smem);
@@ -634,7 +635,7 @@ rb_status build_index_dist(rb_dist *d, const uint32_t *ids_d, const uint8_t *len
         float *Dn = reinterpret_cast<float *>(sc + ((cur_is_rows || !cur_is_A) ? L.matA : L.matB));
         if (c1 > c0) {
           const int grid = std::min<int>(c1 - c0, sms * std::max(per_sm, 1));
-          kern<<<grid, nth, smem, st>>>(PeerRows{reinterpret_cast<const float *const *>(table(r, tcur)), (int)S, ld}, M,
+          kern<<<grid, nth, smem, st>>>(PR{reinterpret_cast<const float *const *>(table(r, tcur)), (int)S, ld}, M,
                                         pa[l].Mn, pa[l].goff, pa[l].gmem, pa[l].colsrc, pa[l].cursor, W, c0, c1, Dn,
                                         at<unsigned long long>(sc, knoff));
           ++launches;

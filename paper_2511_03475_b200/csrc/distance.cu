@@ -282,6 +282,43 @@ __global__ void k_eq1_lut(float *lut, int K, int stride, uint32_t an, uint32_t a
   lut[i] = eq1_from_counts(s, D, (uint32_t)K, an, ad);
 }
 
+// Order-preserving codes of the table (linkage on 16-bit codes, DESIGN.md
+// §6.2).  Reachable entries: s = 0 with D = 0, and 1 <= s <= K with D <=
+// floor(K^2/2).  code(e) = number of reachable entries with a smaller value,
+// so equal values share a code and order is preserved (a dense rank is not
+// needed, only an order-preserving injective map of the values); vals is the
+// sorted multiset of reachable values, vals[code(e)] = lut[e], so the code of
+// a value is the first index holding it.  O(E^2) with E <= 33,792, once per
+// build.
+__global__ void k_code_table(const float *__restrict__ lut, int K, int stride, int E, uint32_t *__restrict__ lutc,
+                             float *__restrict__ vals, int *__restrict__ ncode) {
+  __shared__ float sv[1024];
+  const int dmax = K * K / 2;
+  auto reach = [&](int e) {
+    const int s = e / stride, D = e - s * stride;
+    return e < E && D <= dmax && (s > 0 || D == 0);
+  };
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool ri = reach(i);
+  const float vi = ri ? lut[i] : 0.0f;
+  int cl = 0, ce = 0;
+  for (int j0 = 0; j0 < E; j0 += 1024) {
+    __syncthreads();
+    for (int j = threadIdx.x; j < 1024; j += blockDim.x)
+      sv[j] = reach(j0 + j) ? lut[j0 + j] : __int_as_float(0x7f800000);  // +inf: never below, never equal
+    __syncthreads();
+    const int n = min(1024, E - j0);
+    for (int j = 0; j < n; ++j) {
+      const float v = sv[j];
+      cl += v < vi ? 1 : 0;
+      ce += (v == vi && j0 + j < i) ? 1 : 0;
+    }
+  }
+  if (i < E) lutc[i] = ri ? (uint32_t)cl : 0u;
+  if (ri) vals[cl + ce] = vi;
+  if (i == 0) *ncode = 1 + K * min(stride, dmax + 1);
+}
+
 // a1: validate every context and write the transposed, padded id array.
 __global__ void k_validate(const uint32_t *__restrict__ ids, const uint8_t *__restrict__ lens,
                            int64_t N, int32_t K, int64_t Npad, uint32_t *__restrict__ idsT,
@@ -409,6 +446,14 @@ cudaError_t launch_eq1_lut(float *lut, int32_t K, int stride, int64_t entries, u
                            uint32_t ad, cudaStream_t st, int *launches) {
   if (entries == 0) return cudaSuccess;
   k_eq1_lut<<<(unsigned)((entries + 255) / 256), 256, 0, st>>>(lut, K, stride, an, ad);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_code_table(const float *lut, int32_t K, int stride, int64_t entries, uint32_t *lutc,
+                              float *vals, int *ncode, cudaStream_t st, int *launches) {
+  if (entries == 0) return cudaSuccess;
+  k_code_table<<<(unsigned)((entries + 255) / 256), 256, 0, st>>>(lut, K, stride, (int)entries, lutc, vals, ncode);
   ++*launches;
   return cudaGetLastError();
 }

@@ -41,7 +41,10 @@ struct Plan {
       off_red, off_wsum, off_lut, total;
 };
 
-template <int SHIFT, bool LUT_SMEM, bool COUNTS>
+// CODES: also write codes[i][j] = lutc[packed (s, D)] (16-bit order-preserving
+// value codes, the complete-linkage input; the code table has the float
+// table's layout and is read through L1).
+template <int SHIFT, bool LUT_SMEM, bool COUNTS, bool CODES>
 __global__ void __launch_bounds__(NT, 2) k_dist_tile(DistArgs a, Plan P) {
   constexpr uint32_t DMASK = (1u << SHIFT) - 1u;
   constexpr uint32_t INC = 1u << SHIFT;
@@ -209,6 +212,8 @@ __global__ void __launch_bounds__(NT, 2) k_dist_tile(DistArgs a, Plan P) {
         const char *lutb = reinterpret_cast<const char *>(lut);
         float2 *o = reinterpret_cast<float2 *>(orow);
         const int64_t step = N / 2;  // float2 units per row (N even here)
+        const char *lutcb = reinterpret_cast<const char *>(a.lutc);
+        uint32_t *co = CODES ? reinterpret_cast<uint32_t *>(a.codes + (r0 - a.row0) * N + jb) : nullptr;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const uint32_t w = ap[r * NT];
@@ -223,6 +228,18 @@ __global__ void __launch_bounds__(NT, 2) k_dist_tile(DistArgs a, Plan P) {
           }
           __stcs(o, make_float2(d0, d1));
           o += step;
+          if (CODES) {
+            uint32_t c0, c1;
+            if (SHIFT == 8) {
+              c0 = __ldg(reinterpret_cast<const uint32_t *>(lutcb + (w & 0xffffu)));
+              c1 = __ldg(reinterpret_cast<const uint32_t *>(lutcb + (w >> 16)));
+            } else {
+              c0 = __ldg(a.lutc + (w & 0xffffu));
+              c1 = __ldg(a.lutc + (w >> 16));
+            }
+            __stcs(co, c0 | (c1 << 16));
+            co += step;
+          }
           // strict '<' keeps the smallest column among equal distances (X8)
           const float m = fminf(d0, d1);
           const bool u = m < bv[r];
@@ -245,6 +262,11 @@ __global__ void __launch_bounds__(NT, 2) k_dist_tile(DistArgs a, Plan P) {
             } else {
               if (jb < N) __stcs(o, d0);
               if (jb + 1 < N) __stcs(o + 1, d1);
+            }
+            if (CODES) {
+              uint16_t *cr = a.codes + (gi - a.row0) * N + jb;
+              if (jb < N) __stcs(cr, (uint16_t)__ldg(a.lutc + p0));
+              if (jb + 1 < N) __stcs(cr + 1, (uint16_t)__ldg(a.lutc + p1));
             }
             if (COUNTS) {
               if (jb < N) {
@@ -325,9 +347,9 @@ Plan plan(int K, int shift, int lutSmemEntries) {
   return P;
 }
 
-template <int SHIFT, bool LS, bool C>
+template <int SHIFT, bool LS, bool C, bool CD>
 cudaError_t launch(const DistArgs &a, const Plan &P, cudaStream_t st) {
-  auto kern = k_dist_tile<SHIFT, LS, C>;
+  auto kern = k_dist_tile<SHIFT, LS, C, CD>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)P.total);
   if (e != cudaSuccess) return e;
@@ -359,9 +381,13 @@ cudaError_t launch_distance_tile(const DistArgs &a, cudaStream_t st) {
   const int64_t entries = tile_lut_entries(a.K);
   const bool lut_smem = shift == 8;  // (K+1) * 256 floats <= 23.5 KB
   const Plan P = plan(a.K, shift, lut_smem ? (int)entries : 0);
-  const bool C = a.s_out != nullptr;
-  if (shift == 8) return C ? launch<8, true, true>(a, P, st) : launch<8, true, false>(a, P, st);
-  return C ? launch<10, false, true>(a, P, st) : launch<10, false, false>(a, P, st);
+  const bool C = a.s_out != nullptr, CD = a.codes != nullptr && a.lutc != nullptr;
+  if (shift == 8) {
+    if (CD) return C ? launch<8, true, true, true>(a, P, st) : launch<8, true, false, true>(a, P, st);
+    return C ? launch<8, true, true, false>(a, P, st) : launch<8, true, false, false>(a, P, st);
+  }
+  if (CD) return C ? launch<10, false, true, true>(a, P, st) : launch<10, false, false, true>(a, P, st);
+  return C ? launch<10, false, true, false>(a, P, st) : launch<10, false, false, false>(a, P, st);
 }
 
 }  // namespace ragb

@@ -30,8 +30,10 @@ inline int64_t padded_cols(int64_t N) { return round_up(N, kChunk); }
 // ----------------------------------------------------------------- scratch
 // Byte layout of the caller-owned scratch buffer (all offsets 256-aligned).
 struct ScratchLayout {
-  size_t err, idsT, nnkey, stage_ids, stage_lens, lut, key0, key1, rep0, rep1, sz0, sz1, leader, aux0, aux1, aux2, aux3, aux4,
+  size_t err, idsT, nnkey, stage_ids, stage_lens, lut, lutc, vals, key0, key1, rep0, rep1, sz0, sz1, leader, aux0, aux1, aux2, aux3, aux4,
       alive, za, zb, zh, zs, amask, mlist, counters, matA, matB, total;
+  size_t pmap;         // code mode: int2 [N + 8] new column -> (leader, pair member)
+  size_t codes, mat16;  // code mode (inside matA): [N][N] codes, then the first compacted code matrix
   static ScratchLayout make(int64_t N, int32_t K, bool keep_rows, bool linkage);
 };
 
@@ -48,6 +50,26 @@ struct DistArgs {
   uint16_t *D_out;            // [nrows][N] or nullptr
   unsigned long long *nnkey;  // [N] indexed by global row: (f32 bits << 32) | column
   const float *lut;           // Eq. 1 table d(s, D) for uniform length K, or nullptr
+  // code output (tile path only, complete linkage): codes[i][j] = rank of
+  // d_ij among the distinct values of the table (lutc[e] = code of lut[e])
+  const uint32_t *lutc;       // [lut entries] or nullptr
+  const float *vals;          // [ncode] ascending distinct table values
+  uint16_t *codes;            // [nrows][N] or nullptr
+};
+
+// Order-preserving codes of the Eq. 1 table (distance.cu): lutc[e] = number
+// of distinct reachable table values below lut[e]; vals[c] = the value of code
+// c (strictly ascending); *ncode = their count (device).
+cudaError_t launch_code_table(const float *lut, int32_t K, int stride, int64_t entries, uint32_t *lutc,
+                              float *vals, int *ncode, cudaStream_t st, int *launches);
+
+// Linkage on 16-bit codes (linkage.cu): codes [N][N] (ld N) from the distance
+// kernel, a second buffer for compacted matrices, the code -> value table.
+struct CodeMode {
+  uint16_t *codes;
+  uint16_t *mat16;
+  const float *vals;
+  const int *ncode;  // device
 };
 
 // Eq. 1 table d(s, D) at index s * stride + D.  Tile path (uniform K <= 32):
@@ -91,8 +113,8 @@ cudaError_t run_linkage_intersection(float *rows, int64_t ld, int64_t N, int32_t
                                      int *launches);
 
 cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void *scratch,
-                        const ScratchLayout &L, bool keep_rows, cudaStream_t st, int32_t *za,
-                        int32_t *zb, float *zh, int32_t *zs, LinkageOut *out, int *launches,
+                        const ScratchLayout &L, bool keep_rows, const CodeMode *cm, cudaStream_t st,
+                        int32_t *za, int32_t *zb, float *zh, int32_t *zs, LinkageOut *out, int *launches,
                         const std::function<void(int64_t)> &on_round);
 
 // ----------------------------------------------------------------- host

@@ -43,23 +43,89 @@ T *at(void *base, size_t off) {
   return reinterpret_cast<T *>(static_cast<unsigned char *>(base) + off);
 }
 
+// Compaction launch for element type T (see k_merge_rows): wide rows get
+// 1024-thread CTAs, one per SM, with a window of up to 56K columns; narrow
+// rows 256-thread CTAs so that several rows are in flight per SM.
+template <typename T>
+cudaError_t launch_merge(const T *cur, int64_t ld, int M, int Mn, const PrepArgs &pa, int sms, T *next,
+                         unsigned long long *keyn, cudaStream_t st) {
+  constexpr int VW = Elem<T>::VW;
+  const char *genv = std::getenv("RAGB_GATHER");
+  if (sizeof(T) == 2 && pa.pmap && (size_t)((M + 7) / 8) * 16 <= 227 * 1024 && !(genv && std::atoi(genv) == 0)) {
+    // code mode, old row fits in shared memory: gather form (k_merge_gather)
+    const uint16_t *c16 = reinterpret_cast<const uint16_t *>(cur);
+    uint16_t *n16 = reinterpret_cast<uint16_t *>(next);
+    const bool vec = ld % 8 == 0 && (reinterpret_cast<uintptr_t>(cur) & 15) == 0;
+    const size_t smem = (size_t)((M + 7) / 8) * 16;
+    const bool wide = M > 16 * 1024;
+    auto kern = wide ? (vec ? k_merge_gather<true, 1024> : k_merge_gather<false, 1024>)
+                     : (vec ? k_merge_gather<true, 256> : k_merge_gather<false, 256>);
+    const int nth = wide ? 1024 : 256;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nth, smem);
+    const int grid = std::min<int>(Mn, sms * std::max(per_sm, 1));
+    kern<<<grid, nth, smem, st>>>(c16, ld, M, pa.Mn, pa.goff, pa.gmem, pa.pmap, n16, keyn);
+    return cudaGetLastError();
+  }
+  const bool vec = ld % VW == 0 && (reinterpret_cast<uintptr_t>(cur) & 15) == 0;
+  const bool wide = Mn > 20 * 1024;
+  const int es = (int)sizeof(typename Win<T>::S);  // window element bytes
+  const int maxW = wide ? 224 * 1024 / es : 20 * 1024;
+  const int W = std::min<int>((Mn + VW - 1) / VW * VW, maxW);
+  const size_t smem = (size_t)W * es;
+  const int nth = wide ? 1024 : 256;
+  auto kern = wide ? (vec ? k_merge_rows<true, 1024, T, LocalRows<T>> : k_merge_rows<false, 1024, T, LocalRows<T>>)
+                   : (vec ? k_merge_rows<true, 256, T, LocalRows<T>> : k_merge_rows<false, 256, T, LocalRows<T>>);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nth, smem);
+  const int grid = std::min<int>(Mn, sms * std::max(per_sm, 1));
+  kern<<<grid, nth, smem, st>>>(LocalRows<T>{cur, ld}, M, pa.Mn, pa.goff, pa.gmem, pa.colsrc, pa.cursor, W, 0, -1,
+                                next, keyn);
+  return cudaGetLastError();
+}
+
+// In-place round for element type T (see k_inplace_*).
+template <typename T>
+cudaError_t launch_inplace(T *cur, int64_t ld, int M, const PrepArgs &pa, int sms, uint32_t *amask, int *mlist,
+                           int *nmulti, int *sz, unsigned long long *key, cudaStream_t st) {
+  constexpr int VW = Elem<T>::VW;
+  k_inplace_prep<<<sms * 2, 256, 0, st>>>(pa, M, amask, mlist, nmulti, sz, key);
+  const size_t smem = (size_t)((M + VW - 1) / VW) * 16;
+  cudaFuncSetAttribute(k_inplace_rows<512, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_inplace_rows<512, T><<<sms * 2, 512, smem, st>>>(pa, cur, ld, M, amask, mlist, nmulti, key);
+  k_inplace_cols<T><<<sms * 8, 256, 0, st>>>(pa, cur, ld, M, amask, mlist, nmulti);
+  k_inplace_check<T><<<(M + 255) / 256, 256, 0, st>>>(pa, cur, ld, M, key, pa.cnt, nmulti + 1);  // cnt: free after the compaction map
+  k_inplace_rescan<256, T><<<sms * 4, 256, 0, st>>>(cur, ld, M, amask, pa.cnt, nmulti + 1, key);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void *scratch,
-                        const ScratchLayout &L, bool keep_rows, cudaStream_t st, int32_t *za,
-                        int32_t *zb, float *zh, int32_t *zs, LinkageOut *out, int *launches,
+                        const ScratchLayout &L, bool keep_rows, const CodeMode *cm, cudaStream_t st,
+                        int32_t *za, int32_t *zb, float *zh, int32_t *zs, LinkageOut *out, int *launches,
                         const std::function<void(int64_t)> &on_round) {
   out->rounds = 0;
   if (N <= 1) return cudaSuccess;
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // Code mode (cm != nullptr): the matrices hold 16-bit order-preserving codes
+  // of the Eq. 1 values (written by the distance kernel next to the fp32 rows)
+  // instead of the values: half the bytes per round, same merges (max and
+  // compare commute with an order-preserving map).  Round keys become code
+  // keys; heights are decoded through cm->vals.
+  const bool codes = cm != nullptr;
 
   u64 *key[2] = {nnkey, at<u64>(scratch, L.key1)};
   int *rep[2] = {at<int>(scratch, L.rep0), at<int>(scratch, L.rep1)};
   int *sz[2] = {at<int>(scratch, L.sz0), at<int>(scratch, L.sz1)};
-  float *matA = at<float>(scratch, L.matA);
-  float *matB = keep_rows ? at<float>(scratch, L.matB) : rows;
+  // float mode: rows -> matA -> matB (or rows) -> ...; code mode: codes ->
+  // mat16 -> codes -> ... (the fp32 rows are never touched)
+  void *matA = codes ? static_cast<void *>(cm->mat16) : at<void>(scratch, L.matA);
+  void *matB = codes ? static_cast<void *>(cm->codes) : (keep_rows ? at<void>(scratch, L.matB) : static_cast<void *>(rows));
   int *counters = at<int>(scratch, L.counters);  // [0] zcount, [1] Mn
   cudaError_t e;
   k_init_state<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(rep[0], sz[0], N);
@@ -86,8 +152,15 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
   pa.Mn = counters + 1;
   pa.level = counters + 2;
   pa.cstat = counters + 4;
+  pa.vals = codes ? cm->vals : nullptr;
+  pa.pmap = codes ? at<int2>(scratch, L.pmap) : nullptr;
+  if (codes) {
+    k_keys_to_codes<<<sms, 256, 0, st>>>(nnkey, N, cm->vals, cm->ncode);
+    ++*launches;
+  }
 
-  float *cur = rows;
+  void *cur = codes ? static_cast<void *>(cm->codes) : static_cast<void *>(rows);
+  const void *original = cur;
   int64_t ld = N;
   int M = (int)N;   // rows of the current matrix (live + dead)
   int live = (int)N;  // live clusters
@@ -96,7 +169,7 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
   int *mlist = at<int>(scratch, L.mlist);
   int *nmulti = counters + 12;
   int p = 0;
-  float *next = matA;
+  void *next = matA;
   // RAGB_TRACE=1: per-round timing on stderr (diagnostics only).
   const bool trace = std::getenv("RAGB_TRACE") != nullptr;
   // RAGB_INPLACE=0 / 1: never / always take in-place rounds (testing); unset: cost model
@@ -123,7 +196,10 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
     pa.sz_n = sz[p ^ 1];
     k_prep_mark<<<1, PT, 0, st>>>(pa);
     uint32_t *adj = reinterpret_cast<uint32_t *>(next);  // free until the merge writes it
-    k_level_adj<<<sms * 4, 256, 0, st>>>(pa, adj);
+    if (codes)
+      k_level_adj<uint16_t><<<sms * 4, 256, 0, st>>>(pa, adj);
+    else
+      k_level_adj<float><<<sms * 4, 256, 0, st>>>(pa, adj);
     {
       const size_t m1 = std::min<size_t>((size_t)M, 1024);
       const size_t smem = std::max(2 * (size_t)((M + 31) / 32), m1 * ((m1 + 31) / 32)) * 4;
@@ -164,7 +240,7 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
     // in place when the merged rows, the rewritten columns (one scattered
     // 4-byte store per row and merge, ~30 row-equivalents per merge measured)
     // and the rescans cost less than rewriting the matrix (~live + Mn^2/M rows)
-    const bool inplace = Mn > 1 && cur != rows && M <= kInplaceMaxM && inplace_mode != 0 &&
+    const bool inplace = Mn > 1 && cur != original && M <= kInplaceMaxM && inplace_mode != 0 &&
                          (inplace_mode == 1 || 32.0 * merges_round < (double)live + (double)Mn * Mn / M);
     if (inplace) {
       if (!mask_ok) {
@@ -172,47 +248,32 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
         mask_ok = true;
       }
       if ((e = cudaMemsetAsync(nmulti, 0, 8, st)) != cudaSuccess) return e;  // nmulti, nres
-      k_inplace_prep<<<sms * 2, 256, 0, st>>>(pa, M, amask, mlist, nmulti, sz[p], key[p]);
-      const size_t smem = (size_t)((M + 3) & ~3) * 4;
-      cudaFuncSetAttribute(k_inplace_rows<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      k_inplace_rows<512><<<sms * 2, 512, smem, st>>>(pa, cur, ld, M, amask, mlist, nmulti, key[p]);
-      k_inplace_cols<<<sms * 8, 256, 0, st>>>(pa, cur, ld, M, amask, mlist, nmulti);
-      k_inplace_check<<<(M + 255) / 256, 256, 0, st>>>(pa, cur, ld, M, key[p], pa.cnt, nmulti + 1);  // cnt: free after the compaction map
-      k_inplace_rescan<256><<<sms * 4, 256, 0, st>>>(cur, ld, M, amask, pa.cnt, nmulti + 1, key[p]);
+      e = codes ? launch_inplace<uint16_t>(static_cast<uint16_t *>(cur), ld, M, pa, sms, amask, mlist, nmulti,
+                                           sz[p], key[p], st)
+                : launch_inplace<float>(static_cast<float *>(cur), ld, M, pa, sms, amask, mlist, nmulti, sz[p],
+                                        key[p], st);
       *launches += 5;
-      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+      if (e != cudaSuccess) return e;
     } else if (Mn > 1) {
-      // window: the whole new row if it fits in shared memory, else pieces.
-      // Wide rows: 1024-thread CTAs, one per SM; narrow rows: 256-thread CTAs
-      // so that several rows are in flight per SM (per-row latency dominates).
-      const bool vec = (ld & 3) == 0 && (reinterpret_cast<uintptr_t>(cur) & 15) == 0;
-      const bool wide = Mn > 20 * 1024;
-      const int maxW = wide ? 56 * 1024 : 20 * 1024;
-      const int W = std::min<int>((Mn + 3) & ~3, maxW);
-      const size_t smem = (size_t)W * 4;
-      const int nth = wide ? 1024 : 256;
-      auto kern = wide ? (vec ? k_merge_rows<true, 1024, LocalRows> : k_merge_rows<false, 1024, LocalRows>)
-                       : (vec ? k_merge_rows<true, 256, LocalRows> : k_merge_rows<false, 256, LocalRows>);
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      int per_sm = 1;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nth, smem);
-      const int grid = std::min<int>(Mn, sms * std::max(per_sm, 1));
       cudaEvent_t me[2];
       cudaEventCreate(&me[0]);
       cudaEventCreate(&me[1]);
       cudaEventRecord(me[0], st);
-      kern<<<grid, nth, smem, st>>>(LocalRows{cur, ld}, M, pa.Mn, pa.goff, pa.gmem, pa.colsrc, pa.cursor, W, 0,
-                                    -1, next, key[p ^ 1]);
+      e = codes ? launch_merge<uint16_t>(static_cast<const uint16_t *>(cur), ld, M, Mn, pa, sms,
+                                         static_cast<uint16_t *>(next), key[p ^ 1], st)
+                : launch_merge<float>(static_cast<const float *>(cur), ld, M, Mn, pa, sms, static_cast<float *>(next),
+                                      key[p ^ 1], st);
       cudaEventRecord(me[1], st);
       mev.push_back(me[0]);
       mev.push_back(me[1]);
-      out->merge_bytes += 4.0 * ((double)live * live + (double)Mn * Mn);
+      const double es = codes ? 2.0 : 4.0;
+      out->merge_bytes += es * ((double)live * live + (double)Mn * Mn);
       ++out->merge_launches;
       ++*launches;
-      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+      if (e != cudaSuccess) return e;
       cur = next;
       next = (next == matA) ? matB : matA;
-      ld = ((int64_t)Mn + 3) & ~3ll;  // padded leading dimension of the new matrix
+      ld = codes ? mat_ld<uint16_t>(Mn) : mat_ld<float>(Mn);  // padded leading dimension of the new matrix
       mask_ok = false;
     }
     if (trace) {

@@ -16,9 +16,57 @@ constexpr int PT = 1024;  // threads of the single-CTA round-prep kernel
 constexpr u64 kDead = ~0ull;  // row key of a row merged away by an in-place round
 constexpr int kInplaceMaxM = 48 * 1024;  // in-place rounds keep a whole row in shared memory
 
+// ---------------------------------------------------------------------------
+// Stored element of the linkage matrices.  float: the Eq. 1 value itself;
+// uint16_t: its order-preserving code (rank among the distinct values of the
+// Eq. 1 table), so that max / compare / equality on codes are
+// max / compare / equality on the values (complete linkage only takes max and
+// compares, X7).  Both are handled as unsigned "bits": d >= 0, so the float's
+// bit pattern orders like the float.  A 16-byte vector holds VW elements.
+template <typename T>
+struct Elem;
+template <>
+struct Elem<float> {
+  static constexpr int VW = 4;
+  __device__ __forceinline__ static unsigned bits(float v) { return __float_as_uint(v); }
+  __device__ __forceinline__ static float make(unsigned b) { return __uint_as_float(b); }
+  __device__ __forceinline__ static unsigned vmax(unsigned a, unsigned b) { return max(a, b); }
+  __device__ __forceinline__ static void unpack(const uint4 &v, unsigned (&o)[VW]) {
+    o[0] = v.x;
+    o[1] = v.y;
+    o[2] = v.z;
+    o[3] = v.w;
+  }
+  __device__ __forceinline__ static uint4 pack(const unsigned (&o)[VW]) { return make_uint4(o[0], o[1], o[2], o[3]); }
+};
+template <>
+struct Elem<uint16_t> {
+  static constexpr int VW = 8;
+  __device__ __forceinline__ static unsigned bits(uint16_t v) { return v; }
+  __device__ __forceinline__ static uint16_t make(unsigned b) { return (uint16_t)b; }
+  __device__ __forceinline__ static unsigned vmax(unsigned a, unsigned b) { return __vmaxu2(a, b); }
+  __device__ __forceinline__ static void unpack(const uint4 &v, unsigned (&o)[VW]) {
+    const unsigned w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      o[2 * k] = w[k] & 0xffffu;
+      o[2 * k + 1] = w[k] >> 16;
+    }
+  }
+  __device__ __forceinline__ static uint4 pack(const unsigned (&o)[VW]) {
+    return make_uint4(o[0] | (o[1] << 16), o[2] | (o[3] << 16), o[4] | (o[5] << 16), o[6] | (o[7] << 16));
+  }
+};
+template <typename T>
+__device__ __forceinline__ uint4 vmax4(const uint4 &a, const uint4 &b) {
+  return make_uint4(Elem<T>::vmax(a.x, b.x), Elem<T>::vmax(a.y, b.y), Elem<T>::vmax(a.z, b.z),
+                    Elem<T>::vmax(a.w, b.w));
+}
+
 struct PrepArgs {
-  const float *D;
+  const void *D;  // current matrix (float or uint16_t codes, see Elem)
   int64_t ld;
+  const float *vals;  // code -> Eq. 1 value (uint16_t matrices), or nullptr (float matrices)
   int M;
   const u64 *key;
   const int *rep;
@@ -32,6 +80,7 @@ struct PrepArgs {
   int *newidx, *goff, *gmem, *colsrc /* colmap */, *cnt, *cursor /* then first_old */;
   int *rep_n, *sz_n;
   int *Mn;
+  int2 *pmap;  // [Mn + 8] new column -> (leader, other member of a pair | -1 singleton | -2 larger), or nullptr
   int *level;  // [0] level list length, [1] h bits
   int *cstat;  // clique diagnostics: starts, batches, picks, candidates, level n, clk/1k (warp0, pass)
 };
@@ -102,7 +151,6 @@ __global__ void __launch_bounds__(PT, 1) k_prep_mark(PrepArgs a) {
   if ((tid & 31) == 0) atomicMin(&S.h, hl);
   __syncthreads();
   const unsigned h = S.h;
-  const float hf = __uint_as_float(h);
 
   // -- 2. RNN pairs above h; vertices at h become clique candidates ------------
   for (int x = tid; x < M; x += PT) {
@@ -119,7 +167,7 @@ __global__ void __launch_bounds__(PT, 1) k_prep_mark(PrepArgs a) {
         const int pos = atomicAdd(a.zcount, 1);
         a.za[pos] = a.rep[x];
         a.zb[pos] = a.rep[y];
-        a.zh[pos] = __uint_as_float(hx);
+        a.zh[pos] = a.vals ? a.vals[hx] : __uint_as_float(hx);
         a.zs[pos] = a.sz[x] + a.sz[y];
       }
     }
@@ -140,10 +188,12 @@ __global__ void __launch_bounds__(PT, 1) k_prep_mark(PrepArgs a) {
 // Round step 2 (grid): adjacency bits of the level graph, adj[i][w] bit j <=>
 // D[list[i]][list[32w + j]] == h (j != i).  One warp per word: 32 lanes read
 // 32 ascending columns of the same row.
+template <typename T>
 __global__ void k_level_adj(PrepArgs a, uint32_t *__restrict__ adj) {
   const int n = a.level[0];
   if (n < 2) return;
-  const float hf = __uint_as_float((unsigned)a.level[1]);
+  const unsigned hb = (unsigned)a.level[1];
+  const T *D = static_cast<const T *>(a.D);
   const int W = (n + 31) >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -153,7 +203,7 @@ __global__ void k_level_adj(PrepArgs a, uint32_t *__restrict__ adj) {
     const int i = (int)(q / W), w = (int)(q - (int64_t)i * W);
     const int j = w * 32 + lane;
     bool bit = false;
-    if (j < n && j != i) bit = __ldg(a.D + (int64_t)a.list[i] * a.ld + a.list[j]) == hf;
+    if (j < n && j != i) bit = Elem<T>::bits(__ldg(D + (int64_t)a.list[i] * a.ld + a.list[j])) == hb;
     const unsigned word = __ballot_sync(0xffffffffu, bit);
     if (lane == 0) adj[q] = word;
   }
@@ -297,7 +347,7 @@ __global__ void __launch_bounds__(CT, 1) k_level_cliques(PrepArgs a,
   __shared__ int s_sv[CT / 32], s_sf[CT / 32];
   const int n = a.level[0];
   if (n < 2) return;
-  const float hf = __uint_as_float((unsigned)a.level[1]);
+  const float hf = a.vals ? a.vals[a.level[1]] : __uint_as_float((unsigned)a.level[1]);
   const int W = (n + 31) >> 5;
   uint32_t *A = bits, *C = bits + W;
   int *seq = a.candA, *seqs = a.candB;  // pick list position, its clique's start position
@@ -563,14 +613,27 @@ __global__ void __launch_bounds__(PT, 1) k_prep_compact(PrepArgs a) {
     a.gmem[a.goff[g] + atomicAdd(&a.cursor[g], 1)] = x;
   }
   __syncthreads();
-  // old column -> new column; new column -> its leader (smallest old member)
+  // old column -> new column | writer class << 29 (k_merge_rows): 0 the
+  // group's leader (smallest member), 1 the other member of a 2-member group,
+  // 2 a non-leader of a larger group; new column -> its leader (first_old)
   for (int x = tid; x < M; x += PT) {
     const int l = a.leader[x];
     const int g = l < 0 ? -1 : a.newidx[l];
-    a.colsrc[x] = g;
+    const int cls = (l == x || l < 0) ? 0 : (a.goff[g + 1] - a.goff[g] == 2 ? 1 : 2);
+    a.colsrc[x] = g < 0 ? -1 : (g | (cls << 29));
     if (l == x) a.cursor[g] = x;  // cursor is free after the scatter: first_old
+    if (a.pmap && g >= 0) {
+      const int gs = a.goff[g + 1] - a.goff[g];
+      if (l == x) {
+        a.pmap[g].x = x;
+        if (gs == 1) a.pmap[g].y = -1;
+      } else {
+        a.pmap[g].y = gs == 2 ? x : -2;
+      }
+    }
   }
-  if (tid < 4) a.colsrc[M + tid] = -1;  // padding for 16-byte colmap loads
+  if (a.pmap && tid < 8) a.pmap[Mn + tid] = make_int2(0, -1);  // padding of the last vector
+  if (tid < 8) a.colsrc[M + tid] = -1;  // padding for 16-byte colmap loads (8 codes per vector)
 }
 
 // Fused merge + compaction + row min (complete linkage, X7):
@@ -585,134 +648,211 @@ __global__ void __launch_bounds__(PT, 1) k_prep_compact(PrepArgs a) {
 // needs old columns >= first_old[T0] (members of later groups are never
 // smaller than their leader).
 
-// VEC: 16-byte loads of 4 consecutive old columns (old row stride and base are
-// multiples of 4 floats: every compacted matrix; the original rows when N % 4
-// == 0); colmap is padded with -1 to a multiple of 4.
+// VEC: 16-byte loads of VW consecutive old columns (old row stride and base are
+// multiples of VW elements: every compacted matrix; the original rows when
+// N % VW == 0); colmap is padded with -1 to a multiple of 8.
 // Old rows are addressed through a row source: the local matrix, or (row-
 // sharded build, dist.cu) the shard of the rank owning the row, read from peer
-// memory.  New rows [c0, c1) (c1 < 0: all Mn) are written to Dn[c - c0].
+// memory.  New rows [c0, c1) (c1 < 0: all Mn) are written to Dn[c - c0] with
+// the leading dimension round_up(Mn, VW).
+template <typename T>
 struct LocalRows {
-  const float *D;
+  const T *D;
   int64_t ld;
-  __device__ __forceinline__ const float *row(int x) const { return D + (int64_t)x * ld; }
+  __device__ __forceinline__ const T *row(int x) const { return D + (int64_t)x * ld; }
 };
+template <typename T>
 struct PeerRows {
-  const float *const *mats;  // [world] shard base of each rank (rows [q*S, (q+1)*S))
+  const T *const *mats;  // [world] shard base of each rank (rows [q*S, (q+1)*S))
   int S;
   int64_t ld;
-  __device__ __forceinline__ const float *row(int x) const {
+  __device__ __forceinline__ const T *row(int x) const {
     const int q = x / S;
     return mats[q] + (int64_t)(x - q * S) * ld;
   }
 };
 
-template <bool VEC, int NTH, typename RS>
+template <typename T>
+__host__ __device__ constexpr int64_t mat_ld(int64_t M) {
+  return (M + Elem<T>::VW - 1) / Elem<T>::VW * Elem<T>::VW;
+}
+
+// Window slot update by writer class (see k_prep_compact): the leader's
+// plain store comes first (phase A), then, after a barrier, the other members
+// fold in (phase B): the only other member of a pair with a plain
+// read-max-write, members of larger groups atomically.  Window elements have
+// the matrix's type (16-bit codes: 2 per 32-bit word, the atomic max is a CAS
+// loop on the word; concurrent 16-bit stores to the other half only make it
+// retry).
+template <typename T>
+struct Win;
+template <>
+struct Win<float> {
+  typedef unsigned S;
+  __device__ __forceinline__ static void amax(S *w, int t, unsigned v) { atomicMax(w + t, v); }
+};
+template <>
+struct Win<uint16_t> {
+  typedef uint16_t S;
+  __device__ __forceinline__ static void amax(S *w, int t, unsigned v) {
+    unsigned *word = reinterpret_cast<unsigned *>(w) + (t >> 1);
+    const int sh = (t & 1) * 16;
+    unsigned old = *reinterpret_cast<volatile unsigned *>(word);
+    while (((old >> sh) & 0xffffu) < v) {
+      const unsigned nw = (old & ~(0xffffu << sh)) | (v << sh);
+      const unsigned prev = atomicCAS(word, old, nw);
+      if (prev == old) break;
+      old = prev;
+    }
+  }
+};
+
+template <bool VEC, int NTH, typename T, typename RS>
 __global__ void __launch_bounds__(NTH) k_merge_rows(RS rs, int M, const int *__restrict__ Mn_p,
                                                     const int *__restrict__ goff,
                                                     const int *__restrict__ gmem,
                                                     const int *__restrict__ colmap,
                                                     const int *__restrict__ first_old, int W, int c0, int c1,
-                                                    float *__restrict__ Dn, u64 *__restrict__ keyn) {
-  extern __shared__ __align__(16) int win[];  // [W] float bits (d >= 0: int order == float order)
+                                                    T *__restrict__ Dn, u64 *__restrict__ keyn) {
+  typedef Elem<T> E;
+  typedef typename Win<T>::S S;
+  constexpr int VW = E::VW;
+  extern __shared__ __align__(16) unsigned char wbytes[];
+  S *win = reinterpret_cast<S *>(wbytes);  // [W] element bits (unsigned order == value order)
   __shared__ u64 wmin[NTH / 32];
   const int Mn = *Mn_p;
   const int cend = c1 < 0 ? Mn : c1;
-  const int64_t ldn = (Mn + 3) & ~3;
+  const int64_t ldn = mat_ld<T>(Mn);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   for (int c = c0 + blockIdx.x; c < cend; c += gridDim.x) {
     const int rb = goff[c], re = goff[c + 1];
-    const float *__restrict__ row0 = rs.row(gmem[rb]);
+    const T *__restrict__ row0 = rs.row(gmem[rb]);
     int bval = 0x7fffffff, bidx = 0x7fffffff;  // running (value bits, column) minimum
     for (int T0 = 0; T0 < Mn; T0 += W) {
       const int Wn = min(W, Mn - T0);
-      for (int i = tid * 4; i < Wn; i += NTH * 4) *reinterpret_cast<int4 *>(win + i) = int4{0, 0, 0, 0};
-      __syncthreads();
-      const int s0 = T0 == 0 ? 0 : (first_old[T0] & ~3);
+      const int Wv = (Wn + VW - 1) / VW * VW;  // whole vectors (W is a multiple of VW)
+      for (int i = Wn + tid; i < Wv; i += NTH) win[i] = 0;  // padding columns of the last vector
+      const int s0 = T0 == 0 ? 0 : (first_old[T0] & ~(VW - 1));
+      // every slot of the window has its leader at an old column >= s0, read
+      // in a block-uniform loop (phase A / barrier / phase B per pass)
       if (VEC) {
-        const float4 *__restrict__ r4 = reinterpret_cast<const float4 *>(row0);
+        const uint4 *__restrict__ r4 = reinterpret_cast<const uint4 *>(row0);
         const int4 *__restrict__ c4 = reinterpret_cast<const int4 *>(colmap);
-        constexpr int UV = 4;
-        for (int qb = (s0 >> 2) + tid; qb * 4 < M; qb += NTH * UV) {
-          int4 t4[UV];
-          float4 v4[UV];
+        constexpr int UV = 16 / VW;  // 16 elements per thread and pass (registers: 1024 threads)
+        for (int base = s0 / VW; base * VW < M; base += NTH * UV) {
+          uint4 v4[UV];
+          bool ok[UV];
 #pragma unroll
           for (int u = 0; u < UV; ++u) {
-            const int q = qb + u * NTH;
-            const bool ok = q * 4 < M;
-            t4[u] = ok ? __ldg(c4 + q) : int4{-1, -1, -1, -1};
-            v4[u] = ok ? __ldcs(r4 + q) : float4{0, 0, 0, 0};
+            const int q = base + tid + u * NTH;
+            ok[u] = q * VW < M;
+            v4[u] = ok[u] ? __ldcs(r4 + q) : make_uint4(0, 0, 0, 0);
           }
           for (int rr = rb + 1; rr < re; ++rr) {  // other row members (max)
-            const float4 *__restrict__ k4 = reinterpret_cast<const float4 *>(rs.row(gmem[rr]));
+            const uint4 *__restrict__ k4 = reinterpret_cast<const uint4 *>(rs.row(gmem[rr]));
 #pragma unroll
-            for (int u = 0; u < UV; ++u) {
-              const int q = qb + u * NTH;
-              if (q * 4 < M) {
-                const float4 x = __ldcs(k4 + q);
-                v4[u].x = fmaxf(v4[u].x, x.x);
-                v4[u].y = fmaxf(v4[u].y, x.y);
-                v4[u].z = fmaxf(v4[u].z, x.z);
-                v4[u].w = fmaxf(v4[u].w, x.w);
-              }
-            }
+            for (int u = 0; u < UV; ++u)
+              if (ok[u]) v4[u] = vmax4<T>(v4[u], __ldcs(k4 + base + tid + u * NTH));
           }
+          unsigned vv[UV][VW];
+          int tt[UV][VW];
 #pragma unroll
           for (int u = 0; u < UV; ++u) {
-            const int tt[4] = {t4[u].x - T0, t4[u].y - T0, t4[u].z - T0, t4[u].w - T0};
-            const float vv[4] = {v4[u].x, v4[u].y, v4[u].z, v4[u].w};
+            E::unpack(v4[u], vv[u]);
+            const int q = base + tid + u * NTH;
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              if ((unsigned)tt[k] < (unsigned)Wn) atomicMax(win + tt[k], __float_as_int(vv[k]));
+            for (int g = 0; g < VW / 4; ++g) {
+              const int4 t4 = ok[u] ? __ldg(c4 + q * (VW / 4) + g) : int4{-1, -1, -1, -1};
+              tt[u][4 * g] = t4.x;
+              tt[u][4 * g + 1] = t4.y;
+              tt[u][4 * g + 2] = t4.z;
+              tt[u][4 * g + 3] = t4.w;
+            }
           }
+          // phase A: leaders
+#pragma unroll
+          for (int u = 0; u < UV; ++u)
+#pragma unroll
+            for (int k = 0; k < VW; ++k) {
+              const int x = tt[u][k];
+              const int t = (x & 0x1fffffff) - T0;
+              if (x >= 0 && (x >> 29) == 0 && (unsigned)t < (unsigned)Wn) win[t] = (S)vv[u][k];
+            }
+          __syncthreads();
+          // phase B: the other members
+#pragma unroll
+          for (int u = 0; u < UV; ++u)
+#pragma unroll
+            for (int k = 0; k < VW; ++k) {
+              const int x = tt[u][k];
+              const int t = (x & 0x1fffffff) - T0;
+              if (x >= 0 && (x >> 29) != 0 && (unsigned)t < (unsigned)Wn) {
+                if ((x >> 29) == 1) {
+                  if (vv[u][k] > (unsigned)win[t]) win[t] = (S)vv[u][k];
+                } else {
+                  Win<T>::amax(win, t, vv[u][k]);
+                }
+              }
+            }
         }
       } else {
         constexpr int U = 4;
         for (int sb = s0; sb < M; sb += U * NTH) {
           int t[U];
-          float v[U];
+          unsigned v[U];
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const int s = sb + u * NTH + tid;
-            t[u] = s < M ? __ldg(colmap + s) - T0 : -1;
-            v[u] = s < M ? __ldcs(row0 + s) : 0.0f;
+            t[u] = s < M ? __ldg(colmap + s) : -1;
+            v[u] = s < M ? E::bits(__ldcs(row0 + s)) : 0u;
           }
           for (int rr = rb + 1; rr < re; ++rr) {
-            const float *rowk = rs.row(gmem[rr]);
+            const T *rowk = rs.row(gmem[rr]);
 #pragma unroll
             for (int u = 0; u < U; ++u) {
               const int s = sb + u * NTH + tid;
-              if (s < M) v[u] = fmaxf(v[u], __ldcs(rowk + s));
+              if (s < M) v[u] = max(v[u], E::bits(__ldcs(rowk + s)));
             }
           }
 #pragma unroll
-          for (int u = 0; u < U; ++u)
-            if ((unsigned)t[u] < (unsigned)Wn) atomicMax(win + t[u], __float_as_int(v[u]));
+          for (int u = 0; u < U; ++u) {
+            const int x = t[u], tw = (x & 0x1fffffff) - T0;
+            if (x >= 0 && (x >> 29) == 0 && (unsigned)tw < (unsigned)Wn) win[tw] = (S)v[u];
+          }
+          __syncthreads();
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int x = t[u], tw = (x & 0x1fffffff) - T0;
+            if (x >= 0 && (x >> 29) != 0 && (unsigned)tw < (unsigned)Wn) {
+              if ((x >> 29) == 1) {
+                if (v[u] > (unsigned)win[tw]) win[tw] = (S)v[u];
+              } else {
+                Win<T>::amax(win, tw, v[u]);
+              }
+            }
+          }
         }
       }
       __syncthreads();
-      // write out (16-byte stores; the new leading dimension is a multiple of 4)
-      float4 *__restrict__ out4 = reinterpret_cast<float4 *>(Dn + (int64_t)(c - c0) * ldn + T0);
+      // write out (16-byte stores; the new leading dimension is a multiple of VW)
+      uint4 *__restrict__ out4 = reinterpret_cast<uint4 *>(Dn + (int64_t)(c - c0) * ldn + T0);
       const int cd = c - T0;  // diagonal position inside the window
-      for (int i = tid * 4; i < Wn; i += NTH * 4) {
-        int4 q = *reinterpret_cast<const int4 *>(win + i);
-        // diagonal -> 0 in the matrix, excluded from the row minimum
-        const int4 qm = {(i == cd || i >= Wn) ? 0x7fffffff : q.x,
-                         (i + 1 == cd || i + 1 >= Wn) ? 0x7fffffff : q.y,
-                         (i + 2 == cd || i + 2 >= Wn) ? 0x7fffffff : q.z,
-                         (i + 3 == cd || i + 3 >= Wn) ? 0x7fffffff : q.w};
-        if ((unsigned)(cd - i) < 4u) {
-          q.x = i == cd ? 0 : q.x;
-          q.y = i + 1 == cd ? 0 : q.y;
-          q.z = i + 2 == cd ? 0 : q.z;
-          q.w = i + 3 == cd ? 0 : q.w;
+      for (int i = tid * VW; i < Wn; i += NTH * VW) {
+        unsigned q[VW];
+        E::unpack(*reinterpret_cast<const uint4 *>(win + i), q);
+        // diagonal -> 0 in the matrix, excluded from the row minimum (as are
+        // the padding columns); strict '<' keeps the earliest column (X8)
+#pragma unroll
+        for (int k = 0; k < VW; ++k) {
+          const bool skip = i + k == cd || i + k >= Wn;
+          const int m = skip ? 0x7fffffff : (int)q[k];
+          if (m < bval) {
+            bval = m;
+            bidx = T0 + i + k;
+          }
+          q[k] = i + k == cd ? 0u : q[k];
         }
-        __stcs(out4 + (i >> 2), make_float4(__int_as_float(q.x), __int_as_float(q.y),
-                                            __int_as_float(q.z), __int_as_float(q.w)));
-        const int m4 = min(min(qm.x, qm.y), min(qm.z, qm.w));
-        if (m4 < bval) {  // strict: the earliest column wins among equal values (X8)
-          bval = m4;
-          bidx = T0 + i + (qm.x == m4 ? 0 : qm.y == m4 ? 1 : qm.z == m4 ? 2 : 3);
-        }
+        __stcs(out4 + i / VW, E::pack(q));
       }
       __syncthreads();
     }
@@ -731,6 +871,153 @@ __global__ void __launch_bounds__(NTH) k_merge_rows(RS rs, int M, const int *__r
       keyn[c] = b;
     }
     __syncthreads();
+  }
+}
+
+// 1-D bulk copies (TMA engine, cp.async.bulk) global -> shared, completion
+// counted in bytes on an mbarrier.
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// Code-mode compaction when the old row fits in shared memory (2 B x M <=
+// 227 KB): one CTA per new row c.  Phase 1 streams the old row(s) of group c
+// into shared memory in the OLD column order (16-byte loads, max over the
+// group's rows, no atomics); phase 2 gathers each new column t from its
+// leader's slot, folded with the other member of a pair (pmap) or, for larger
+// groups, every member (CSR) — 16-byte stores of 8 new columns and the row min.
+template <bool VEC, int NTH>
+__global__ void __launch_bounds__(NTH) k_merge_gather(const uint16_t *__restrict__ D, int64_t ld, int M,
+                                                      const int *__restrict__ Mn_p, const int *__restrict__ goff,
+                                                      const int *__restrict__ gmem, const int2 *__restrict__ pmap,
+                                                      uint16_t *__restrict__ Dn, u64 *__restrict__ keyn) {
+  typedef Elem<uint16_t> E;
+  extern __shared__ __align__(16) uint4 srow4[];  // [ceil(M / 8)]
+  const uint16_t *srow = reinterpret_cast<const uint16_t *>(srow4);
+  __shared__ u64 wmin[NTH / 32];
+  const int Mn = *Mn_p;
+  const int64_t ldn = mat_ld<uint16_t>(Mn);
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int MV = (M + 7) >> 3;
+  __shared__ __align__(8) unsigned long long bar;
+  unsigned parity = 0u;
+  if (VEC && tid == 0) mbar_init(&bar, 1);
+  __syncthreads();
+  for (int c = blockIdx.x; c < Mn; c += gridDim.x) {
+    const int rb = goff[c], re = goff[c + 1];
+    // ---- phase 1: old row(s) -> shared memory -------------------------------
+    if (VEC) {
+      // the first member's row by bulk copies (all of it in flight at once),
+      // then the other members folded in with 16-byte loads
+      if (tid == 0) {
+        fence_proxy_async_smem();  // the previous row's generic reads of srow come first
+        const unsigned bytes = (unsigned)MV * 16u;
+        mbar_expect_tx(&bar, bytes);
+        const unsigned char *src = reinterpret_cast<const unsigned char *>(D + (int64_t)gmem[rb] * ld);
+        unsigned char *dst = reinterpret_cast<unsigned char *>(srow4);
+        for (unsigned o = 0; o < bytes; o += 32768u) bulk_g2s(dst + o, src + o, min(32768u, bytes - o), &bar);
+      }
+      mbar_wait(&bar, parity);
+      parity ^= 1u;
+      if (re - rb > 1) {
+        constexpr int UV = 8;
+        for (int qb = tid; qb < MV; qb += NTH * UV) {
+          uint4 v[UV];
+#pragma unroll
+          for (int u = 0; u < UV; ++u) {
+            const int q = qb + u * NTH;
+            v[u] = make_uint4(0, 0, 0, 0);
+            for (int rr = rb + 1; rr < re; ++rr)
+              if (q < MV) v[u] = vmax4<uint16_t>(v[u], __ldcs(reinterpret_cast<const uint4 *>(D + (int64_t)gmem[rr] * ld) + q));
+          }
+#pragma unroll
+          for (int u = 0; u < UV; ++u) {
+            const int q = qb + u * NTH;
+            if (q < MV) srow4[q] = vmax4<uint16_t>(srow4[q], v[u]);
+          }
+        }
+      }
+    } else {
+      uint16_t *sr = reinterpret_cast<uint16_t *>(srow4);
+      for (int s = tid; s < M; s += NTH) {
+        unsigned v = 0u;
+        for (int rr = rb; rr < re; ++rr) v = max(v, (unsigned)__ldcs(D + (int64_t)gmem[rr] * ld + s));
+        sr[s] = (uint16_t)v;
+      }
+    }
+    __syncthreads();
+    // ---- phase 2: gather the new row ----------------------------------------
+    // a thread takes 2 consecutive new columns per step (lanes read adjacent
+    // slots: no bank conflicts; 4-byte stores coalesce per warp), UP steps
+    // per iteration for memory-level parallelism on the pmap loads
+    int bval = 0x7fffffff, bidx = 0x7fffffff;
+    unsigned *__restrict__ out2 = reinterpret_cast<unsigned *>(Dn + (int64_t)c * ldn);
+    const int4 *__restrict__ pm4 = reinterpret_cast<const int4 *>(pmap);
+    const int npair = (Mn + 1) >> 1;
+    constexpr int UP = NTH <= 512 ? 16 : 4;
+    for (int pb = tid; pb < npair; pb += NTH * UP) {
+      int4 pm[UP];
+#pragma unroll
+      for (int u = 0; u < UP; ++u) {
+        const int pi = pb + u * NTH;
+        pm[u] = pi < npair ? __ldg(pm4 + pi) : make_int4(0, -1, 0, -1);
+      }
+#pragma unroll
+      for (int u = 0; u < UP; ++u) {
+        const int pi = pb + u * NTH;
+        const int t0 = 2 * pi;
+        const int xs[2] = {pm[u].x, pm[u].z}, ys[2] = {pm[u].y, pm[u].w};
+        unsigned q[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          unsigned v = srow[xs[k]];
+          if (ys[k] >= 0) v = max(v, (unsigned)srow[ys[k]]);
+          if (ys[k] == -2)  // larger group (a level clique): every member
+            for (int r = goff[t0 + k]; r < goff[t0 + k + 1]; ++r) v = max(v, (unsigned)srow[gmem[r]]);
+          const int t = t0 + k;
+          q[k] = t == c ? 0u : v;  // diagonal (excluded from the minimum)
+          const int m = (t == c || t >= Mn) ? 0x7fffffff : (int)v;
+          if (m < bval) {  // strict: the earliest column wins among equal values (X8)
+            bval = m;
+            bidx = t;
+          }
+        }
+        if (pi < npair) __stcs(out2 + pi, q[0] | (q[1] << 16));
+      }
+    }
+    u64 best = bval == 0x7fffffff ? ~0ull : (((u64)(unsigned)bval << 32) | (unsigned)bidx);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const u64 y = __shfl_xor_sync(0xffffffffu, best, o);
+      best = y < best ? y : best;
+    }
+    if (lane == 0) wmin[w] = best;
+    __syncthreads();  // also: every gather of this row is done before phase 1 of the next
+    if (tid == 0) {
+      u64 b = wmin[0];
+#pragma unroll
+      for (int k = 1; k < NTH / 32; ++k) b = wmin[k] < b ? wmin[k] : b;
+      keyn[c] = b;
+    }
   }
 }
 
@@ -773,53 +1060,52 @@ __global__ void k_inplace_prep(PrepArgs a, int M, uint32_t *__restrict__ amask, 
 // row(L)[c] = max over members m of D[m][c]; then the entries at the other
 // merged groups' survivors, row(L)[L_h] = max over x in h of row(L)[x]; the
 // diagonal; write back and the row's nearest neighbour over live columns.
-template <int NTH>
-__global__ void __launch_bounds__(NTH, 2) k_inplace_rows(PrepArgs a, float *__restrict__ D, int64_t ld, int M,
+template <int NTH, typename T>
+__global__ void __launch_bounds__(NTH, 2) k_inplace_rows(PrepArgs a, T *__restrict__ D, int64_t ld, int M,
                                                       const uint32_t *__restrict__ amask,
                                                       const int *__restrict__ mlist,
                                                       const int *__restrict__ nmulti_p, u64 *__restrict__ key) {
-  extern __shared__ __align__(16) float row[];  // [M rounded up to 4]
+  typedef Elem<T> E;
+  constexpr int VW = E::VW;
+  extern __shared__ __align__(16) uint4 rowv[];  // [ceil(M / VW)] vectors
+  T *row = reinterpret_cast<T *>(rowv);
   __shared__ u64 wmin[NTH / 32];
   const int nmulti = *nmulti_p;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int M4 = (M + 3) >> 2;
+  const int MV = (M + VW - 1) / VW;
   for (int gi = blockIdx.x; gi < nmulti; gi += gridDim.x) {
     const int g = mlist[gi];
     const int rb = a.goff[g], re = a.goff[g + 1];
     const int L = a.cursor[g];  // first_old: the survivor
-    for (int q = tid; q < M4; q += NTH) {
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int r = rb; r < re; ++r) {
-        const float4 x = __ldcs(reinterpret_cast<const float4 *>(D + (int64_t)a.gmem[r] * ld) + q);
-        v.x = fmaxf(v.x, x.x);
-        v.y = fmaxf(v.y, x.y);
-        v.z = fmaxf(v.z, x.z);
-        v.w = fmaxf(v.w, x.w);
-      }
-      reinterpret_cast<float4 *>(row)[q] = v;
+    for (int q = tid; q < MV; q += NTH) {
+      uint4 v = make_uint4(0, 0, 0, 0);
+      for (int r = rb; r < re; ++r)
+        v = vmax4<T>(v, __ldcs(reinterpret_cast<const uint4 *>(D + (int64_t)a.gmem[r] * ld) + q));
+      rowv[q] = v;
     }
     __syncthreads();
     for (int hi = tid; hi < nmulti; hi += NTH) {
       const int h = mlist[hi];
       if (h == g) continue;
-      float v = 0.f;
-      for (int r = a.goff[h]; r < a.goff[h + 1]; ++r) v = fmaxf(v, row[a.gmem[r]]);
-      row[a.cursor[h]] = v;
+      unsigned v = 0u;
+      for (int r = a.goff[h]; r < a.goff[h + 1]; ++r) v = max(v, E::bits(row[a.gmem[r]]));
+      row[a.cursor[h]] = E::make(v);
     }
     __syncthreads();
-    if (tid == 0) row[L] = 0.f;
+    if (tid == 0) row[L] = E::make(0u);
     __syncthreads();
     u64 best = ~0ull;
-    float4 *out = reinterpret_cast<float4 *>(D + (int64_t)L * ld);
-    for (int q = tid; q < M4; q += NTH) {
-      const float4 v = reinterpret_cast<const float4 *>(row)[q];
+    uint4 *out = reinterpret_cast<uint4 *>(D + (int64_t)L * ld);
+    for (int q = tid; q < MV; q += NTH) {
+      const uint4 v = rowv[q];
       __stcs(out + q, v);
-      const float vv[4] = {v.x, v.y, v.z, v.w};
+      unsigned vv[VW];
+      E::unpack(v, vv);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int c = 4 * q + k;
+      for (int k = 0; k < VW; ++k) {
+        const int c = VW * q + k;
         const bool live = c < M && c != L && ((amask[c >> 5] >> (c & 31)) & 1u);
-        const u64 kk = ((u64)__float_as_uint(vv[k]) << 32) | (unsigned)c;
+        const u64 kk = ((u64)vv[k] << 32) | (unsigned)c;
         best = (live && kk < best) ? kk : best;
       }
     }
@@ -842,9 +1128,10 @@ __global__ void __launch_bounds__(NTH, 2) k_inplace_rows(PrepArgs a, float *__re
 
 // S2: columns from rows (symmetry): D[r][L] = D[L][r] for every live row r.
 // Work items = (merged group, 1024-row chunk); each thread moves 4 rows
-// (coalesced loads, scattered 4-byte stores).  Few, long-lived CTAs: with one
+// (coalesced loads, scattered stores).  Few, long-lived CTAs: with one
 // short CTA per item the block scheduler, not the stores, set the pace.
-__global__ void __launch_bounds__(256) k_inplace_cols(PrepArgs a, float *__restrict__ D, int64_t ld, int M,
+template <typename T>
+__global__ void __launch_bounds__(256) k_inplace_cols(PrepArgs a, T *__restrict__ D, int64_t ld, int M,
                                                       const uint32_t *__restrict__ amask,
                                                       const int *__restrict__ mlist,
                                                       const int *__restrict__ nmulti_p) {
@@ -854,14 +1141,14 @@ __global__ void __launch_bounds__(256) k_inplace_cols(PrepArgs a, float *__restr
   for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
     const int gi = (int)(it / nchunk), ch = (int)(it - (int64_t)gi * nchunk);
     const int L = a.cursor[mlist[gi]];
-    const float *src = D + (int64_t)L * ld;
-    float v[4];
+    const T *src = D + (int64_t)L * ld;
+    T v[4];
     int rr[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int r = (ch << 10) + u * 256 + (int)threadIdx.x;
       rr[u] = (r < M && ((amask[r >> 5] >> (r & 31)) & 1u)) ? r : -1;
-      v[u] = rr[u] >= 0 ? __ldg(src + r) : 0.f;
+      v[u] = rr[u] >= 0 ? __ldg(src + r) : Elem<T>::make(0u);
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u)
@@ -874,7 +1161,8 @@ __global__ void __launch_bounds__(256) k_inplace_cols(PrepArgs a, float *__restr
 // (column L was rewritten by S2) is >= the old d(r, t); if equal, (d, L) is
 // the new key without a scan (L <= t, every other entry is unchanged or
 // larger); otherwise r goes to the rescan list.
-__global__ void k_inplace_check(PrepArgs a, const float *__restrict__ D, int64_t ld, int M,
+template <typename T>
+__global__ void k_inplace_check(PrepArgs a, const T *__restrict__ D, int64_t ld, int M,
                                 u64 *__restrict__ key, int *__restrict__ rlist, int *__restrict__ nres) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < M; r += gridDim.x * blockDim.x) {
     const u64 kr = key[r];
@@ -882,7 +1170,7 @@ __global__ void k_inplace_check(PrepArgs a, const float *__restrict__ D, int64_t
     const int t = (int)(kr & 0xffffffffu);
     if (!a.alive[t]) continue;  // neighbour not merged: unchanged
     const int Lg = a.leader[t];
-    const unsigned v = __float_as_uint(D[(int64_t)r * ld + Lg]);
+    const unsigned v = Elem<T>::bits(D[(int64_t)r * ld + Lg]);
     if (v == (unsigned)(kr >> 32))
       key[r] = ((u64)v << 32) | (unsigned)Lg;
     else
@@ -891,27 +1179,29 @@ __global__ void k_inplace_check(PrepArgs a, const float *__restrict__ D, int64_t
 }
 
 // S3b: full rescans of the listed rows over the live columns.
-template <int NTH>
-__global__ void __launch_bounds__(NTH) k_inplace_rescan(const float *__restrict__ D, int64_t ld, int M,
+template <int NTH, typename T>
+__global__ void __launch_bounds__(NTH) k_inplace_rescan(const T *__restrict__ D, int64_t ld, int M,
                                                         const uint32_t *__restrict__ amask,
                                                         const int *__restrict__ rlist,
                                                         const int *__restrict__ nres_p, u64 *__restrict__ key) {
+  typedef Elem<T> E;
+  constexpr int VW = E::VW;
   __shared__ u64 wmin[NTH / 32];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int M4 = (M + 3) >> 2;
+  const int MV = (M + VW - 1) / VW;
   const int nres = *nres_p;
   for (int i = blockIdx.x; i < nres; i += gridDim.x) {
     const int r = rlist[i];
     u64 best = ~0ull;
-    const float4 *src = reinterpret_cast<const float4 *>(D + (int64_t)r * ld);
-    for (int q = tid; q < M4; q += NTH) {
-      const float4 v = __ldcs(src + q);
-      const float vv[4] = {v.x, v.y, v.z, v.w};
+    const uint4 *src = reinterpret_cast<const uint4 *>(D + (int64_t)r * ld);
+    for (int q = tid; q < MV; q += NTH) {
+      unsigned vv[VW];
+      E::unpack(__ldcs(src + q), vv);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int c = 4 * q + k;
+      for (int k = 0; k < VW; ++k) {
+        const int c = VW * q + k;
         const bool live = c < M && c != r && ((amask[c >> 5] >> (c & 31)) & 1u);
-        const u64 kk = ((u64)__float_as_uint(vv[k]) << 32) | (unsigned)c;
+        const u64 kk = ((u64)vv[k] << 32) | (unsigned)c;
         best = (live && kk < best) ? kk : best;
       }
     }
@@ -929,6 +1219,27 @@ __global__ void __launch_bounds__(NTH) k_inplace_rescan(const float *__restrict_
       key[r] = b;
     }
     __syncthreads();
+  }
+}
+
+// Row keys of the distance kernel ((f32 bits << 32) | column) -> code keys:
+// the code of a value is its position in the ascending table vals[0, ncode).
+__global__ void k_keys_to_codes(u64 *__restrict__ key, int64_t N, const float *__restrict__ vals,
+                                const int *__restrict__ ncode_p) {
+  const int ncode = *ncode_p;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+    const u64 k = key[i];
+    if (k == ~0ull) continue;
+    const float v = __uint_as_float((unsigned)(k >> 32));
+    int lo = 0, hi = ncode - 1;  // vals strictly ascending and v is one of them
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (vals[mid] < v)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    key[i] = ((u64)(unsigned)lo << 32) | (k & 0xffffffffull);
   }
 }
 

@@ -250,13 +250,17 @@ def test_full_size_configs(name):
     assert np.array_equal(idx2.order_contexts()[0], out)
 
 
+@pytest.mark.parametrize("codes", ["0", "1"])
 @pytest.mark.parametrize("mode", ["0", "1"])
 @pytest.mark.parametrize("case", ["C2", "var", "ties"])
-def test_round_strategy(mode, case, monkeypatch):
+def test_round_strategy(mode, case, codes, monkeypatch):
     """Linkage rounds in place (RAGB_INPLACE=1, forced wherever allowed) or
-    always compacting (0) give the oracle's merge order (the strategy is an
-    implementation choice, X7-X9 fix the result)."""
+    always compacting (0), on fp32 matrices (RAGB_CODES=0) or on 16-bit value
+    codes (default where the Eq. 1 table exists), give the oracle's merge order
+    (the strategy and the stored form are implementation choices, X7-X9 fix
+    the result)."""
     monkeypatch.setenv("RAGB_INPLACE", mode)
+    monkeypatch.setenv("RAGB_CODES", codes)
     if case == "C2":
         check_full(config("C2").ids, counts=False)
     elif case == "var":
@@ -269,18 +273,21 @@ def test_round_strategy(mode, case, monkeypatch):
 
 def test_round_strategy_full_size(monkeypatch):
     """At C4 size (level cliques above 4096 vertices, block path) the merge
-    order and the document order do not depend on the round strategy."""
+    order and the document order do not depend on the round strategy nor on
+    the stored form of the matrices (fp32 values or 16-bit value codes)."""
     ids = config("C4").ids
     t = torch.from_numpy(ids.view(np.int32)).cuda()
     res = []
-    for mode in ("0", "2"):
+    for mode, codes in (("0", "1"), ("2", "1"), ("2", "0")):
         monkeypatch.setenv("RAGB_INPLACE", mode)
+        monkeypatch.setenv("RAGB_CODES", codes)
         idx, ws = F.build_index(t)
         res.append((idx.linkage(), idx.order_contexts()))
         del idx, ws
         torch.cuda.empty_cache()
-    for x, y in zip(res[0][0] + res[0][1], res[1][0] + res[1][1]):
-        assert np.array_equal(x, y)
+    for r in res[1:]:
+        for x, y in zip(res[0][0] + res[0][1], r[0] + r[1]):
+            assert np.array_equal(x, y)
 
 
 def test_multiturn_cumulative_index():
