@@ -119,22 +119,34 @@ __global__ void __launch_bounds__(NT, 2) k_dist_tile(DistArgs a, Plan P) {
     }
     __syncthreads();
 
-    float bv[R];
-    uint32_t bj[R];
+    // running row minimum per thread: (d, column) in fp32 mode; in code mode
+    // one packed word (code << 16 | chunk << 1 | column bit) — codes order
+    // like the values and, for one thread, (chunk, bit) orders like the
+    // column, so the strict minimum keeps the smallest column (X8) in half
+    // the registers
+    float bv[CODES ? 1 : R];
+    uint32_t bj[CODES ? 1 : R];
+    uint32_t bk[CODES ? R : 1];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      bv[r] = __int_as_float(0x7f800000);
-      bj[r] = 0xffffffffu;
+      if constexpr (CODES) {
+        bk[r] = 0xffffffffu;
+      } else {
+        bv[r] = __int_as_float(0x7f800000);
+        bj[r] = 0xffffffffu;
+      }
     }
 
     uint16_t *myq = qent + warp * P.qcap;
-    for (int64_t c0 = 0; c0 < N; c0 += CH) {
+    uint32_t chunk = 0;
+    for (int64_t c0 = 0; c0 < N; c0 += CH, ++chunk) {
       const int64_t jb = c0 + (int64_t)tid * CPT;
       const uint32_t *colp = a.idsT + jb;
 
       // ---- probe: filter every column doc, keep candidate bits per column --
       uint32_t cm0 = 0u, cm1 = 0u;  // bit k: doc k of column 0 / 1 may be in the tile
-#pragma unroll 4
+      constexpr int PU = CODES ? 6 : 4;  // column-doc loads in flight (registers)
+#pragma unroll PU
       for (int k = 0; k < K; ++k) {
         const uint2 v = __ldg(reinterpret_cast<const uint2 *>(colp + (int64_t)k * Npad));
         const uint32_t f0 = hash_filter(v.x), f1 = hash_filter(v.y);
@@ -239,12 +251,15 @@ __global__ void __launch_bounds__(NT, 2) k_dist_tile(DistArgs a, Plan P) {
             }
             __stcs(co, c0 | (c1 << 16));
             co += step;
+            const uint32_t lk = chunk << 1;
+            bk[r] = min(bk[r], min((c0 << 16) | lk, (c1 << 16) | lk | 1u));
+          } else {
+            // strict '<' keeps the smallest column among equal distances (X8)
+            const float m = fminf(d0, d1);
+            const bool u = m < bv[r];
+            bj[r] = u ? (d0 <= d1 ? j0 : j1) : bj[r];
+            bv[r] = u ? m : bv[r];
           }
-          // strict '<' keeps the smallest column among equal distances (X8)
-          const float m = fminf(d0, d1);
-          const bool u = m < bv[r];
-          bj[r] = u ? (d0 <= d1 ? j0 : j1) : bj[r];
-          bv[r] = u ? m : bv[r];
         }
       } else {
 #pragma unroll
@@ -263,10 +278,13 @@ __global__ void __launch_bounds__(NT, 2) k_dist_tile(DistArgs a, Plan P) {
               if (jb < N) __stcs(o, d0);
               if (jb + 1 < N) __stcs(o + 1, d1);
             }
+            uint32_t cc0 = 0u, cc1 = 0u;
             if (CODES) {
               uint16_t *cr = a.codes + (gi - a.row0) * N + jb;
-              if (jb < N) __stcs(cr, (uint16_t)__ldg(a.lutc + p0));
-              if (jb + 1 < N) __stcs(cr + 1, (uint16_t)__ldg(a.lutc + p1));
+              cc0 = __ldg(a.lutc + p0);
+              cc1 = __ldg(a.lutc + p1);
+              if (jb < N) __stcs(cr, (uint16_t)cc0);
+              if (jb + 1 < N) __stcs(cr + 1, (uint16_t)cc1);
             }
             if (COUNTS) {
               if (jb < N) {
@@ -278,13 +296,20 @@ __global__ void __launch_bounds__(NT, 2) k_dist_tile(DistArgs a, Plan P) {
                 a.D_out[(gi - a.row0) * N + jb + 1] = (uint16_t)(p1 & DMASK);
               }
             }
-            const float inf = __int_as_float(0x7f800000);
-            const float e0 = (jb < N && jb != gi) ? d0 : inf;
-            const float e1 = (jb + 1 < N && jb + 1 != gi) ? d1 : inf;
-            const float m = fminf(e0, e1);
-            const bool u = m < bv[r];
-            bj[r] = u ? (e0 <= e1 ? j0 : j1) : bj[r];
-            bv[r] = u ? m : bv[r];
+            if constexpr (CODES) {
+              const uint32_t lk = chunk << 1;
+              const uint32_t k0 = (jb < N && jb != gi) ? ((cc0 << 16) | lk) : 0xffffffffu;
+              const uint32_t k1 = (jb + 1 < N && jb + 1 != gi) ? ((cc1 << 16) | lk | 1u) : 0xffffffffu;
+              bk[r] = min(bk[r], min(k0, k1));
+            } else {
+              const float inf = __int_as_float(0x7f800000);
+              const float e0 = (jb < N && jb != gi) ? d0 : inf;
+              const float e1 = (jb + 1 < N && jb + 1 != gi) ? d1 : inf;
+              const float m = fminf(e0, e1);
+              const bool u = m < bv[r];
+              bj[r] = u ? (e0 <= e1 ? j0 : j1) : bj[r];
+              bv[r] = u ? m : bv[r];
+            }
           }
         }
       }
@@ -294,7 +319,15 @@ __global__ void __launch_bounds__(NT, 2) k_dist_tile(DistArgs a, Plan P) {
     unsigned long long mine = ~0ull;  // lane r: this warp's best key of row r
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      unsigned long long key = ((unsigned long long)__float_as_uint(bv[r]) << 32) | bj[r];
+      unsigned long long key;
+      if constexpr (CODES) {  // (code << 32 | column); decoded to the value below
+        const uint32_t lk = bk[r];
+        key = lk == 0xffffffffu ? ~0ull
+                                : (((unsigned long long)(lk >> 16) << 32) |
+                                   (((lk >> 1) & 0x7fffu) * (uint32_t)CH + (uint32_t)tid * CPT + (lk & 1u)));
+      } else {
+        key = ((unsigned long long)__float_as_uint(bv[r]) << 32) | bj[r];
+      }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) key = umin64(key, __shfl_xor_sync(0xffffffffu, key, o));
       mine = (lane == r) ? key : mine;
@@ -305,6 +338,8 @@ __global__ void __launch_bounds__(NT, 2) k_dist_tile(DistArgs a, Plan P) {
       unsigned long long best = ~0ull;
 #pragma unroll
       for (int w = 0; w < NW; ++w) best = umin64(best, red[w * R + tid]);
+      if (CODES && best != ~0ull)
+        best = ((unsigned long long)__float_as_uint(__ldg(a.vals + (best >> 32))) << 32) | (best & 0xffffffffull);
       a.nnkey[r0 + tid] = best;
     }
     __syncthreads();
