@@ -299,7 +299,9 @@ def run_ours(args, ws, rank, local):
     # (a5, k_merge_rows: every launch reads the live rows of the old matrix and
     # writes the new one); "roofline" is the one with the larger step share
     rows_here = -(-N // ws) if sharded else N  # rows of the distance matrix this rank writes
-    dist_bytes = 4.0 * rows_here * N + 4.0 * N * K   # fp32 rows written + ids read (algorithmic)
+    codes = bool(mean.get("value_codes", 0))
+    # fp32 rows (+ 16-bit value codes in code mode) written + ids read (algorithmic)
+    dist_bytes = (6.0 if codes else 4.0) * rows_here * N + 4.0 * N * K
     dist_gbs = dist_bytes / (mean["distance_ms"] * 1e-3) / 1e9
     traffic = load_traffic(args.config)
     roof_dist = {"kernel": "k_dist_tile (a2-a4, distance rows + fused row NN)", "bound": "hbm",
@@ -309,11 +311,13 @@ def run_ours(args, ws, rank, local):
                  "share_of_step": mean["distance_ms"] / ms}
     mb = mean["merge_bytes"] / max(mean["merge_launches"], 1)
     merge_gbs = mean["merge_bytes"] / (mean["merge_ms"] * 1e-3) / 1e9 if mean["merge_ms"] > 0 else 0.0
-    roof_merge = {"kernel": "k_merge_rows (a5, linkage compaction rounds)", "bound": "hbm",
+    mkern = "k_merge_gather" if codes else "k_merge_rows"
+    roof_merge = {"kernel": f"{mkern} (a5, linkage compaction rounds)", "bound": "hbm",
                   "achieved": merge_gbs, "peak": hbm, "unit": "GB/s", "frac": merge_gbs / hbm,
-                  "traffic": traffic.get("k_merge_rows") if traffic else None, "peak_source": peak_src,
+                  "traffic": traffic.get(mkern) if traffic else None, "peak_source": peak_src,
                   "algorithmic_bytes_per_launch": mb, "launches_per_step": mean["merge_launches"],
-                  "algorithmic_bytes_note": "4 B x (live old rows^2 + new rows^2) per launch, averaged",
+                  "algorithmic_bytes_note": ("2 B (16-bit value code)" if codes else "4 B (fp32)") +
+                  " x (live old rows^2 + new rows^2) per launch, averaged",
                   "share_of_step": mean["merge_ms"] / ms}
     if roof_merge["share_of_step"] >= roof_dist["share_of_step"]:
         roofline, roofline_other = roof_merge, roof_dist
@@ -325,7 +329,7 @@ def run_ours(args, ws, rank, local):
         "unit": "context-pairs/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong" if sharded else "weak", "vs_baseline": None,
-        "dtype": "u32+f32", "data": "synthetic",
+        "dtype": "u32+f32" + ("+u16codes" if codes else ""), "data": "synthetic",
         "config": {"workload": workload_desc(args.config, w) + ("; rank r uses seed+1000r" if replicas else ""),
                    "l2": "256 MB flush write between builds; per-build working set 80 GB >> 126 MB L2",
                    "parallelism": (f"one index, rows sharded over {ws} GPUs (peer-memory exchange)" if sharded

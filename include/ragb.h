@@ -106,6 +106,9 @@ typedef struct rb_stats {
   float merge_ms;         /* CUDA-event time of the linkage compaction launches    */
   int32_t merge_launches; /* number of compaction launches                         */
   double merge_bytes;     /* their algorithmic bytes (live rows read, rows written)*/
+  int32_t value_codes;    /* 1: the linkage ran on 16-bit value codes written by the
+                             distance kernel next to the fp32 rows (uniform K <= 32,
+                             complete linkage); 0: on the fp32 rows              */
 } rb_stats;
 
 typedef struct rb_index rb_index;

@@ -392,6 +392,7 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
   H.stats.merge_ms = lo.merge_ms;
   H.stats.merge_launches = lo.merge_launches;
   H.stats.merge_bytes = lo.merge_bytes;
+  H.stats.value_codes = code_mode ? 1 : 0;
   H.stats.kernel_launches = launches;
 
   // ---- a6-a7: tree, orders, schedule (host) --------------------------------

@@ -57,7 +57,8 @@ class Stats(ctypes.Structure):
                 ("total_ms", ctypes.c_float), ("linkage_rounds", ctypes.c_int32),
                 ("kernel_launches", ctypes.c_int32), ("n_virtual", ctypes.c_int64),
                 ("max_depth", ctypes.c_int64), ("merge_ms", ctypes.c_float),
-                ("merge_launches", ctypes.c_int32), ("merge_bytes", ctypes.c_double)]
+                ("merge_launches", ctypes.c_int32), ("merge_bytes", ctypes.c_double),
+                ("value_codes", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
