@@ -284,9 +284,9 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
       cudaEventElapsedTime(&b, tev[1], tev[2]);
       std::fprintf(stderr,
                    "[ragb linkage] round %d M=%d live=%d Mn=%d merges=%d %s prep=%.3fms merge=%.3fms | level n=%d "
-                   "starts=%d batches=%d picks=%d cands=%d kclk w0=%d pass=%d\n",
+                   "starts=%d batches=%d picks=%d cands=%d kclk w0=%d pass=%d collect=%d\n",
                    out->rounds, M, live, Mn, merges_round, inplace ? "inplace" : "compact", a, b, host_c[8],
-                   host_c[4], host_c[5], host_c[6], host_c[7], host_c[9], host_c[10]);
+                   host_c[4], host_c[5], host_c[6], host_c[7], host_c[9], host_c[10], host_c[11]);
     }
     if (!inplace) {
       p ^= 1;

@@ -340,9 +340,10 @@ constexpr int CT = 512;  // threads of k_level_cliques (128 registers for the pi
 __global__ void __launch_bounds__(CT, 1) k_level_cliques(PrepArgs a,
                                                          const uint32_t *__restrict__ adj) {
   extern __shared__ uint32_t bits[];  // [2][W]: alive, candidates
-  __shared__ int s_first[2][CT / 32];
   __shared__ int s_p[64];     // next candidates (list positions), ascending
   __shared__ int s_pick[32];  // picks of the batch (list positions)
+  __shared__ uint32_t s_m[32];  // candidate r: bit j set <=> p_j adjacent to p_r (j < r)
+  __shared__ int s_wsum[CT / 32];
   __shared__ int s_npick, s_last, s_nseq;
   __shared__ int s_sv[CT / 32], s_sf[CT / 32];
   const int n = a.level[0];
@@ -357,27 +358,42 @@ __global__ void __launch_bounds__(CT, 1) k_level_cliques(PrepArgs a,
     A[w] = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
   }
   __syncthreads();
-  int parity = 0;
-  // C[w] = f(w) for w >= w0; returns the first set bit position (or INT_MAX)
-  auto pass = [&](int w0, auto f) {
-    int first = 0x7fffffff;
-    for (int w = w0 + tid; w < W; w += CT) {
-      const uint32_t c = f(w);
-      C[w] = c;
-      first = (c != 0u && first == 0x7fffffff) ? w * 32 + __ffs(c) - 1 : first;
+  // C[w] = f(w) for w >= w0 (every such word), and the first <= 32 set bits
+  // of C from w0 on -> s_p (ascending); returns their total count (uniform)
+  auto pass_collect = [&](int w0, auto f) {
+    int got = 0;
+    for (int wb = w0; wb < W; wb += CT) {
+      const int w = wb + tid;
+      uint32_t x = w < W ? f(w) : 0u;
+      if (w < W) C[w] = x;
+      const int cnt = __popc(x);
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        incl += lane >= o ? y : 0;
+      }
+      if (lane == 31) s_wsum[wid] = incl;
+      __syncthreads();
+      int before = 0, tot = 0;
+#pragma unroll
+      for (int q = 0; q < CT / 32; ++q) {
+        const int v = s_wsum[q];
+        before += q < wid ? v : 0;
+        tot += v;
+      }
+      int slot = got + before + incl - cnt;
+      while (x != 0u && slot < 32) {
+        s_p[slot++] = w * 32 + __ffs(x) - 1;
+        x &= x - 1u;
+      }
+      got += tot;
+      __syncthreads();  // s_p complete; s_wsum reusable
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
-    if (lane == 0) s_first[parity][wid] = first;
-    __syncthreads();
-    int m = lane < CT / 32 ? s_first[parity][lane] : 0x7fffffff;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
-    parity ^= 1;
-    return m;
+    return got;
   };
   int nseq = 0;  // warp 0: picks recorded so far
-  long long st_starts = 0, st_batches = 0, st_picks = 0, st_cands = 0, st_w0 = 0, st_pass = 0;
+  long long st_starts = 0, st_batches = 0, st_picks = 0, st_cands = 0, st_w0 = 0, st_pass = 0, st_col = 0;
   if (n <= kWarpCliqueMaxN) {
     if (n <= 1024) {  // stage the adjacency (n x W <= 32K words) in shared memory
       for (int i = tid; i < n * W; i += CT) bits[i] = __ldg(adj + i);
@@ -392,62 +408,40 @@ __global__ void __launch_bounds__(CT, 1) k_level_cliques(PrepArgs a,
     const int w0 = ia >> 5;
     const uint32_t gt = (ia & 31) == 31 ? 0u : (0xffffffffu << ((ia & 31) + 1));
     const uint32_t *row = adj + (int64_t)ia * W;
+    long long c0 = clock64();
+    // C = adj(ia) & alive above ia, by the block (coalesced row loads), and
+    // its first candidates
+    int got = pass_collect(w0, [&](int w) {
+      const uint32_t c = __ldg(row + w) & A[w];
+      return w == w0 ? (c & gt) : c;
+    });
+    st_pass += clock64() - c0;
+    if (got == 0) continue;  // no h-neighbour left: stays a singleton at h (uniform)
     ++st_starts;
-    // the first batch reads adj(ia) & A above ia directly; later ones read C
-    bool first = true;
-    int cur = ia;
     while (true) {
-      long long c0 = clock64();
+      c0 = clock64();
       ++st_batches;
-      if (wid == 0) {
-        // -- collect the next <= 32 candidates; lane l covers 16 consecutive
-        //    words of each 512-word chunk (all loads in flight) --------------
-        int got = 0;
-        for (int wpos = cur >> 5; got < 32 && wpos < W; wpos += 512) {
-          const int wq = wpos + lane * 16;
-          uint32_t c[16];
-#pragma unroll
-          for (int u = 0; u < 16; ++u) {
-            const int w = wq + u;
-            uint32_t x = 0u;
-            if (w < W) x = first ? (__ldg(row + w) & A[w] & (w == w0 ? gt : 0xffffffffu)) : C[w];
-            c[u] = x;
-          }
-          int cnt = 0;
-#pragma unroll
-          for (int u = 0; u < 16; ++u) cnt += __popc(c[u]);
-          int incl = cnt;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, incl, o);
-            incl += lane >= o ? y : 0;
-          }
-          int slot = got + incl - cnt;
-#pragma unroll
-          for (int u = 0; u < 16; ++u) {
-            uint32_t x = c[u];
-            while (x != 0u && slot < 32) {
-              s_p[slot++] = (wq + u) * 32 + __ffs(x) - 1;
-              x &= x - 1u;
-            }
-          }
-          got += __shfl_sync(0xffffffffu, incl, 31);
+      const int k = min(got, 32);
+      // -- 2. mutual adjacency of the candidates: warp r (and r + 16) tests
+      //       row p_r against p_j, j < r (the words of one row: few sectors)
+      for (int r = wid; r < k; r += CT / 32) {
+        const int pr = s_p[r];
+        bool bit = false;
+        if (lane < r) {
+          const int pj = s_p[lane];
+          bit = (__ldg(adj + (int64_t)pr * W + (pj >> 5)) >> (pj & 31)) & 1u;
         }
-        __syncwarp();
-        const int k = min(got, 32);
+        const uint32_t m = __ballot_sync(0xffffffffu, bit);
+        if (lane == 0) s_m[r] = m;
+      }
+      __syncthreads();
+      // -- 3. the pick chain (warp 0): p_1, then the smallest remaining
+      //       candidate adjacent to every pick so far
+      if (wid == 0) {
         int npick = 0;
         if (k > 0) {
           const int pi = lane < k ? s_p[lane] : 0;
-          // -- m bit j (j < lane): p_j adjacent to p_lane ----------------------
-          const uint32_t *arow = adj + (int64_t)pi * W;
-          uint32_t wd[31];
-#pragma unroll
-          for (int j = 0; j < 31; ++j) wd[j] = (j < lane && lane < k) ? __ldg(arow + (s_p[j] >> 5)) : 0u;
-          uint32_t m = 0u;
-#pragma unroll
-          for (int j = 0; j < 31; ++j) m |= ((wd[j] >> (s_p[j] & 31)) & 1u) << j;
-          // -- the pick chain: p_1, then the smallest remaining candidate
-          //    adjacent to every pick so far (rem = lanes adjacent to all picks)
+          const uint32_t m = lane < k ? s_m[lane] : 0u;
           uint32_t ch = 1u;
           uint32_t rem = __ballot_sync(0xffffffffu, lane < k && (m & 1u));
           while (rem != 0u) {
@@ -481,16 +475,15 @@ __global__ void __launch_bounds__(CT, 1) k_level_cliques(PrepArgs a,
       const int npick = s_npick;
       const int wl = last >> 5;
       const uint32_t above = (last & 31) == 31 ? 0u : (0xffffffffu << ((last & 31) + 1));
-      const bool fst = first;
-      cur = pass(wl, [&](int w) {
-        uint32_t c = fst ? (__ldg(row + w) & A[w]) : C[w];
+      // fold the picks into C above the last candidate, collect the next ones
+      got = pass_collect(wl, [&](int w) {
+        uint32_t c = C[w];
         c &= w == wl ? above : 0xffffffffu;
         for (int t = 0; t < npick; ++t) c &= __ldg(adj + (int64_t)s_pick[t] * W + w);
         return c;
       });
       st_pass += clock64() - c0;
-      first = false;
-      if (cur == 0x7fffffff) break;
+      if (got == 0) break;
     }
     __syncthreads();
   }
@@ -557,6 +550,7 @@ __global__ void __launch_bounds__(CT, 1) k_level_cliques(PrepArgs a,
       a.cstat[4] = n;
       a.cstat[5] = (int)(st_w0 >> 10);
       a.cstat[6] = (int)(st_pass >> 10);
+      a.cstat[7] = (int)(st_col >> 10);
     }
   }
 }
