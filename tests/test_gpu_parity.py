@@ -271,6 +271,17 @@ def test_round_strategy(mode, case, codes, monkeypatch):
         check_full(w.ids, counts=False)
 
 
+@pytest.mark.parametrize("case", ["C2", "odd"])
+def test_code_window_compaction(case, monkeypatch):
+    """Code-mode compaction through the shared-memory window kernel
+    (RAGB_GATHER=0; the path for matrices too wide for the gather kernel)
+    gives the oracle's merge order, also for an odd N (scalar loads)."""
+    monkeypatch.setenv("RAGB_GATHER", "0")
+    monkeypatch.setenv("RAGB_CODES", "1")
+    ids = config("C2").ids if case == "C2" else generate(1029, 8, 3087, 1129).ids
+    check_full(ids, counts=False)
+
+
 def test_round_strategy_full_size(monkeypatch):
     """At C4 size (level cliques above 4096 vertices, block path) the merge
     order and the document order do not depend on the round strategy nor on
