@@ -560,10 +560,10 @@ rb_status build_index_dist(rb_dist *d, const uint32_t *ids_d, const uint8_t *len
       const float *Dloc = cur_is_rows ? d->rows[r] : reinterpret_cast<float *>(sc + (cur_is_A ? L.matA : L.matB));
       a.D = Dloc;
       a.ld = ld;
-      k_prep_mark<<<1, PT, 0, st>>>(a);
+      launch_prep_mark(a, sms, st, &launches);
       k_level_adj_dist<<<sms * 4, 256, 0, st>>>(a, Dloc, ld, (int64_t)r * S, std::min<int64_t>((int64_t)(r + 1) * S, M),
                                                 at<uint32_t>(sc, L.adj));
-      launches += 2;
+      launches += 1;
     }
     if ((e = barrier()) != cudaSuccess) break;
     for (int l = 0; l < nloc; ++l) {
@@ -576,8 +576,8 @@ rb_status build_index_dist(rb_dist *d, const uint32_t *ids_d, const uint8_t *len
       if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_level_cliques, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       k_level_cliques<<<1, CT, smem, st>>>(pa[l], at<uint32_t>(sc, L.adj));
-      k_prep_compact<<<1, PT, 0, st>>>(pa[l]);
-      launches += 3;
+      launch_prep_compact(pa[l], sms, st, &launches);
+      launches += 2;
     }
     if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) break;
     int host_c[2];

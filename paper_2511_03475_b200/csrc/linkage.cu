@@ -194,7 +194,7 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
     pa.sz = sz[p];
     pa.rep_n = rep[p ^ 1];
     pa.sz_n = sz[p ^ 1];
-    k_prep_mark<<<1, PT, 0, st>>>(pa);
+    launch_prep_mark(pa, sms, st, launches);
     uint32_t *adj = reinterpret_cast<uint32_t *>(next);  // free until the merge writes it
     if (codes)
       k_level_adj<uint16_t><<<sms * 4, 256, 0, st>>>(pa, adj);
@@ -207,8 +207,8 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
         cudaFuncSetAttribute(k_level_cliques, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       k_level_cliques<<<1, CT, smem, st>>>(pa, adj);
     }
-    k_prep_compact<<<1, PT, 0, st>>>(pa);
-    *launches += 4;
+    launch_prep_compact(pa, sms, st, launches);
+    *launches += 2;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (trace) cudaEventRecord(tev[1], st);
     int host_c[12] = {0};

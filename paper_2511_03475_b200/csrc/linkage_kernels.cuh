@@ -118,42 +118,61 @@ __device__ __forceinline__ int block_scan1024(int v, BlockScratch &S, int *total
   return before + x - v;
 }
 
-// Order-preserving compaction: out[...] = value(i) for i in [0, n) with pred(i).
-template <typename Pred, typename Val>
-__device__ int block_compact(int n, Pred pred, Val value, int *out, BlockScratch &S) {
+// Exclusive scan of get(i), i in [0, n), by the 1024-thread block: put(i,
+// prefix) for every i; returns the total.  A thread owns SE consecutive
+// elements per pass (SE x fewer block scans than one element per thread).
+constexpr int SE = 8;
+template <typename Get, typename Put>
+__device__ int block_scan_all(int n, Get get, Put put, BlockScratch &S) {
   int base = 0;
-  for (int c0 = 0; c0 < n; c0 += PT) {
-    const int i = c0 + (int)threadIdx.x;
-    const bool p = i < n && pred(i);
+  for (int c0 = 0; c0 < n; c0 += PT * SE) {
+    const int i0 = c0 + (int)threadIdx.x * SE;
+    int v[SE], sum = 0;
+#pragma unroll
+    for (int e = 0; e < SE; ++e) {
+      v[e] = i0 + e < n ? get(i0 + e) : 0;
+      sum += v[e];
+    }
     int tot;
-    const int pre = block_scan1024(p ? 1 : 0, S, &tot);
-    if (p) out[base + pre] = value(i);
+    int pre = base + block_scan1024(sum, S, &tot);
+#pragma unroll
+    for (int e = 0; e < SE; ++e) {
+      if (i0 + e < n) put(i0 + e, pre);
+      pre += v[e];
+    }
     base += tot;
   }
   __syncthreads();
   return base;
 }
 
-// Round step 1 (one CTA): h = min row key; RNN pairs above h (emitted); the
-// vertices whose row min equals h become the level list (ascending).
-__global__ void __launch_bounds__(PT, 1) k_prep_mark(PrepArgs a) {
-  __shared__ BlockScratch S;
-  const int tid = threadIdx.x;
-  const int M = a.M;
+// Order-preserving compaction: out[...] = value(i) for i in [0, n) with pred(i).
+template <typename Pred, typename Val>
+__device__ int block_compact(int n, Pred pred, Val value, int *out, BlockScratch &S) {
+  return block_scan_all(
+      n, [&](int i) { return pred(i) ? 1 : 0; },
+      [&](int i, int pre) {
+        if (pred(i)) out[pre] = value(i);
+      },
+      S);
+}
 
-  // -- 1. current minimum height h ------------------------------------------
+// Round step 1: h = min row key (grid, atomicMin on level[1], preset to
+// ~0); RNN pairs above h (grid, emitted); the vertices whose row min equals h
+// become the level list (one CTA, ascending).  Only the scans run in one CTA;
+// the per-row work with dependent loads and atomics is spread over the grid.
+__global__ void k_prep_min(PrepArgs a) {
   unsigned hl = 0xffffffffu;
-  for (int x = tid; x < M; x += PT) hl = min(hl, (unsigned)(a.key[x] >> 32));
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < a.M; x += gridDim.x * blockDim.x)
+    hl = min(hl, (unsigned)(a.key[x] >> 32));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) hl = min(hl, __shfl_xor_sync(0xffffffffu, hl, o));
-  if (tid == 0) S.h = 0xffffffffu;
-  __syncthreads();
-  if ((tid & 31) == 0) atomicMin(&S.h, hl);
-  __syncthreads();
-  const unsigned h = S.h;
+  if ((threadIdx.x & 31) == 0 && hl != 0xffffffffu) atomicMin(reinterpret_cast<unsigned *>(a.level + 1), hl);
+}
 
-  // -- 2. RNN pairs above h; vertices at h become clique candidates ------------
-  for (int x = tid; x < M; x += PT) {
+__global__ void k_prep_rnn(PrepArgs a) {
+  const unsigned h = (unsigned)a.level[1];
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < a.M; x += gridDim.x * blockDim.x) {
     const u64 kx = a.key[x];
     const unsigned hx = (unsigned)(kx >> 32);
     const int y = (int)(kx & 0xffffffffu);
@@ -173,16 +192,14 @@ __global__ void __launch_bounds__(PT, 1) k_prep_mark(PrepArgs a) {
     }
     a.leader[x] = lead;
   }
-  __syncthreads();
+}
 
-  // level list: vertices at h, ascending
+__global__ void __launch_bounds__(PT, 1) k_prep_list(PrepArgs a) {
+  __shared__ BlockScratch S;
   const uint8_t *alive = a.alive;
   const int nlist = block_compact(
-      M, [&](int i) { return alive[i] != 0; }, [&](int i) { return i; }, a.list, S);
-  if (tid == 0) {
-    a.level[0] = nlist;
-    a.level[1] = (int)h;
-  }
+      a.M, [&](int i) { return alive[i] != 0; }, [&](int i) { return i; }, a.list, S);
+  if (threadIdx.x == 0) a.level[0] = nlist;
 }
 
 // Round step 2 (grid): adjacency bits of the level graph, adj[i][w] bit j <=>
@@ -555,29 +572,24 @@ __global__ void __launch_bounds__(CT, 1) k_level_cliques(PrepArgs a,
   }
 }
 
-// Round step 4 (one CTA): order-preserving compaction map and group CSR.
-__global__ void __launch_bounds__(PT, 1) k_prep_compact(PrepArgs a) {
+// Round step 4: order-preserving compaction map and group CSR.  Scans in one
+// CTA (newidx, goff), the per-row passes over the grid.
+__global__ void __launch_bounds__(PT, 1) k_compact_scan1(PrepArgs a) {
   __shared__ BlockScratch S;
-  const int tid = threadIdx.x;
   const int M = a.M;
-  // -- 4. compaction map: new index of every survivor (order preserving) ------
-  int base = 0;
-  for (int c0 = 0; c0 < M; c0 += PT) {
-    const int x = c0 + tid;
-    const int f = (x < M && a.leader[x] == x) ? 1 : 0;
-    int tot;
-    const int pre = block_scan1024(f, S, &tot);
-    if (x < M) a.newidx[x] = base + pre;  // valid for survivors
-    base += tot;
-  }
-  const int Mn = base;
-  for (int g = tid; g < Mn; g += PT) {
+  // new index of every survivor (order preserving)
+  const int Mn = block_scan_all(
+      M, [&](int x) { return a.leader[x] == x ? 1 : 0; }, [&](int x, int pre) { a.newidx[x] = pre; }, S);
+  for (int g = threadIdx.x; g < Mn; g += PT) {
     a.cnt[g] = 0;
     a.cursor[g] = 0;
     a.sz_n[g] = 0;
   }
-  __syncthreads();
-  for (int x = tid; x < M; x += PT) {
+  if (threadIdx.x == 0) *a.Mn = Mn;
+}
+
+__global__ void k_compact_groups(PrepArgs a) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < a.M; x += gridDim.x * blockDim.x) {
     const int l = a.leader[x];
     if (l < 0) continue;  // dead row
     const int g = a.newidx[l];
@@ -585,39 +597,40 @@ __global__ void __launch_bounds__(PT, 1) k_prep_compact(PrepArgs a) {
     atomicAdd(&a.sz_n[g], a.sz[x]);
     if (l == x) a.rep_n[g] = a.rep[x];
   }
-  __syncthreads();
-  base = 0;
-  for (int c0 = 0; c0 < Mn; c0 += PT) {
-    const int g = c0 + tid;
-    const int v = g < Mn ? a.cnt[g] : 0;
-    int tot;
-    const int pre = block_scan1024(v, S, &tot);
-    if (g < Mn) a.goff[g] = base + pre;
-    base += tot;
-  }
-  if (tid == 0) {
-    a.goff[Mn] = base;  // live rows (dead rows of in-place rounds are in no group)
-    *a.Mn = Mn;
-  }
-  __syncthreads();
-  for (int x = tid; x < M; x += PT) {
+}
+
+__global__ void __launch_bounds__(PT, 1) k_compact_scan2(PrepArgs a) {
+  __shared__ BlockScratch S;
+  const int Mn = *a.Mn;
+  const int live = block_scan_all(
+      Mn, [&](int g) { return a.cnt[g]; }, [&](int g, int pre) { a.goff[g] = pre; }, S);
+  if (threadIdx.x == 0) a.goff[Mn] = live;  // live rows (dead rows of in-place rounds are in no group)
+}
+
+__global__ void k_compact_members(PrepArgs a) {
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < a.M; x += gridDim.x * blockDim.x) {
     const int l = a.leader[x];
     if (l < 0) continue;
     const int g = a.newidx[l];
     a.gmem[a.goff[g] + atomicAdd(&a.cursor[g], 1)] = x;
   }
-  __syncthreads();
-  // old column -> new column | writer class << 29 (k_merge_rows): 0 the
-  // group's leader (smallest member), 1 the other member of a 2-member group,
-  // 2 a non-leader of a larger group; new column -> its leader (first_old)
-  for (int x = tid; x < M; x += PT) {
+}
+
+// old column -> new column | writer class << 29 (k_merge_rows): 0 the
+// group's leader (smallest member), 1 the other member of a 2-member group,
+// 2 a non-leader of a larger group; new column -> its leader (first_old,
+// in cursor, free after the member scatter); pmap for k_merge_gather
+__global__ void k_compact_maps(PrepArgs a) {
+  const int M = a.M, Mn = *a.Mn;
+  const int i0 = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int x = i0; x < M; x += gridDim.x * blockDim.x) {
     const int l = a.leader[x];
     const int g = l < 0 ? -1 : a.newidx[l];
-    const int cls = (l == x || l < 0) ? 0 : (a.goff[g + 1] - a.goff[g] == 2 ? 1 : 2);
+    const int gs = g < 0 ? 0 : a.goff[g + 1] - a.goff[g];
+    const int cls = (l == x || l < 0) ? 0 : (gs == 2 ? 1 : 2);
     a.colsrc[x] = g < 0 ? -1 : (g | (cls << 29));
-    if (l == x) a.cursor[g] = x;  // cursor is free after the scatter: first_old
+    if (l == x) a.cursor[g] = x;
     if (a.pmap && g >= 0) {
-      const int gs = a.goff[g + 1] - a.goff[g];
       if (l == x) {
         a.pmap[g].x = x;
         if (gs == 1) a.pmap[g].y = -1;
@@ -626,8 +639,27 @@ __global__ void __launch_bounds__(PT, 1) k_prep_compact(PrepArgs a) {
       }
     }
   }
-  if (a.pmap && tid < 8) a.pmap[Mn + tid] = make_int2(0, -1);  // padding of the last vector
-  if (tid < 8) a.colsrc[M + tid] = -1;  // padding for 16-byte colmap loads (8 codes per vector)
+  if (i0 < 8) {
+    if (a.pmap) a.pmap[Mn + i0] = make_int2(0, -1);  // padding of the last vector
+    a.colsrc[M + i0] = -1;  // padding for 16-byte colmap loads (8 codes per vector)
+  }
+}
+
+// Launch sequences of the round preparation (single GPU and sharded build).
+inline void launch_prep_mark(const PrepArgs &pa, int sms, cudaStream_t st, int *launches) {
+  cudaMemsetAsync(pa.level + 1, 0xff, 4, st);
+  k_prep_min<<<sms, 256, 0, st>>>(pa);
+  k_prep_rnn<<<sms * 2, 256, 0, st>>>(pa);
+  k_prep_list<<<1, PT, 0, st>>>(pa);
+  *launches += 3;
+}
+inline void launch_prep_compact(const PrepArgs &pa, int sms, cudaStream_t st, int *launches) {
+  k_compact_scan1<<<1, PT, 0, st>>>(pa);
+  k_compact_groups<<<sms * 2, 256, 0, st>>>(pa);
+  k_compact_scan2<<<1, PT, 0, st>>>(pa);
+  k_compact_members<<<sms * 2, 256, 0, st>>>(pa);
+  k_compact_maps<<<sms * 2, 256, 0, st>>>(pa);
+  *launches += 5;
 }
 
 // Fused merge + compaction + row min (complete linkage, X7):
