@@ -89,6 +89,12 @@ class Clocks:
             pynvml.nvmlInit()
             h = pynvml.nvmlDeviceGetHandleByIndex(index)
             bits = {nm: getattr(pynvml, attr) for nm, attr in self.NAMES.items()}
+            # first queries outside the timed region: on a fresh box the first
+            # NVML calls of a process can stall CUDA launches for tens of ms
+            for _ in range(2):
+                pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+                pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
 
             def loop():
                 while not self.stop_ev.is_set():
@@ -239,19 +245,27 @@ def run_ours(args, ws, rank, local):
         return idx
 
     for _ in range(args.warmup):
+        flush.zero_()   # warm too: the first launch of torch's fill kernel loads its module (ms to s)
         step()
     torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
-    clk = Clocks(local)
+    clk = Clocks(local, period_s=float(os.environ.get("RAGB_CLOCKS_PERIOD", "0.05")))
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     stats = []
+    dbg = os.environ.get("RAGB_BENCH_DEBUG")
     e0.record(stream)
     for _ in range(args.steps):
+        ta = time.perf_counter()
         flush.zero_()   # L2 flush between builds (256 MB > 126 MB L2)
+        tb = time.perf_counter()
         idx = step()
+        tc = time.perf_counter()
         stats.append(idx.stats())
+        if dbg:
+            print(f"step: flush {1e3 * (tb - ta):.2f} step {1e3 * (tc - tb):.2f} lib {stats[-1]['total_ms']:.2f}",
+                  file=sys.stderr, flush=True)
     e1.record(stream)
     torch.cuda.synchronize()
     clocks = clk.stop()

@@ -992,25 +992,33 @@ __global__ void __launch_bounds__(NTH) k_merge_gather(const uint16_t *__restrict
     }
     __syncthreads();
     // ---- phase 2: gather the new row ----------------------------------------
-    // a thread takes 2 consecutive new columns per step (lanes read adjacent
-    // slots: no bank conflicts; 4-byte stores coalesce per warp), UP steps
-    // per iteration for memory-level parallelism on the pmap loads
-    int bval = 0x7fffffff, bidx = 0x7fffffff;
+    // The old columns of group c (the row's own members) map only to the
+    // diagonal: they are set to 0xffff (above every code) so that the gather
+    // loop needs no diagonal test — the diagonal entry (0) is stored after it.
+    if (tid < re - rb) reinterpret_cast<uint16_t *>(srow4)[gmem[rb + tid]] = 0xffffu;
+    for (int r = rb + NTH + tid; r < re; r += NTH) reinterpret_cast<uint16_t *>(srow4)[gmem[r]] = 0xffffu;
+    __syncthreads();
+    // A thread takes 2 consecutive new columns per step (lanes read adjacent
+    // slots: no bank conflicts; 4-byte stores coalesce per warp).  Its row
+    // minimum is one packed word (value << 16 | step << 1 | column bit):
+    // columns are visited in increasing order per thread, so the strict
+    // minimum keeps the smallest column among equal values (X8).
+    unsigned kmin = 0xffffffffu;
     unsigned *__restrict__ out2 = reinterpret_cast<unsigned *>(Dn + (int64_t)c * ldn);
     const int4 *__restrict__ pm4 = reinterpret_cast<const int4 *>(pmap);
-    const int npair = (Mn + 1) >> 1;
-    constexpr int UP = NTH <= 512 ? 16 : 4;
-    for (int pb = tid; pb < npair; pb += NTH * UP) {
+    const int nfull = Mn >> 1;  // pairs of real columns; an odd last column is the tail below
+    constexpr int UP = 4;
+    unsigned step = 0;
+    for (int pb = tid; pb < nfull; pb += NTH * UP) {
       int4 pm[UP];
 #pragma unroll
       for (int u = 0; u < UP; ++u) {
         const int pi = pb + u * NTH;
-        pm[u] = pi < npair ? __ldg(pm4 + pi) : make_int4(0, -1, 0, -1);
+        pm[u] = pi < nfull ? __ldg(pm4 + pi) : make_int4(0, -1, 0, -1);
       }
 #pragma unroll
-      for (int u = 0; u < UP; ++u) {
+      for (int u = 0; u < UP; ++u, ++step) {
         const int pi = pb + u * NTH;
-        const int t0 = 2 * pi;
         const int xs[2] = {pm[u].x, pm[u].z}, ys[2] = {pm[u].y, pm[u].w};
         unsigned q[2];
 #pragma unroll
@@ -1018,19 +1026,34 @@ __global__ void __launch_bounds__(NTH) k_merge_gather(const uint16_t *__restrict
           unsigned v = srow[xs[k]];
           if (ys[k] >= 0) v = max(v, (unsigned)srow[ys[k]]);
           if (ys[k] == -2)  // larger group (a level clique): every member
-            for (int r = goff[t0 + k]; r < goff[t0 + k + 1]; ++r) v = max(v, (unsigned)srow[gmem[r]]);
-          const int t = t0 + k;
-          q[k] = t == c ? 0u : v;  // diagonal (excluded from the minimum)
-          const int m = (t == c || t >= Mn) ? 0x7fffffff : (int)v;
-          if (m < bval) {  // strict: the earliest column wins among equal values (X8)
-            bval = m;
-            bidx = t;
-          }
+            for (int r = goff[2 * pi + k]; r < goff[2 * pi + k + 1]; ++r) v = max(v, (unsigned)srow[gmem[r]]);
+          q[k] = v;
+          if (pi < nfull) kmin = min(kmin, (v << 16) | (step << 1) | (unsigned)k);
         }
-        if (pi < npair) __stcs(out2 + pi, q[0] | (q[1] << 16));
+        if (pi < nfull) __stcs(out2 + pi, q[0] | (q[1] << 16));
       }
     }
-    u64 best = bval == 0x7fffffff ? ~0ull : (((u64)(unsigned)bval << 32) | (unsigned)bidx);
+    u64 best = ~0ull;
+    if (kmin != 0xffffffffu && (kmin >> 16) != 0xffffu) {  // decode (step, bit) -> column
+      const unsigned st_ = (kmin >> 1) & 0x7fffu;
+      const int t = 2 * (tid + (int)(st_ / UP) * NTH * UP + (int)(st_ % UP) * NTH) + (int)(kmin & 1u);
+      best = ((u64)(kmin >> 16) << 32) | (unsigned)t;
+    }
+    if ((Mn & 1) && tid == 0) {  // odd last column
+      const int t = Mn - 1;
+      const int2 e = pmap[t];
+      unsigned v = srow[e.x];
+      if (e.y >= 0) v = max(v, (unsigned)srow[e.y]);
+      if (e.y == -2)
+        for (int r = goff[t]; r < goff[t + 1]; ++r) v = max(v, (unsigned)srow[gmem[r]]);
+      out2[t >> 1] = v;  // with the padding column (0)
+      if (v != 0xffffu) {
+        const u64 kt = ((u64)v << 32) | (unsigned)t;
+        best = kt < best ? kt : best;
+      }
+    }
+    __syncthreads();  // every store of the row is done: the diagonal entry last
+    if (tid == 0) Dn[(int64_t)c * ldn + c] = 0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const u64 y = __shfl_xor_sync(0xffffffffu, best, o);
