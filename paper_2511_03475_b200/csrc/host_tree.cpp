@@ -286,17 +286,22 @@ rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg) {
   for (int64_t i = 0; i < N; ++i) ++H.kids_off[H.lparent[i] + 1];
   for (int64_t k = 0; k <= V; ++k) H.kids_off[k + 1] += H.kids_off[k];
   H.kids.assign(V + N, 0);
-  {
-    std::vector<int64_t> fill(H.kids_off.begin(), H.kids_off.end() - 1);
-    for (int64_t k = 1; k <= V; ++k) H.kids[fill[vpar[k - 1]]++] = (int32_t)k;
-    for (int64_t i = 0; i < N; ++i) H.kids[fill[H.lparent[i]]++] = (int32_t)(V + 1 + i);
-  }
   std::vector<int32_t> child_idx(1 + V + N, 0);
-#pragma omp parallel for num_threads(nth) schedule(dynamic, 256)
-  for (int64_t k = 0; k <= V; ++k) {
-    int32_t *b = H.kids.data() + H.kids_off[k], *e = H.kids.data() + H.kids_off[k + 1];
-    std::sort(b, e, [&](int32_t x, int32_t y) { return rep_of[x] < rep_of[y]; });
-    for (int32_t *p = b; p < e; ++p) child_idx[*p] = (int32_t)(p - b);
+  {
+    // nodes in ascending rep order (counting sort over reps in [0, N); a node
+    // and its leftmost descendants share a rep but are never siblings), then
+    // scattered to their parents: every child list comes out sorted (X12)
+    std::vector<int32_t> rcnt(N + 1, 0), byrep(V + N);
+    for (int64_t x = 1; x <= V + N; ++x) ++rcnt[rep_of[x] + 1];
+    for (int64_t r = 0; r < N; ++r) rcnt[r + 1] += rcnt[r];
+    for (int64_t x = 1; x <= V + N; ++x) byrep[rcnt[rep_of[x]]++] = (int32_t)x;
+    std::vector<int64_t> fill(H.kids_off.begin(), H.kids_off.end() - 1);
+    for (int64_t z = 0; z < V + N; ++z) {
+      const int32_t x = byrep[z];
+      const int32_t par = x <= V ? vpar[x - 1] : H.lparent[x - V - 1];
+      child_idx[x] = (int32_t)(fill[par] - H.kids_off[par]);
+      H.kids[fill[par]++] = x;
+    }
   }
   lap("children");
 
