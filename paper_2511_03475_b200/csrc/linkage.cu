@@ -56,7 +56,9 @@ cudaError_t launch_merge(const T *cur, int64_t ld, int M, int Mn, const PrepArgs
     const uint16_t *c16 = reinterpret_cast<const uint16_t *>(cur);
     uint16_t *n16 = reinterpret_cast<uint16_t *>(next);
     const bool vec = ld % 8 == 0 && (reinterpret_cast<uintptr_t>(cur) & 15) == 0;
-    const size_t smem = (size_t)((M + 7) / 8) * 16;
+    const size_t row_bytes = (size_t)((M + 7) / 8) * 16;
+    const int db = vec && 2 * row_bytes <= 227 * 1024 ? 1 : 0;  // double-buffered rows
+    const size_t smem = row_bytes * (1 + db);
     const bool wide = M > 16 * 1024;
     auto kern = wide ? (vec ? k_merge_gather<true, 1024> : k_merge_gather<false, 1024>)
                      : (vec ? k_merge_gather<true, 256> : k_merge_gather<false, 256>);
@@ -65,7 +67,7 @@ cudaError_t launch_merge(const T *cur, int64_t ld, int M, int Mn, const PrepArgs
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nth, smem);
     const int grid = std::min<int>(Mn, sms * std::max(per_sm, 1));
-    kern<<<grid, nth, smem, st>>>(c16, ld, M, pa.Mn, pa.goff, pa.gmem, pa.pmap, n16, keyn);
+    kern<<<grid, nth, smem, st>>>(c16, ld, M, pa.Mn, pa.goff, pa.gmem, pa.pmap, n16, keyn, db);
     return cudaGetLastError();
   }
   const bool vec = ld % VW == 0 && (reinterpret_cast<uintptr_t>(cur) & 15) == 0;

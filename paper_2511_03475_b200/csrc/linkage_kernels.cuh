@@ -935,35 +935,47 @@ template <bool VEC, int NTH>
 __global__ void __launch_bounds__(NTH) k_merge_gather(const uint16_t *__restrict__ D, int64_t ld, int M,
                                                       const int *__restrict__ Mn_p, const int *__restrict__ goff,
                                                       const int *__restrict__ gmem, const int2 *__restrict__ pmap,
-                                                      uint16_t *__restrict__ Dn, u64 *__restrict__ keyn) {
+                                                      uint16_t *__restrict__ Dn, u64 *__restrict__ keyn, int db) {
   typedef Elem<uint16_t> E;
-  extern __shared__ __align__(16) uint4 srow4[];  // [ceil(M / 8)]
-  const uint16_t *srow = reinterpret_cast<const uint16_t *>(srow4);
+  // db: two row buffers (when 2 x 2M bytes fit): the next row's bulk copy is
+  // in flight while this row is folded and gathered
+  extern __shared__ __align__(16) uint4 smem4[];  // [1 + db][ceil(M / 8)]
   __shared__ u64 wmin[NTH / 32];
   const int Mn = *Mn_p;
   const int64_t ldn = mat_ld<uint16_t>(Mn);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int MV = (M + 7) >> 3;
-  __shared__ __align__(8) unsigned long long bar;
-  unsigned parity = 0u;
-  if (VEC && tid == 0) mbar_init(&bar, 1);
+  __shared__ __align__(8) unsigned long long bar[2];
+  unsigned parity[2] = {0u, 0u};
+  if (VEC && tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+  }
   __syncthreads();
-  for (int c = blockIdx.x; c < Mn; c += gridDim.x) {
+  // one thread: bulk copies (TMA engine) of row `row`'s first member into slot
+  auto issue = [&](int row, int slot) {
+    fence_proxy_async_smem();  // earlier generic accesses of the buffer come first
+    const unsigned bytes = (unsigned)MV * 16u;
+    mbar_expect_tx(&bar[slot], bytes);
+    const unsigned char *src = reinterpret_cast<const unsigned char *>(D + (int64_t)gmem[goff[row]] * ld);
+    unsigned char *dst = reinterpret_cast<unsigned char *>(smem4 + (size_t)slot * MV);
+    for (unsigned o = 0; o < bytes; o += 32768u) bulk_g2s(dst + o, src + o, min(32768u, bytes - o), &bar[slot]);
+  };
+  if (VEC && db && tid == 0 && (int)blockIdx.x < Mn) issue(blockIdx.x, 0);
+  int it = 0;
+  for (int c = blockIdx.x; c < Mn; c += gridDim.x, ++it) {
     const int rb = goff[c], re = goff[c + 1];
+    const int slot = db ? (it & 1) : 0;
+    uint4 *srow4 = smem4 + (size_t)slot * MV;
+    const uint16_t *srow = reinterpret_cast<const uint16_t *>(srow4);
     // ---- phase 1: old row(s) -> shared memory -------------------------------
     if (VEC) {
       // the first member's row by bulk copies (all of it in flight at once),
       // then the other members folded in with 16-byte loads
-      if (tid == 0) {
-        fence_proxy_async_smem();  // the previous row's generic reads of srow come first
-        const unsigned bytes = (unsigned)MV * 16u;
-        mbar_expect_tx(&bar, bytes);
-        const unsigned char *src = reinterpret_cast<const unsigned char *>(D + (int64_t)gmem[rb] * ld);
-        unsigned char *dst = reinterpret_cast<unsigned char *>(srow4);
-        for (unsigned o = 0; o < bytes; o += 32768u) bulk_g2s(dst + o, src + o, min(32768u, bytes - o), &bar);
-      }
-      mbar_wait(&bar, parity);
-      parity ^= 1u;
+      if (!db && tid == 0) issue(c, 0);
+      mbar_wait(&bar[slot], parity[slot]);
+      parity[slot] ^= 1u;
+      if (db && tid == 0 && c + (int)gridDim.x < Mn) issue(c + gridDim.x, slot ^ 1);
       if (re - rb > 1) {
         constexpr int UV = 8;
         for (int qb = tid; qb < MV; qb += NTH * UV) {
