@@ -90,14 +90,15 @@ cudaError_t launch_merge(const T *cur, int64_t ld, int M, int Mn, const PrepArgs
 
 // In-place round for element type T (see k_inplace_*).
 template <typename T>
-cudaError_t launch_inplace(T *cur, int64_t ld, int M, const PrepArgs &pa, int sms, uint32_t *amask, int *mlist,
-                           int *nmulti, int *sz, unsigned long long *key, cudaStream_t st) {
+cudaError_t launch_inplace(T *cur, int64_t ld, int M, int max_groups, const PrepArgs &pa, int sms, uint32_t *amask,
+                           int *mlist, int *nmulti, int *sz, unsigned long long *key, cudaStream_t st) {
   constexpr int VW = Elem<T>::VW;
   k_inplace_prep<<<sms * 2, 256, 0, st>>>(pa, M, amask, mlist, nmulti, sz, key);
   const size_t smem = (size_t)((M + VW - 1) / VW) * 16;
   cudaFuncSetAttribute(k_inplace_rows<512, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_inplace_rows<512, T><<<sms * 2, 512, smem, st>>>(pa, cur, ld, M, amask, mlist, nmulti, key);
-  k_inplace_cols<T><<<sms * 8, 256, 0, st>>>(pa, cur, ld, M, amask, mlist, nmulti);
+  k_inplace_cols<T><<<dim3((unsigned)std::max(max_groups, 1), (unsigned)((M + kColsRows - 1) / kColsRows)), 256, 0,
+                      st>>>(pa, cur, ld, M, amask, mlist, nmulti);
   k_inplace_check<T><<<(M + 255) / 256, 256, 0, st>>>(pa, cur, ld, M, key, pa.cnt, nmulti + 1);  // cnt: free after the compaction map
   k_inplace_rescan<256, T><<<sms * 4, 256, 0, st>>>(cur, ld, M, amask, pa.cnt, nmulti + 1, key);
   return cudaGetLastError();
@@ -250,10 +251,11 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
         mask_ok = true;
       }
       if ((e = cudaMemsetAsync(nmulti, 0, 8, st)) != cudaSuccess) return e;  // nmulti, nres
-      e = codes ? launch_inplace<uint16_t>(static_cast<uint16_t *>(cur), ld, M, pa, sms, amask, mlist, nmulti,
-                                           sz[p], key[p], st)
-                : launch_inplace<float>(static_cast<float *>(cur), ld, M, pa, sms, amask, mlist, nmulti, sz[p],
-                                        key[p], st);
+      // merged groups <= merges of the round (the grid of the column kernel)
+      e = codes ? launch_inplace<uint16_t>(static_cast<uint16_t *>(cur), ld, M, merges_round, pa, sms, amask, mlist,
+                                           nmulti, sz[p], key[p], st)
+                : launch_inplace<float>(static_cast<float *>(cur), ld, M, merges_round, pa, sms, amask, mlist, nmulti,
+                                        sz[p], key[p], st);
       *launches += 5;
       if (e != cudaSuccess) return e;
     } else if (Mn > 1) {

@@ -1188,33 +1188,33 @@ __global__ void __launch_bounds__(NTH, 2) k_inplace_rows(PrepArgs a, T *__restri
 }
 
 // S2: columns from rows (symmetry): D[r][L] = D[L][r] for every live row r.
-// Work items = (merged group, 1024-row chunk); each thread moves 4 rows
-// (coalesced loads, scattered stores).  Few, long-lived CTAs: with one
-// short CTA per item the block scheduler, not the stores, set the pace.
+// CTA (x = merged group, y = chunk of CR rows): the group's survivor L is
+// looked up once, then every thread moves CR / 256 rows (independent
+// coalesced loads, scattered 2- or 4-byte stores), so the dependent-load
+// chain is paid once per CTA instead of once per handful of rows.
+constexpr int kColsRows = 4096;
 template <typename T>
 __global__ void __launch_bounds__(256) k_inplace_cols(PrepArgs a, T *__restrict__ D, int64_t ld, int M,
                                                       const uint32_t *__restrict__ amask,
                                                       const int *__restrict__ mlist,
                                                       const int *__restrict__ nmulti_p) {
-  const int nmulti = *nmulti_p;
-  const int nchunk = (M + 1023) >> 10;
-  const int64_t items = (int64_t)nmulti * nchunk;
-  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
-    const int gi = (int)(it / nchunk), ch = (int)(it - (int64_t)gi * nchunk);
-    const int L = a.cursor[mlist[gi]];
-    const T *src = D + (int64_t)L * ld;
-    T v[4];
-    int rr[4];
+  const int gi = blockIdx.x;
+  if (gi >= *nmulti_p) return;
+  const int L = a.cursor[mlist[gi]];
+  const T *src = D + (int64_t)L * ld;
+  constexpr int PER = kColsRows / 256;
+  const int rbase = blockIdx.y * kColsRows + (int)threadIdx.x;
+  T v[PER];
+  bool ok[PER];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int r = (ch << 10) + u * 256 + (int)threadIdx.x;
-      rr[u] = (r < M && ((amask[r >> 5] >> (r & 31)) & 1u)) ? r : -1;
-      v[u] = rr[u] >= 0 ? __ldg(src + r) : Elem<T>::make(0u);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (rr[u] >= 0) D[(int64_t)rr[u] * ld + L] = v[u];
+  for (int u = 0; u < PER; ++u) {
+    const int r = rbase + u * 256;
+    ok[u] = r < M && ((__ldg(amask + (r >> 5)) >> (r & 31)) & 1u);
+    v[u] = ok[u] ? __ldg(src + r) : Elem<T>::make(0u);
   }
+#pragma unroll
+  for (int u = 0; u < PER; ++u)
+    if (ok[u]) D[(int64_t)(rbase + u * 256) * ld + L] = v[u];
 }
 
 // S3a: one thread per live row r outside the merged groups whose nearest
