@@ -271,6 +271,17 @@ def test_round_strategy(mode, case, codes, monkeypatch):
         check_full(w.ids, counts=False)
 
 
+@pytest.mark.parametrize("K", [7, 22, 23, 30, 32])
+def test_code_mode_fast_path(K):
+    """Code mode through the tile kernel's fast finalize (no (s, D) output):
+    both Eq. 1 table layouts (K <= 22: packed byte offsets into a shared-memory
+    table; 23 <= K <= 32: global table) give the oracle's rows, row NN, merge
+    order and document order, with a ragged last tile and column chunk."""
+    w = generate(2000 + 3 * K, K, 60 * K, 500 + K)
+    idx = check_full(w.ids, counts=False)
+    assert idx.stats()["value_codes"] == 1
+
+
 @pytest.mark.parametrize("case", ["C2", "odd"])
 def test_code_window_compaction(case, monkeypatch):
     """Code-mode compaction through the shared-memory window kernel
