@@ -334,8 +334,17 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
     std::condition_variable cv;
     int64_t avail = 0;
     bool finished = false;
+    cudaError_t copy_err = cudaSuccess;
+    int cur_dev = 0;
+    cudaGetDevice(&cur_dev);
     std::thread worker([&] {
+      cudaSetDevice(cur_dev);  // a new thread starts on device 0
       ragb::host_begin(H, T);  // sorted leaf sets overlap the device work
+      // the round's merges come from the device on this thread's own
+      // non-blocking stream: the launching thread never waits for them
+      cudaStream_t cs = nullptr;
+      cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+      int64_t have = 0;
       for (;;) {
         int64_t upto;
         bool fin;
@@ -345,9 +354,27 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
           upto = avail;
           fin = finished;
         }
+        if (upto > have) {
+          const size_t n = (size_t)(upto - have);
+          cudaMemcpyAsync(H.za.data() + have, reinterpret_cast<int32_t *>(sc + L.za) + have, n * 4,
+                          cudaMemcpyDeviceToHost, cs);
+          cudaMemcpyAsync(H.zb.data() + have, reinterpret_cast<int32_t *>(sc + L.zb) + have, n * 4,
+                          cudaMemcpyDeviceToHost, cs);
+          cudaMemcpyAsync(H.zh.data() + have, reinterpret_cast<float *>(sc + L.zh) + have, n * 4,
+                          cudaMemcpyDeviceToHost, cs);
+          cudaMemcpyAsync(H.zs.data() + have, reinterpret_cast<int32_t *>(sc + L.zs) + have, n * 4,
+                          cudaMemcpyDeviceToHost, cs);
+          const cudaError_t ce = cudaStreamSynchronize(cs);
+          if (ce != cudaSuccess) {
+            copy_err = ce;
+            break;
+          }
+          have = upto;
+        }
         ragb::host_replay(H, T, upto);
         if (!T.ok || (fin && T.done >= upto)) break;
       }
+      if (cs) cudaStreamDestroy(cs);
     });
     const cudaError_t le = ragb::run_linkage(
         rows_dev, N, da.nnkey, scratch_dev, L, keep_rows, code_mode ? &cm : nullptr, st, H.za.data(), H.zb.data(),
@@ -365,6 +392,7 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
     cv.notify_one();
     worker.join();
     if (le != cudaSuccess) return cleanup(cuda_fail(le, "linkage"));
+    if (copy_err != cudaSuccess) return cleanup(cuda_fail(copy_err, "D2H merges"));
   }
   RB_CUDA(cudaEventRecord(ev[3], st), "event");
   RB_CUDA(cudaStreamSynchronize(st), "sync");

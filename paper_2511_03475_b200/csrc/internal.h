@@ -99,10 +99,12 @@ struct LinkageOut {
 };
 
 // a5: complete linkage on the full rows (rows ld = N) starting from the fused
-// row-NN keys.  Merges are written to the host arrays za/zb/zh/zs ([N-1]) in a
-// dependency-respecting order, round by round; on_round(upto) is called after
-// each round with the number of merges available so far (used to pipeline the
-// host tree build with the device rounds; may be empty).
+// row-NN keys.  Merges are produced in a dependency-respecting order, round by
+// round, in the device arrays of the scratch layout (za/zb/zh/zs).  Without
+// on_round they are copied to the host arrays za/zb/zh/zs ([N-1]) after each
+// round; with on_round, on_round(upto) is called after each round with the
+// number of final device merges and the caller copies them (used to pipeline
+// the host tree build with the device rounds on a worker thread).
 // NEXT-3: intersection-representative linkage (ilinkage.cu); rows [N][ld] are
 // updated in place, ctxT [K][Npad] holds the contexts (updated in place),
 // merges come back to the host arrays in greedy (merge) order.

@@ -224,16 +224,21 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
       const int z0 = zdone, z1 = host_c[0];
       if (z1 > (int)N - 1 || z1 < z0) return cudaErrorUnknown;
       if (z1 > z0) {
-        const size_t n = (size_t)(z1 - z0);
-        cudaMemcpyAsync(za + z0, pa.za + z0, n * 4, cudaMemcpyDeviceToHost, st);
-        cudaMemcpyAsync(zb + z0, pa.zb + z0, n * 4, cudaMemcpyDeviceToHost, st);
-        cudaMemcpyAsync(zh + z0, pa.zh + z0, n * 4, cudaMemcpyDeviceToHost, st);
-        if ((e = cudaMemcpyAsync(zs + z0, pa.zs + z0, n * 4, cudaMemcpyDeviceToHost, st)) !=
-            cudaSuccess)
-          return e;
-        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+        if (on_round) {
+          // the caller's worker thread fetches merges [.., z1) itself (they
+          // are final: device rows only ever get appended) while this thread
+          // goes on launching the next kernels
+          on_round(z1);
+        } else {
+          const size_t n = (size_t)(z1 - z0);
+          cudaMemcpyAsync(za + z0, pa.za + z0, n * 4, cudaMemcpyDeviceToHost, st);
+          cudaMemcpyAsync(zb + z0, pa.zb + z0, n * 4, cudaMemcpyDeviceToHost, st);
+          cudaMemcpyAsync(zh + z0, pa.zh + z0, n * 4, cudaMemcpyDeviceToHost, st);
+          if ((e = cudaMemcpyAsync(zs + z0, pa.zs + z0, n * 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+            return e;
+          if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+        }
         zdone = z1;
-        if (on_round) on_round(zdone);
       }
     }
     const int Mn = host_c[1];
