@@ -461,6 +461,7 @@ cudaError_t launch_code_table(const float *lut, int32_t K, int stride, int64_t e
 cudaError_t launch_distance(const DistArgs &a, cudaStream_t st, int *launches) {
   ++*launches;
   if (tile_path_ok(a.K, a.lens == nullptr) && a.lut) return launch_distance_tile(a, st);
+  if (wide_path_ok(a.K, a.lens == nullptr) && !std::getenv("RAGB_NO_WIDE")) return launch_distance_wide(a, st);
   // General path (variable lengths, K > 32): a table of d(s, D) when every
   // context has K docs (smem copy if small, else read through L1/L2), else the
   // exact division.

@@ -85,6 +85,9 @@ bool tile_path_ok(int32_t K, bool uniform);
 int tile_lut_shift(int32_t K);
 int64_t tile_lut_entries(int32_t K);
 cudaError_t launch_distance_tile(const DistArgs &a, cudaStream_t st);
+// Long lists (distance_wide.cu): uniform contexts with 32 < K <= 128.
+bool wide_path_ok(int32_t K, bool uniform);
+cudaError_t launch_distance_wide(const DistArgs &a, cudaStream_t st);
 
 cudaError_t launch_validate(const uint32_t *ids, const uint8_t *lens, int64_t N, int32_t K,
                             int64_t Npad, uint32_t *idsT, uint32_t *err, cudaStream_t st,

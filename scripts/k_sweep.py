@@ -40,7 +40,7 @@ for K in (5, 10, 15, 20, 30, 50, 75, 100):
     gbs = bytes_skip / (best_d * 1e-3) / 1e9
     rec = {"K": K, "N": N, "distance_ms": round(best_d, 3), "pairs_per_s": N * (N - 1) / 2 / (best_d * 1e-3),
            "GBps": round(gbs, 1), "frac_hbm": round(gbs / peak, 3),
-           "kernel": "k_dist_tile" if K <= 32 else "k_dist_rows_nn", "build_ms": round(best_b, 2),
+           "kernel": "k_dist_tile" if K <= 32 else ("k_dist_wide" if K <= 128 else "k_dist_rows_nn"), "build_ms": round(best_b, 2),
            "linkage_on_codes": bool(codes)}
     out.append(rec)
     print(json.dumps(rec), flush=True)
