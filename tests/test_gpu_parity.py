@@ -282,6 +282,17 @@ def test_code_mode_fast_path(K):
     assert idx.stats()["value_codes"] == 1
 
 
+@pytest.mark.parametrize("K", [33, 48, 64, 65, 100, 128])
+def test_wide_lists(K):
+    """Uniform 32 < K <= 128 (the long-list distance kernel, both candidate-
+    mask widths, with and without the (s, D) output): rows, row NN, merge
+    order and document order equal the oracle's; odd N and a ragged last
+    tile and chunk."""
+    w = generate(1201 + K, K, 40 * K, 900 + K)
+    check_full(w.ids, counts=False)
+    check_full(w.ids[: 333], counts=True)
+
+
 @pytest.mark.parametrize("case", ["C2", "odd"])
 def test_code_window_compaction(case, monkeypatch):
     """Code-mode compaction through the shared-memory window kernel
