@@ -38,8 +38,9 @@ constexpr int FWORDS = 2048;   // filter words (65536 bits)
 struct Plan {
   int T, logT, shift, lutEntries, qcap;
   size_t off_acc, off_key, off_mask, off_base, off_slot, off_plist, off_filter, off_qdoc, off_qmeta,
-      off_red, off_wsum, off_lut, total;
+      off_red, off_wsum, off_lut, off_lutc, total;
 };
+constexpr int QW = 512;  // candidate-queue window per warp (entries), drained as often as needed
 
 // CODES: also write codes[i][j] = lutc[packed (s, D)] (16-bit order-preserving
 // value codes, the complete-linkage input; the code table has the float
@@ -63,6 +64,7 @@ __global__ void __launch_bounds__(NT, 2) k_dist_tile(DistArgs a, Plan P) {
   unsigned long long *red = reinterpret_cast<unsigned long long *>(smem + P.off_red);  // [NW][R]
   int *wsum = reinterpret_cast<int *>(smem + P.off_wsum);
   float *slut = reinterpret_cast<float *>(smem + P.off_lut);
+  uint16_t *slutc = reinterpret_cast<uint16_t *>(smem + P.off_lutc);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int K = a.K, T = P.T, logT = P.logT;
@@ -70,7 +72,10 @@ __global__ void __launch_bounds__(NT, 2) k_dist_tile(DistArgs a, Plan P) {
   const int64_t ntiles = (a.nrows + R - 1) / R;
   const float *lut = LUT_SMEM ? slut : a.lut;
   if (LUT_SMEM)
-    for (int i = tid; i < P.lutEntries; i += NT) slut[i] = a.lut[i];
+    for (int i = tid; i < P.lutEntries; i += NT) {
+      slut[i] = a.lut[i];
+      if (CODES) slutc[i] = (uint16_t)a.lutc[i];
+    }
   const bool even_n = (N & 1) == 0;
 
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -162,20 +167,27 @@ __global__ void __launch_bounds__(NT, 2) k_dist_tile(DistArgs a, Plan P) {
           const int y = __shfl_up_sync(0xffffffffu, x, o);
           if (lane >= o) x += y;
         }
-        const int qn = __shfl_sync(0xffffffffu, x, 31);
-        int pos = x - n;
+        const int qn_all = __shfl_sync(0xffffffffu, x, 31);
+        const int pos0 = x - n;
         const uint32_t col0 = (uint32_t)(tid * CPT);
-        while (cm0) {
-          const int k = __ffs(cm0) - 1;
-          cm0 &= cm0 - 1u;
-          myq[pos++] = (uint16_t)((k << 9) | col0);
+        // windows of qcap queue entries (almost always one)
+        for (int lo = 0; lo < qn_all; lo += P.qcap) {
+        int pos = pos0;
+        uint32_t m0 = cm0, m1 = cm1;
+        while (m0) {
+          const int k = __ffs(m0) - 1;
+          m0 &= m0 - 1u;
+          if ((unsigned)(pos - lo) < (unsigned)P.qcap) myq[pos - lo] = (uint16_t)((k << 9) | col0);
+          ++pos;
         }
-        while (cm1) {
-          const int k = __ffs(cm1) - 1;
-          cm1 &= cm1 - 1u;
-          myq[pos++] = (uint16_t)((k << 9) | (col0 + 1u));
+        while (m1) {
+          const int k = __ffs(m1) - 1;
+          m1 &= m1 - 1u;
+          if ((unsigned)(pos - lo) < (unsigned)P.qcap) myq[pos - lo] = (uint16_t)((k << 9) | (col0 + 1u));
+          ++pos;
         }
         __syncwarp();
+        const int qn = min(P.qcap, qn_all - lo);
         // ---- drain: all 32 lanes process the warp's candidates; the doc
         // reloads of DB consecutive rounds are issued together (latency)
         constexpr int DB = 4;
@@ -211,6 +223,7 @@ __global__ void __launch_bounds__(NT, 2) k_dist_tile(DistArgs a, Plan P) {
           }
         }
         __syncwarp();
+        }
       }
 
       // ---- finalize: d = table[packed (s, D)], stores, row min in registers
@@ -242,7 +255,11 @@ __global__ void __launch_bounds__(NT, 2) k_dist_tile(DistArgs a, Plan P) {
           o += step;
           if (CODES) {
             uint32_t c0, c1;
-            if (SHIFT == 8) {
+            if (SHIFT == 8 && LUT_SMEM) {  // byte offset 4 x index -> 16-bit entry at 2 x index
+              const char *sc = reinterpret_cast<const char *>(slutc);
+              c0 = *reinterpret_cast<const uint16_t *>(sc + ((w & 0xffffu) >> 1));
+              c1 = *reinterpret_cast<const uint16_t *>(sc + (w >> 17));
+            } else if (SHIFT == 8) {
               c0 = __ldg(reinterpret_cast<const uint32_t *>(lutcb + (w & 0xffffu)));
               c1 = __ldg(reinterpret_cast<const uint32_t *>(lutcb + (w >> 16)));
             } else {
@@ -372,12 +389,13 @@ Plan plan(int K, int shift, int lutSmemEntries) {
   P.off_slot = take((size_t)R * K * 2, 16);
   P.off_plist = take((size_t)R * K * 2, 16);
   P.off_filter = take((size_t)FWORDS * 4, 16);
-  P.qcap = 32 * CPT * K;  // every (lane, column, k) can be a candidate
+  P.qcap = std::min(32 * CPT * K, QW);  // every (lane, column, k) can be a candidate: windows
   P.off_qdoc = take((size_t)NW * P.qcap * 2, 16);
   P.off_qmeta = P.off_qdoc;
   P.off_red = take((size_t)NW * R * 8, 16);
   P.off_wsum = take(32 * 4, 16);
   P.off_lut = take((size_t)lutSmemEntries * 4, 16);
+  P.off_lutc = take((size_t)lutSmemEntries * 2, 16);  // 16-bit value codes of the table (code mode)
   P.total = (o + 15) / 16 * 16;
   return P;
 }
