@@ -47,7 +47,7 @@ size_t take(size_t &o, size_t bytes) {
 }
 
 struct DistLayout {
-  size_t err, counters, table, idsT, lut, key0, key1, rep0, rep1, sz0, sz1, leader, aux0, aux1, aux2, aux3,
+  size_t err, counters, table, idsT, lut, lutc, vals, key0, key1, rep0, rep1, sz0, sz1, leader, aux0, aux1, aux2, aux3,
       aux4, alive, za, zb, zh, zs, adj, matA, matB, total;
   int64_t S0;  // rows per rank of the distance matrix
   static DistLayout make(int64_t N, int32_t K, int world) {
@@ -63,6 +63,8 @@ struct DistLayout {
       int64_t entries;
       distance_lut_layout(K, true, &stride, &entries);
       L.lut = take(o, (size_t)std::max<int64_t>(entries, 1) * 4);
+      L.lutc = take(o, (size_t)std::max<int64_t>(entries, 1) * 4);
+      L.vals = take(o, (size_t)std::max<int64_t>(entries, 1) * 4);
     }
     L.key0 = take(o, (size_t)(N + world) * 8);
     L.key1 = take(o, (size_t)(N + world) * 8);
@@ -112,11 +114,12 @@ __global__ void k_gather_slices(T *__restrict__ dst, const T *const *__restrict_
 
 // Level adjacency rows of the level vertices whose row this rank owns (other
 // rows written as zero): adj[i][w] bit j <=> D[list[i]][list[32w + j]] == h.
-__global__ void k_level_adj_dist(PrepArgs a, const float *__restrict__ Dloc, int64_t ld, int64_t r0,
+template <typename T>
+__global__ void k_level_adj_dist(PrepArgs a, const T *__restrict__ Dloc, int64_t ld, int64_t r0,
                                  int64_t r1, uint32_t *__restrict__ adj) {
   const int n = a.level[0];
   if (n < 2) return;
-  const float hf = __uint_as_float((unsigned)a.level[1]);
+  const unsigned hb = (unsigned)a.level[1];
   const int W = (n + 31) >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -127,7 +130,7 @@ __global__ void k_level_adj_dist(PrepArgs a, const float *__restrict__ Dloc, int
     const int j = w * 32 + lane;
     const int64_t r = a.list[i];
     bool bit = false;
-    if (r >= r0 && r < r1 && j < n && j != i) bit = __ldg(Dloc + (r - r0) * ld + a.list[j]) == hf;
+    if (r >= r0 && r < r1 && j < n && j != i) bit = Elem<T>::bits(__ldg(Dloc + (r - r0) * ld + a.list[j])) == hb;
     const unsigned word = __ballot_sync(0xffffffffu, bit);
     if (lane == 0) adj[q] = word;
   }
@@ -429,6 +432,11 @@ rb_status build_index_dist(rb_dist *d, const uint32_t *ids_d, const uint8_t *len
   cudaEventRecord(ev[0], st);
 
   // ---- a2-a4: this rank's distance rows + their NN keys --------------------
+  // code mode (as in the single-GPU build): each rank also
+  // writes the 16-bit value codes of its rows (into its B buffer, the first
+  // round's input) and the rounds run on codes
+  const char *cenv = std::getenv("RAGB_CODES");
+  const bool codes = N > 1 && tile_path_ok(K, lens_d == nullptr) && !(cenv && std::atoi(cenv) == 0);
   for (int l = 0; l < nloc; ++l) {
     const int r = g0 + l;
     unsigned char *sc = d->scratch[r];
@@ -452,6 +460,14 @@ rb_status build_index_dist(rb_dist *d, const uint32_t *ids_d, const uint8_t *len
       DC(launch_eq1_lut(at<float>(sc, L.lut), K, stride, entries, p->alpha_num, p->alpha_den, st, &launches),
          "eq1 table");
       da.lut = at<float>(sc, L.lut);
+      if (codes) {
+        DC(launch_code_table(da.lut, K, stride, entries, at<uint32_t>(sc, L.lutc), at<float>(sc, L.vals),
+                             at<int>(sc, L.err + 16), st, &launches),
+           "code table");
+        da.lutc = at<uint32_t>(sc, L.lutc);
+        da.vals = at<float>(sc, L.vals);
+        da.codes = at<uint16_t>(sc, L.matB);
+      }
     }
     if (da.nrows > 0) DC(launch_distance(da, st, &launches), "distance kernel");
   }
@@ -509,6 +525,11 @@ rb_status build_index_dist(rb_dist *d, const uint32_t *ids_d, const uint8_t *len
     a.Mn = counters + 1;
     a.level = counters + 2;
     a.cstat = nullptr;
+    a.vals = codes ? at<float>(sc, L.vals) : nullptr;
+    if (codes) {  // row keys (f32 bits) -> code keys, after the host copy of the NN above
+      k_keys_to_codes<<<sms, 256, 0, st>>>(at<unsigned long long>(sc, L.key0), N, a.vals, at<int>(sc, L.err + 16));
+      ++launches;
+    }
     DC(cudaMemsetAsync(counters, 0, 64, st), "memset");
     k_init_state<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(at<int>(sc, L.rep0), at<int>(sc, L.sz0), N);
     ++launches;
@@ -543,7 +564,9 @@ rb_status build_index_dist(rb_dist *d, const uint32_t *ids_d, const uint8_t *len
   };
   int M = (int)N, rounds = 0, zdone = 0, par = 0;
   int64_t S = L.S0, ld = N;
-  bool cur_is_rows = true, cur_is_A = false;  // current matrix: the distance shards, then A / B
+  // current matrix: the fp32 distance shards (rows), then A / B alternately;
+  // in code mode the first matrix is the code shard in B (then A / B)
+  bool cur_is_rows = !codes, cur_is_A = false;
   rb_status rs = RB_OK;
   while (M > 1) {
     const size_t koff = par ? L.key1 : L.key0, knoff = par ? L.key0 : L.key1;
@@ -557,12 +580,18 @@ rb_status build_index_dist(rb_dist *d, const uint32_t *ids_d, const uint8_t *len
       a.sz = at<int>(sc, par ? L.sz1 : L.sz0);
       a.rep_n = at<int>(sc, par ? L.rep0 : L.rep1);
       a.sz_n = at<int>(sc, par ? L.sz0 : L.sz1);
-      const float *Dloc = cur_is_rows ? d->rows[r] : reinterpret_cast<float *>(sc + (cur_is_A ? L.matA : L.matB));
+      const void *Dloc = cur_is_rows ? static_cast<const void *>(d->rows[r])
+                                     : static_cast<const void *>(sc + (cur_is_A ? L.matA : L.matB));
       a.D = Dloc;
       a.ld = ld;
       launch_prep_mark(a, sms, st, &launches);
-      k_level_adj_dist<<<sms * 4, 256, 0, st>>>(a, Dloc, ld, (int64_t)r * S, std::min<int64_t>((int64_t)(r + 1) * S, M),
-                                                at<uint32_t>(sc, L.adj));
+      const int64_t ra = (int64_t)r * S, rz = std::min<int64_t>((int64_t)(r + 1) * S, M);
+      if (codes)
+        k_level_adj_dist<uint16_t><<<sms * 4, 256, 0, st>>>(a, static_cast<const uint16_t *>(Dloc), ld, ra, rz,
+                                                            at<uint32_t>(sc, L.adj));
+      else
+        k_level_adj_dist<float><<<sms * 4, 256, 0, st>>>(a, static_cast<const float *>(Dloc), ld, ra, rz,
+                                                         at<uint32_t>(sc, L.adj));
       launches += 1;
     }
     if ((e = barrier()) != cudaSuccess) break;
@@ -614,30 +643,45 @@ rb_status build_index_dist(rb_dist *d, const uint32_t *ids_d, const uint8_t *len
     }
     if (Mn > 1) {
       const int64_t Sn = (Mn + world - 1) / world;
-      const int64_t ldn = ((int64_t)Mn + 3) & ~3ll;
-      const bool vec = (ld & 3) == 0;
+      const int64_t ldn = codes ? mat_ld<uint16_t>(Mn) : mat_ld<float>(Mn);
+      const int VW = codes ? Elem<uint16_t>::VW : Elem<float>::VW;
+      const bool vec = ld % VW == 0;
       const bool wide = Mn > 20 * 1024;
-      const int maxW = wide ? 56 * 1024 : 20 * 1024;  // window of 32-bit slots (fp32 matrices)
-      const int W = std::min<int>((Mn + 3) & ~3, maxW);
-      const size_t smem = (size_t)W * 4;
+      const int es = codes ? 2 : 4;  // window slot bytes (Win<T>)
+      const int maxW = wide ? 224 * 1024 / es : 20 * 1024;
+      const int W = std::min<int>((Mn + VW - 1) / VW * VW, maxW);
+      const size_t smem = (size_t)W * es;
       const int nth = wide ? 1024 : 256;
       typedef PeerRows<float> PR;
-      auto kern = wide ? (vec ? k_merge_rows<true, 1024, float, PR> : k_merge_rows<false, 1024, float, PR>)
-                       : (vec ? k_merge_rows<true, 256, float, PR> : k_merge_rows<false, 256, float, PR>);
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      typedef PeerRows<uint16_t> PR16;
+      auto kf = wide ? (vec ? k_merge_rows<true, 1024, float, PR> : k_merge_rows<false, 1024, float, PR>)
+                     : (vec ? k_merge_rows<true, 256, float, PR> : k_merge_rows<false, 256, float, PR>);
+      auto kc = wide ? (vec ? k_merge_rows<true, 1024, uint16_t, PR16> : k_merge_rows<false, 1024, uint16_t, PR16>)
+                     : (vec ? k_merge_rows<true, 256, uint16_t, PR16> : k_merge_rows<false, 256, uint16_t, PR16>);
       int per_sm = 1;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nth, smem);
+      if (codes) {
+        cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kc, nth, smem);
+      } else {
+        cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kf, nth, smem);
+      }
       for (int l = 0; l < nloc; ++l) {
         const int r = g0 + l;
         unsigned char *sc = d->scratch[r];
         const int tcur = cur_is_rows ? TROWS : (cur_is_A ? TA : TB);
         const int c0 = (int)std::min<int64_t>((int64_t)r * Sn, Mn), c1 = (int)std::min<int64_t>((int64_t)(r + 1) * Sn, Mn);
-        float *Dn = reinterpret_cast<float *>(sc + ((cur_is_rows || !cur_is_A) ? L.matA : L.matB));
+        unsigned char *Dn = sc + ((cur_is_rows || !cur_is_A) ? L.matA : L.matB);
         if (c1 > c0) {
           const int grid = std::min<int>(c1 - c0, sms * std::max(per_sm, 1));
-          kern<<<grid, nth, smem, st>>>(PR{reinterpret_cast<const float *const *>(table(r, tcur)), (int)S, ld}, M,
-                                        pa[l].Mn, pa[l].goff, pa[l].gmem, pa[l].colsrc, pa[l].cursor, W, c0, c1, Dn,
-                                        at<unsigned long long>(sc, knoff));
+          if (codes)
+            kc<<<grid, nth, smem, st>>>(PR16{reinterpret_cast<const uint16_t *const *>(table(r, tcur)), (int)S, ld},
+                                        M, pa[l].Mn, pa[l].goff, pa[l].gmem, pa[l].colsrc, pa[l].cursor, W, c0, c1,
+                                        reinterpret_cast<uint16_t *>(Dn), at<unsigned long long>(sc, knoff));
+          else
+            kf<<<grid, nth, smem, st>>>(PR{reinterpret_cast<const float *const *>(table(r, tcur)), (int)S, ld}, M,
+                                        pa[l].Mn, pa[l].goff, pa[l].gmem, pa[l].colsrc, pa[l].cursor, W, c0, c1,
+                                        reinterpret_cast<float *>(Dn), at<unsigned long long>(sc, knoff));
           ++launches;
         }
       }

@@ -415,6 +415,16 @@ def test_row_sharded_build_matches_single_gpu(world):
     _dist_vs_single(w.ids, None, world)
 
 
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_sharded_fp32_matrices(world, monkeypatch):
+    """The sharded rounds on fp32 matrices (RAGB_CODES=0; the code-mode rounds
+    are the default for uniform K <= 32) give the same index."""
+    monkeypatch.setenv("RAGB_CODES", "0")
+    _dist_vs_single(config("C2").ids, None, world)
+    w = generate(1500, 4, 200, 78)
+    _dist_vs_single(w.ids, None, world)
+
+
 def test_row_sharded_tiny_and_vs_oracle():
     w = generate(5, 4, 12, 3)
     _dist_vs_single(w.ids, None, 8)  # fewer rows than ranks
