@@ -349,7 +349,7 @@ rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg) {
   lap("virtual");
 
   // ---- leaves (parallel): ordered contexts (a7), prefix lengths, paths -----
-  H.ordered.assign(H.ids.begin(), H.ids.end());
+  H.ordered.resize((size_t)N * K);  // every entry written below (no fill)
   H.prefix_len.assign(N, 0);
   H.path_off.assign(N + 1, 0);
   for (int64_t i = 0; i < N; ++i) H.path_off[i + 1] = H.path_off[i] + depth[H.lparent[i]] + 1;
@@ -368,6 +368,7 @@ rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg) {
     const int L = len_of(i);
     for (int k = 0; k < L; ++k)
       if (!in_sorted(sp, np, row[k])) out[o++] = row[k];
+    for (int k = L; k < K; ++k) out[k] = row[k];  // padding slots of a shorter context
     H.prefix_len[i] = (uint8_t)(p1 - p0);
     int32_t *pp = H.path.data() + H.path_off[i];
     for (int64_t z = vpath_off[p]; z < vpath_off[p + 1]; ++z) *pp++ = vpath[z];
@@ -385,9 +386,13 @@ rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg) {
     int64_t ng = 0;
     std::vector<int64_t> key(N);
     const int64_t LMAX = max_depth + 1;
-    for (int64_t i = 0; i < N; ++i) {
+    for (int64_t i = 0; i < N; ++i) {  // group ranks by first appearance (sequential, cheap)
       const int32_t g = H.path[H.path_off[i]];
       if (grank[g] < 0) grank[g] = ng++;
+    }
+#pragma omp parallel for num_threads(nth) schedule(static)
+    for (int64_t i = 0; i < N; ++i) {
+      const int32_t g = H.path[H.path_off[i]];
       const int64_t len = H.path_off[i + 1] - H.path_off[i];
       key[i] = grank[g] * LMAX + (LMAX - len);  // length descending within a group
     }

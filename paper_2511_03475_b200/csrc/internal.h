@@ -8,6 +8,7 @@
 #include <functional>
 #include <memory>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "ragb.h"
@@ -125,6 +126,25 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
 // ----------------------------------------------------------------- host
 struct DynTree;  // online (mutable) form of the tree, online.cpp
 
+// std::allocator without value-initialisation on resize (large host outputs
+// that a parallel loop fills completely: no sequential zero-fill first).
+template <typename T>
+struct NoInitAlloc : std::allocator<T> {
+  template <typename U>
+  struct rebind {
+    using other = NoInitAlloc<U>;
+  };
+  NoInitAlloc() = default;
+  template <typename U>
+  NoInitAlloc(const NoInitAlloc<U> &) noexcept {}
+  template <typename U>
+  void construct(U *) noexcept {}
+  template <typename U, typename... A>
+  void construct(U *p, A &&...args) {
+    ::new ((void *)p) U(std::forward<A>(args)...);
+  }
+};
+
 struct HostIndex {
   int64_t N = 0;
   int32_t K = 0;
@@ -146,7 +166,7 @@ struct HostIndex {
   std::vector<int64_t> path_off;       // [N+1] leaf search paths
   std::vector<int32_t> path;
   // offline orders
-  std::vector<uint32_t> ordered;   // [N][K]
+  std::vector<uint32_t, NoInitAlloc<uint32_t>> ordered;   // [N][K]
   std::vector<uint8_t> prefix_len;  // [N]
   std::vector<int64_t> schedule;    // [N]
   rb_stats stats{};
