@@ -289,6 +289,7 @@ __device__ int cliques_warp(const PrepArgs &a, const uint32_t *adj, int n, int W
       const int total = __shfl_sync(0xffffffffu, incl, 31);
       if (total == 0) break;
       int slot = incl - cnt;
+      __syncwarp();  // every lane is done reading the previous batch's s_p (racecheck)
 #pragma unroll
       for (int u = 0; u < WPL; ++u) {
         uint32_t x = C[u];
