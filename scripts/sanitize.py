@@ -20,7 +20,8 @@ for mode in ("1", "0"):
     os.environ["RAGB_INPLACE"] = mode
     run(w.ids[:1500])
 os.environ.pop("RAGB_INPLACE")
-run(generate(1200, 4, 150, 78).ids)                      # tie-heavy: level cliques
+run(generate(1200, 4, 150, 78).ids)                      # tie-heavy: level cliques (warp path)
+run(generate(10000, 3, 100000, 5).ids)                    # mostly disjoint: a level of > 4096 vertices (block path)
 v = generate(900, 12, 3000, 31, len_min=2); run(v.ids, v.lens)  # variable lengths (fp32 rounds)
 run(generate(700, 50, 2000, 9).ids)                       # long lists
 run(generate(600, 10, 2000, 8).ids, linkage=ragb.RB_LINK_INTERSECTION)
