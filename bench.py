@@ -195,7 +195,8 @@ def run_reference(args, ws, rank):
     from oracle import oracle_c as oc
     pairs = n_s * (n_s - 1) / 2
     value = pairs * args.steps / el
-    line = {"impl": "reference", "metric": f"context-pair distances/s (index build, {args.config})",
+    N, K = w.ids.shape
+    line = {"impl": "reference", "metric": f"context-pair distances/s (index build, N={N}, K={K})",
             "value": value, "unit": "context-pairs/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u32+f32", "data": "synthetic",
