@@ -238,14 +238,6 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
   if (err_h & ragb::kErrLen) return cleanup(fail(RB_EINVAL, "context length not in [1, K]"));
   if (err_h & ragb::kErrReserved) return cleanup(fail(RB_EINVAL, "reserved DocId 0xFFFFFFFF"));
   if (err_h & ragb::kErrDup) return cleanup(fail(RB_EDUPDOC, "duplicate DocId within a context"));
-  if (!ids_host) {
-    // transposed copy holds the same ids; fetch the row-major input directly
-    RB_CUDA(cudaMemcpyAsync(H.ids.data(), ids_d, (size_t)N * K * 4, cudaMemcpyDeviceToHost, st),
-            "D2H ids");
-    if (lens_d)
-      RB_CUDA(cudaMemcpyAsync(H.lens.data(), lens_d, (size_t)N, cudaMemcpyDeviceToHost, st),
-              "D2H lens");
-  }
   RB_CUDA(cudaEventRecord(ev[1], st), "event");
 
   // ---- a2-a4: distance rows + fused row NN --------------------------------
@@ -298,6 +290,18 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
   }
   RB_CUDA(ragb::launch_distance(da, st, &launches), "distance kernel");
   RB_CUDA(cudaEventRecord(ev[2], st), "event");
+  if (!ids_host) {
+    // the host copy of the contexts (tree stage) comes from the caller's
+    // buffer on a side stream while the distance kernel runs (the input is
+    // complete: the stream was synchronised after validation)
+    cudaStream_t side = nullptr;
+    RB_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking), "side stream");
+    e = cudaMemcpyAsync(H.ids.data(), ids_d, (size_t)N * K * 4, cudaMemcpyDeviceToHost, side);
+    if (e == cudaSuccess && lens_d) e = cudaMemcpyAsync(H.lens.data(), lens_d, (size_t)N, cudaMemcpyDeviceToHost, side);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(side);
+    cudaStreamDestroy(side);
+    if (e != cudaSuccess) return cleanup(cuda_fail(e, "D2H ids"));
+  }
   H.nn_idx.resize(nrows);
   H.nn_d.resize(nrows);
   std::vector<unsigned long long> keys(nrows);
