@@ -29,6 +29,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <functional>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "internal.h"
@@ -41,6 +44,32 @@ namespace {
 template <typename T>
 T *at(void *base, size_t off) {
   return reinterpret_cast<T *>(static_cast<unsigned char *>(base) + off);
+}
+
+// Launch configuration cache: the dynamic shared-memory opt-in is set once
+// per kernel (to the largest size requested so far) and occupancy is queried
+// once per (kernel, block, shared-memory) triple — both are host round trips
+// into the driver that otherwise sit between a round's counter read and its
+// launches (measured: ~0.3 ms per round at small N).
+template <typename F>
+int occupancy_cached(F kern, int nth, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void *, int, size_t>, int> occ;
+  static std::map<const void *, size_t> attr;
+  const void *key = reinterpret_cast<const void *>(kern);
+  std::lock_guard<std::mutex> lk(mu);
+  size_t &a = attr[key];
+  if (smem > a) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    a = smem;
+  }
+  auto it = occ.find({key, nth, smem});
+  if (it != occ.end()) return it->second;
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nth, smem);
+  per_sm = std::max(per_sm, 1);
+  occ[{key, nth, smem}] = per_sm;
+  return per_sm;
 }
 
 // Compaction launch for element type T (see k_merge_rows): wide rows get
@@ -63,10 +92,8 @@ cudaError_t launch_merge(const T *cur, int64_t ld, int M, int Mn, const PrepArgs
     auto kern = wide ? (vec ? k_merge_gather<true, 1024> : k_merge_gather<false, 1024>)
                      : (vec ? k_merge_gather<true, 256> : k_merge_gather<false, 256>);
     const int nth = wide ? 1024 : 256;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nth, smem);
-    const int grid = std::min<int>(Mn, sms * std::max(per_sm, 1));
+    const int per_sm = occupancy_cached(kern, nth, smem);
+    const int grid = std::min<int>(Mn, sms * per_sm);
     kern<<<grid, nth, smem, st>>>(c16, ld, M, pa.Mn, pa.goff, pa.gmem, pa.pmap, n16, keyn, db);
     return cudaGetLastError();
   }
@@ -79,10 +106,8 @@ cudaError_t launch_merge(const T *cur, int64_t ld, int M, int Mn, const PrepArgs
   const int nth = wide ? 1024 : 256;
   auto kern = wide ? (vec ? k_merge_rows<true, 1024, T, LocalRows<T>> : k_merge_rows<false, 1024, T, LocalRows<T>>)
                    : (vec ? k_merge_rows<true, 256, T, LocalRows<T>> : k_merge_rows<false, 256, T, LocalRows<T>>);
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nth, smem);
-  const int grid = std::min<int>(Mn, sms * std::max(per_sm, 1));
+  const int per_sm = occupancy_cached(kern, nth, smem);
+  const int grid = std::min<int>(Mn, sms * per_sm);
   kern<<<grid, nth, smem, st>>>(LocalRows<T>{cur, ld}, M, pa.Mn, pa.goff, pa.gmem, pa.colsrc, pa.cursor, W, 0, -1,
                                 next, keyn);
   return cudaGetLastError();
@@ -95,7 +120,7 @@ cudaError_t launch_inplace(T *cur, int64_t ld, int M, int max_groups, const Prep
   constexpr int VW = Elem<T>::VW;
   k_inplace_prep<<<sms * 2, 256, 0, st>>>(pa, M, amask, mlist, nmulti, sz, key);
   const size_t smem = (size_t)((M + VW - 1) / VW) * 16;
-  cudaFuncSetAttribute(k_inplace_rows<512, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  occupancy_cached(k_inplace_rows<512, T>, 512, smem);
   k_inplace_rows<512, T><<<sms * 2, 512, smem, st>>>(pa, cur, ld, M, amask, mlist, nmulti, key);
   k_inplace_cols<T><<<dim3((unsigned)std::max(max_groups, 1), (unsigned)((M + kColsRows - 1) / kColsRows)), 256, 0,
                       st>>>(pa, cur, ld, M, amask, mlist, nmulti);
@@ -207,7 +232,7 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
       const size_t m1 = std::min<size_t>((size_t)M, 1024);
       const size_t smem = std::max(2 * (size_t)((M + 31) / 32), m1 * ((m1 + 31) / 32)) * 4;
       if (smem > 48 * 1024)
-        cudaFuncSetAttribute(k_level_cliques, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        occupancy_cached(k_level_cliques, CT, smem);
       k_level_cliques<<<1, CT, smem, st>>>(pa, adj);
     }
     launch_prep_compact(pa, sms, st, launches);
@@ -265,8 +290,8 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
       if (e != cudaSuccess) return e;
     } else if (Mn > 1) {
       cudaEvent_t me[2];
-      cudaEventCreate(&me[0]);
-      cudaEventCreate(&me[1]);
+      cudaEventCreateWithFlags(&me[0], cudaEventDefault);
+      cudaEventCreateWithFlags(&me[1], cudaEventDefault);
       cudaEventRecord(me[0], st);
       e = codes ? launch_merge<uint16_t>(static_cast<const uint16_t *>(cur), ld, M, Mn, pa, sms,
                                          static_cast<uint16_t *>(next), key[p ^ 1], st)
