@@ -729,6 +729,7 @@ rb_status build_index_dist(rb_dist *d, const uint32_t *ids_d, const uint8_t *len
   H.stats.linkage_ms = ms;
   H.stats.linkage_rounds = rounds;
   H.stats.kernel_launches = launches;
+  H.stats.value_codes = codes ? 1 : 0;
   const auto th = std::chrono::steady_clock::now();
   rs = host_finish(H, T, msg);
   if (rs != RB_OK) return rs;
