@@ -126,9 +126,12 @@ RB_API rb_status rb_params_init(rb_params *p);
 
 /* Caller-owned buffer sizes for rb_build_index(N, K, p):
  *   rows_bytes    — float rows_dev[nrows][N] (nrows from p; 4*nrows*N bytes);
- *   scratch_bytes — device scratch (validation staging, linkage ping-pong
- *                   matrix of at most (N-1)^2 floats, or two of them with
- *                   RB_KEEP_ROWS, plus O(N) state).
+ *   scratch_bytes — device scratch (validation staging, the Eq. 1 table and
+ *                   its value-code table, the linkage matrices: either two
+ *                   16-bit code matrices of about N^2 entries each (uniform
+ *                   K <= 32, complete linkage) or one fp32 ping-pong matrix
+ *                   of at most (N-1)^2 floats — two with RB_KEEP_ROWS —, plus
+ *                   O(N) state).  The same size covers both forms.
  * Errors: RB_EINVAL on null outputs, N < 1, K not in [1,255]. */
 RB_API rb_status rb_workspace_size(int64_t N, int32_t K, const rb_params *p, size_t *rows_bytes,
                                    size_t *scratch_bytes);
@@ -147,7 +150,9 @@ RB_API rb_status rb_workspace_size(int64_t N, int32_t K, const rb_params *p, siz
  *            order (most relevant first).  Slots past lens[i] are ignored.
  * lens_dev : uint8 [N] device, or NULL (all contexts have K docs).
  * rows_dev : float [nrows][N] device, caller-owned (rows p->row0 ..).
- *            Overwritten by the linkage unless RB_KEEP_ROWS.
+ *            Overwritten by the linkage unless RB_KEEP_ROWS (the fp32-matrix
+ *            linkage uses it as a ping-pong buffer; the code-matrix linkage,
+ *            reported by rb_stats.value_codes, leaves it intact).
  * scratch_dev / scratch_bytes : device scratch of rb_workspace_size() bytes.
  * s_dev, D_dev : with RB_EMIT_COUNTS, uint8/uint16 [nrows][N] device outputs
  *            (else ignored, may be NULL).
