@@ -33,11 +33,6 @@ namespace ragb {
 
 namespace {
 
-struct MergeKey {
-  float h;
-  int32_t a, b, size;
-};
-
 bool key_less(const MergeKey &x, const MergeKey &y) {
   if (x.h != y.h) return x.h < y.h;
   if (x.a != y.a) return x.a < y.a;
@@ -73,6 +68,9 @@ void host_begin(HostIndex &H, TreeBuild &T) {
   const int32_t K = H.K;
   const bool uniform = H.lens.empty();
   const int nth = host_threads();
+  T.zk.clear();
+  T.runs.clear();
+  if (H.sort_merges) T.zk.reserve((size_t)std::max<int64_t>(N - 1, 0));
   // sorted leaf sets (parallel)
   T.lset.resize((size_t)N * K);
 #pragma omp parallel for num_threads(nth) schedule(static)
@@ -108,6 +106,7 @@ void host_replay(HostIndex &H, TreeBuild &T, int64_t upto) {
   const int64_t N = H.N;
   const int32_t K = H.K;
   const bool uniform = H.lens.empty();
+  const int64_t t_from = T.done;
   for (int64_t t = T.done; t < upto && T.ok; ++t) {
     const int32_t a = H.za[t], b = H.zb[t];
     if (a < 0 || b >= N || a >= b || T.cur[a] < 0 || T.cur[b] < 0 ||
@@ -154,6 +153,15 @@ void host_replay(HostIndex &H, TreeBuild &T, int64_t upto) {
     T.cur[b] = -1;
     T.csize[a] += T.csize[b];
     T.done = t + 1;
+  }
+  // the exported order (X9) is built here too, batch by batch: each replayed
+  // batch is sorted while the device runs the next rounds, and host_finish
+  // only merges the sorted runs
+  if (T.ok && H.sort_merges && T.done > t_from) {
+    if (T.runs.empty()) T.runs.push_back(0);
+    for (int64_t t = t_from; t < T.done; ++t) T.zk.push_back({H.zh[t], H.za[t], H.zb[t], H.zs[t]});
+    std::sort(T.zk.begin() + t_from, T.zk.end(), key_less);
+    T.runs.push_back((int64_t)T.zk.size());
   }
 }
 
@@ -214,11 +222,27 @@ rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg) {
 
   // ---- exported merge order: ascending key (X9), sorted on a side thread
   //      while the tree is built (the tree reads the replay order) ---------
-  std::vector<MergeKey> zk(H.sort_merges ? nz : 0);
+  std::vector<MergeKey> &zk = T.zk;
   std::thread sorter([&] {
     if (!H.sort_merges) return;  // non-reducible linkage: keep the merge order
-    for (int64_t t = 0; t < nz; ++t) zk[t] = {H.zh[t], H.za[t], H.zb[t], H.zs[t]};
-    std::sort(zk.begin(), zk.end(), key_less);
+    if ((int64_t)zk.size() != nz) {  // not built by the replay: sort here
+      zk.resize(nz);
+      for (int64_t t = 0; t < nz; ++t) zk[t] = {H.zh[t], H.za[t], H.zb[t], H.zs[t]};
+      std::sort(zk.begin(), zk.end(), key_less);
+      return;
+    }
+    // merge the sorted batches pairwise (log2(rounds) passes)
+    std::vector<int64_t> r = T.runs;
+    while (r.size() > 2) {
+      std::vector<int64_t> nr;
+      for (size_t i = 0; i + 2 < r.size(); i += 2) {
+        std::inplace_merge(zk.begin() + r[i], zk.begin() + r[i + 1], zk.begin() + r[i + 2], key_less);
+        nr.push_back(r[i]);
+      }
+      if (r.size() % 2 == 0) nr.push_back(r[r.size() - 2]);
+      nr.push_back(r.back());
+      r.swap(nr);
+    }
   });
 
   // ---- collapse (X11) -----------------------------------------------------

@@ -198,7 +198,13 @@ int host_threads();
 
 // Incremental raw-tree replay, so the host tree can be built while the device
 // is still running later linkage rounds.
+struct MergeKey {  // one merge in the exported (key-sorted, X9) order
+  float h;
+  int32_t a, b, size;
+};
 struct TreeBuild {
+  std::vector<MergeKey> zk;     // merges replayed so far, each round's batch sorted by key
+  std::vector<int64_t> runs;    // boundaries of the sorted batches in zk
   std::vector<uint32_t> lset;   // [N][K] sorted leaf sets
   std::vector<int64_t> voff;    // [N] offsets of merge t's intersection set
   std::vector<uint32_t> vpool;
