@@ -70,6 +70,8 @@ void host_begin(HostIndex &H, TreeBuild &T) {
   const int nth = host_threads();
   T.zk.clear();
   T.runs.clear();
+  T.rpar.assign((size_t)(N + std::max<int64_t>(N - 1, 0)), -1);
+  T.keep.assign((size_t)std::max<int64_t>(N - 1, 0), 1);
   if (H.sort_merges) T.zk.reserve((size_t)std::max<int64_t>(N - 1, 0));
   // sorted leaf sets (parallel)
   T.lset.resize((size_t)N * K);
@@ -149,6 +151,14 @@ void host_replay(HostIndex &H, TreeBuild &T, int64_t upto) {
     }
     T.vpool.insert(T.vpool.end(), tmp, tmp + n);
     T.voff[t + 1] = (int64_t)T.vpool.size();
+    // the two children now have their raw parent: collapse flags (X11) of
+    // virtual children are final (a child collapses iff its set equals this
+    // merge's set), computed here while the device runs later rounds
+    T.rpar[A] = N + t;
+    T.rpar[B] = N + t;
+    const uint32_t *ps = T.vpool.data() + T.voff[t];
+    if (A >= N) T.keep[A - N] = (la == n && std::memcmp(pa, ps, 4 * (size_t)n) == 0) ? 0 : 1;
+    if (B >= N) T.keep[B - N] = (lb == n && std::memcmp(pb, ps, 4 * (size_t)n) == 0) ? 0 : 1;
     T.cur[a] = (int32_t)(N + t);
     T.cur[b] = -1;
     T.csize[a] += T.csize[b];
@@ -257,26 +267,17 @@ rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg) {
   vpar.reserve(nz);
   H.lparent.assign(N, 0);
   {
-    std::vector<int64_t> rpar(N + nz, -1);
-#pragma omp parallel for num_threads(nth) schedule(static)
-    for (int64_t t = 0; t < nz; ++t) {
-      rpar[rchild[2 * t]] = N + t;
-      rpar[rchild[2 * t + 1]] = N + t;
-    }
-    std::vector<uint8_t> keep(nz);
-#pragma omp parallel for num_threads(nth) schedule(static)
-    for (int64_t t = 0; t < nz; ++t) {
-      int n1, n2;
-      const uint32_t *s1 = set_ptr(N + t, &n1);
-      const int64_t p = rpar[N + t];
-      bool same;
-      if (p < 0) {
-        same = n1 == 0;
-      } else {
-        const uint32_t *s2 = set_ptr(p, &n2);
-        same = n1 == n2 && std::memcmp(s1, s2, 4 * (size_t)n1) == 0;
-      }
-      keep[t] = same ? 0 : 1;
+    // raw parents and collapse flags come from the replay; the top merge (no
+    // parent) is collapsed iff its set is empty (the root's set)
+    const std::vector<int64_t> &rpar = T.rpar;
+    std::vector<uint8_t> &keep = T.keep;
+    if (nz > 0) {
+      int n1;
+      for (int64_t t = 0; t < nz; ++t)
+        if (rpar[N + t] < 0) {
+          set_ptr(N + t, &n1);
+          keep[t] = n1 == 0 ? 0 : 1;
+        }
     }
     std::vector<int32_t> eff(nz);  // kept node id standing for raw merge t
     for (int64_t t = nz - 1; t >= 0; --t) {

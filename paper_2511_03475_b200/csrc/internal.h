@@ -205,6 +205,8 @@ struct MergeKey {  // one merge in the exported (key-sorted, X9) order
 struct TreeBuild {
   std::vector<MergeKey> zk;     // merges replayed so far, each round's batch sorted by key
   std::vector<int64_t> runs;    // boundaries of the sorted batches in zk
+  std::vector<int64_t> rpar;    // [N + N-1] raw parent node of every node (-1: none yet)
+  std::vector<uint8_t> keep;    // [N-1] raw merge t kept by the collapse (X11), set once its parent exists
   std::vector<uint32_t> lset;   // [N][K] sorted leaf sets
   std::vector<int64_t> voff;    // [N] offsets of merge t's intersection set
   std::vector<uint32_t> vpool;
