@@ -321,15 +321,17 @@ def run_ours(args, ws, rank, local):
     traffic = load_traffic(args.config)
     roof_dist = {"kernel": "k_dist_tile (a2-a4, distance rows + fused row NN)", "bound": "hbm",
                  "achieved": dist_gbs, "peak": hbm, "unit": "GB/s", "frac": dist_gbs / hbm,
-                 "traffic": traffic.get("k_dist_tile") if traffic else None, "peak_source": peak_src,
+                 "traffic": traffic.get("k_dist_tile") if traffic and not sharded else None, "peak_source": peak_src,
                  "algorithmic_bytes_per_launch": dist_bytes, "launches_per_step": 1,
                  "share_of_step": mean["distance_ms"] / ms}
     mb = mean["merge_bytes"] / max(mean["merge_launches"], 1)
     merge_gbs = mean["merge_bytes"] / (mean["merge_ms"] * 1e-3) / 1e9 if mean["merge_ms"] > 0 else 0.0
-    mkern = "k_merge_gather" if codes else "k_merge_rows"
+    # the single-GPU code-mode rounds compact with the gather kernel; the
+    # sharded build and the fp32 rounds with the window kernel
+    mkern = "k_merge_gather" if codes and not sharded else "k_merge_rows"
     roof_merge = {"kernel": f"{mkern} (a5, linkage compaction rounds)", "bound": "hbm",
                   "achieved": merge_gbs, "peak": hbm, "unit": "GB/s", "frac": merge_gbs / hbm,
-                  "traffic": traffic.get(mkern) if traffic else None, "peak_source": peak_src,
+                  "traffic": traffic.get(mkern) if traffic and not sharded else None, "peak_source": peak_src,
                   "algorithmic_bytes_per_launch": mb, "launches_per_step": mean["merge_launches"],
                   "algorithmic_bytes_note": ("2 B (16-bit value code)" if codes else "4 B (fp32)") +
                   " x (live old rows^2 + new rows^2) per launch, averaged",

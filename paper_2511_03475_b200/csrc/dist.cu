@@ -563,6 +563,9 @@ rb_status build_index_dist(rb_dist *d, const uint32_t *ids_d, const uint8_t *len
     worker.join();
   };
   int M = (int)N, rounds = 0, zdone = 0, par = 0;
+  std::vector<cudaEvent_t> merge_ev;
+  double merge_bytes = 0.0;
+  int merge_launches = 0;
   int64_t S = L.S0, ld = N;
   // current matrix: the fp32 distance shards (rows), then A / B alternately;
   // in code mode the first matrix is the code shard in B (then A / B)
@@ -666,6 +669,10 @@ rb_status build_index_dist(rb_dist *d, const uint32_t *ids_d, const uint8_t *len
         cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kf, nth, smem);
       }
+      cudaEvent_t me[2];  // compaction timing (rb_stats.merge_ms / merge_bytes, this process's ranks)
+      cudaEventCreate(&me[0]);
+      cudaEventCreate(&me[1]);
+      cudaEventRecord(me[0], st);
       for (int l = 0; l < nloc; ++l) {
         const int r = g0 + l;
         unsigned char *sc = d->scratch[r];
@@ -683,8 +690,17 @@ rb_status build_index_dist(rb_dist *d, const uint32_t *ids_d, const uint8_t *len
                                         pa[l].Mn, pa[l].goff, pa[l].gmem, pa[l].colsrc, pa[l].cursor, W, c0, c1,
                                         reinterpret_cast<float *>(Dn), at<unsigned long long>(sc, knoff));
           ++launches;
+          // algorithmic bytes of this rank: its new rows' member rows read
+          // (M columns each) and the new rows written
+          const double es = codes ? 2.0 : 4.0;
+          merge_bytes += es * ((double)(c1 - c0) * (double)M * ((double)M / (double)Mn) +
+                               (double)(c1 - c0) * (double)Mn);
         }
       }
+      cudaEventRecord(me[1], st);
+      merge_ev.push_back(me[0]);
+      merge_ev.push_back(me[1]);
+      ++merge_launches;
       if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) break;
       if ((e = barrier()) != cudaSuccess) break;
       for (int l = 0; l < nloc; ++l) {
@@ -728,6 +744,18 @@ rb_status build_index_dist(rb_dist *d, const uint32_t *ids_d, const uint8_t *len
   cudaEventElapsedTime(&ms, ev[1], ev[2]);
   H.stats.linkage_ms = ms;
   H.stats.linkage_rounds = rounds;
+  {
+    float mt = 0.f;
+    for (size_t i = 0; i + 1 < merge_ev.size(); i += 2) {
+      float x = 0.f;
+      cudaEventElapsedTime(&x, merge_ev[i], merge_ev[i + 1]);
+      mt += x;
+    }
+    for (auto &x : merge_ev) cudaEventDestroy(x);
+    H.stats.merge_ms = mt;
+    H.stats.merge_bytes = merge_bytes;
+    H.stats.merge_launches = merge_launches;
+  }
   H.stats.kernel_launches = launches;
   H.stats.value_codes = codes ? 1 : 0;
   const auto th = std::chrono::steady_clock::now();
