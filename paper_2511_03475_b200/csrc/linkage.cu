@@ -203,6 +203,8 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
   // RAGB_INPLACE=0 / 1: never / always take in-place rounds (testing); unset: cost model
   const char *ipm = std::getenv("RAGB_INPLACE");
   const int inplace_mode = ipm ? std::atoi(ipm) : 2;
+  const char *ipw = std::getenv("RAGB_INPLACE_W");  // cost-model weight of a merge (row equivalents)
+  const double inplace_w = ipw ? std::atof(ipw) : 32.0;
   cudaEvent_t tev[3];
   if (trace)
     for (auto &x : tev) cudaEventCreate(&x);
@@ -274,7 +276,7 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
     // 4-byte store per row and merge, ~30 row-equivalents per merge measured)
     // and the rescans cost less than rewriting the matrix (~live + Mn^2/M rows)
     const bool inplace = Mn > 1 && cur != original && M <= kInplaceMaxM && inplace_mode != 0 &&
-                         (inplace_mode == 1 || 32.0 * merges_round < (double)live + (double)Mn * Mn / M);
+                         (inplace_mode == 1 || inplace_w * merges_round < (double)live + (double)Mn * Mn / M);
     if (inplace) {
       if (!mask_ok) {
         if ((e = cudaMemsetAsync(amask, 0xff, (size_t)(M / 32 + 1) * 4, st)) != cudaSuccess) return e;
