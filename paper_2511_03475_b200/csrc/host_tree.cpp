@@ -313,19 +313,24 @@ rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg) {
   H.kids.assign(V + N, 0);
   std::vector<int32_t> child_idx(1 + V + N, 0);
   {
-    // nodes in ascending rep order (counting sort over reps in [0, N); a node
-    // and its leftmost descendants share a rep but are never siblings), then
-    // scattered to their parents: every child list comes out sorted (X12)
-    std::vector<int32_t> rcnt(N + 1, 0), byrep(V + N);
-    for (int64_t x = 1; x <= V + N; ++x) ++rcnt[rep_of[x] + 1];
-    for (int64_t r = 0; r < N; ++r) rcnt[r + 1] += rcnt[r];
-    for (int64_t x = 1; x <= V + N; ++x) byrep[rcnt[rep_of[x]]++] = (int32_t)x;
+    // nodes in ascending rep order, then appended to their parents' lists:
+    // every child list comes out sorted (X12).  Leaf i is the rep of itself
+    // and of the chain of kept ancestors whose smallest leaf it is, so walking
+    // up from each leaf in index order visits every node once, by rep (a node
+    // and its leftmost descendants share a rep but are never siblings).
     std::vector<int64_t> fill(H.kids_off.begin(), H.kids_off.end() - 1);
-    for (int64_t z = 0; z < V + N; ++z) {
-      const int32_t x = byrep[z];
-      const int32_t par = x <= V ? vpar[x - 1] : H.lparent[x - V - 1];
+    auto put = [&](int32_t x, int32_t par) {
       child_idx[x] = (int32_t)(fill[par] - H.kids_off[par]);
       H.kids[fill[par]++] = x;
+    };
+    for (int64_t i = 0; i < N; ++i) {
+      int32_t y = H.lparent[i];
+      put((int32_t)(V + 1 + i), y);
+      while (y > 0 && rep_of[y] == (int32_t)i) {
+        const int32_t py = vpar[y - 1];
+        put(y, py);
+        y = py;
+      }
     }
   }
   lap("children");
