@@ -89,6 +89,19 @@ typedef struct rb_params {
   void *stream;         /* cudaStream_t to launch on (NULL = legacy default stream)  */
   int64_t row0;         /* first distance row this call computes (row sharding)     */
   int64_t nrows;        /* number of rows, -1 = all N (linkage needs all rows)      */
+  /* Implementation strategy (tuning and testing).  No result depends on these:
+   * the GPU tests compare every setting with the oracle bit for bit.
+   * rb_params_init sets each one to its automatic default (-1 or 0). */
+  int32_t value_codes;    /* -1 auto: the linkage runs on 16-bit value codes for
+                             uniform K <= 32 (complete linkage); 0: fp32 matrices  */
+  int32_t inplace;        /* -1 cost model; 0 never; 1 every round where allowed   */
+  float inplace_weight;   /* cost-model weight of one merge, in row equivalents
+                             (0 = default 32)                                      */
+  int32_t gather;         /* -1 auto; 0 window compaction only (no row gather)     */
+  int32_t long_lists;     /* -1 auto; 0 the general distance kernel for 32<K<=128  */
+  int32_t dist_grid;      /* 0 auto; > 0 caps the distance kernel's grid           */
+  int32_t host_threads;   /* 0 auto (all cores); > 0 host tree-stage threads       */
+  int32_t trace;          /* 1: per-round linkage / host-stage trace on stderr     */
 } rb_params;
 
 /* Per-build statistics (host, filled by rb_build_index). Times are CUDA-event
@@ -109,7 +122,22 @@ typedef struct rb_stats {
   int32_t value_codes;    /* 1: the linkage ran on 16-bit value codes written by the
                              distance kernel next to the fp32 rows (uniform K <= 32,
                              complete linkage); 0: on the fp32 rows              */
+  int32_t max_level;      /* largest level list of the linkage rounds (vertices at
+                             the round's minimum height)                          */
+  int32_t paths;          /* kernel variants the linkage ran (RB_PATH_* bits)     */
 } rb_stats;
+
+/* rb_stats.paths bits: which implementation variants a build exercised (tests
+ * use them to prove that a parity case reaches the path it is meant for). */
+enum rb_path_bits {
+  RB_PATH_GATHER = 1u << 0,        /* row-gather compaction, 256-thread CTAs      */
+  RB_PATH_GATHER_WIDE = 1u << 1,   /* row-gather compaction, 1024-thread CTAs     */
+  RB_PATH_WINDOW = 1u << 2,        /* window compaction, 256-thread CTAs          */
+  RB_PATH_WINDOW_WIDE = 1u << 3,   /* window compaction, 1024-thread CTAs         */
+  RB_PATH_INPLACE = 1u << 4,       /* in-place round                              */
+  RB_PATH_CLIQUE_WARP = 1u << 5,   /* level cliques, warp-resident path           */
+  RB_PATH_CLIQUE_BLOCK = 1u << 6   /* level cliques, block path (> 4096 vertices) */
+};
 
 typedef struct rb_index rb_index;
 typedef struct rb_session rb_session;

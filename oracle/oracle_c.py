@@ -89,9 +89,13 @@ def row_nn(d, row0=0):
     return idx, val
 
 
-def linkage(d):
-    """Complete linkage (NN-chain) of a full N×N matrix (copied)."""
-    d = np.array(d, dtype=np.float32, order="C", copy=True)
+def linkage(d, overwrite=False):
+    """Complete linkage (NN-chain) of a full N×N matrix (copied, unless
+    overwrite=True and d is already a C-contiguous float32 array: then d is
+    used as the work matrix and destroyed — for C4's 40 GB rows)."""
+    if not (overwrite and isinstance(d, np.ndarray) and d.dtype == np.float32 and d.flags.c_contiguous
+            and d.flags.writeable):
+        d = np.array(d, dtype=np.float32, order="C", copy=True)
     N = d.shape[0]
     a = np.empty(max(N - 1, 0), dtype=np.int32)
     b = np.empty_like(a)

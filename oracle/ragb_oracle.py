@@ -322,13 +322,17 @@ def build_tree(ctxs, Z) -> Tree:
     t.ordered[root] = []
 
     def expand(raw, parent_set):
-        # collapse a virtual node whose set equals its parent's (X11)
-        if raw >= N and r_set[raw] == parent_set:
-            out = []
-            for c in r_children[raw]:
-                out.extend(expand(c, parent_set))
-            return out
-        return [raw]
+        # collapse a virtual node whose set equals its parent's (X11), and
+        # recursively its collapsed descendants; left-to-right preorder with an
+        # explicit stack (caterpillar trees outgrow Python's recursion limit)
+        out, todo = [], [raw]
+        while todo:
+            r = todo.pop()
+            if r >= N and r_set[r] == parent_set:
+                todo.extend(reversed(r_children[r]))
+            else:
+                out.append(r)
+        return out
 
     stack = [(root, top)]
     pending = [(root, [top])]

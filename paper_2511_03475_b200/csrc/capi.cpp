@@ -73,6 +73,19 @@ rb_status check_params(int64_t N, int32_t K, const rb_params *p, int64_t *row0, 
 
 namespace ragb {
 
+Tuning Tuning::from(const rb_params *p) {
+  Tuning t;
+  t.value_codes = p->value_codes;
+  t.inplace = p->inplace;
+  if (p->inplace_weight > 0.f) t.inplace_weight = p->inplace_weight;
+  t.gather = p->gather;
+  t.long_lists = p->long_lists;
+  t.dist_grid = p->dist_grid;
+  t.host_threads = p->host_threads;
+  t.trace = p->trace != 0;
+  return t;
+}
+
 ScratchLayout ScratchLayout::make(int64_t N, int32_t K, bool keep_rows, bool linkage) {
   ScratchLayout L{};
   size_t o = 0;
@@ -146,6 +159,14 @@ rb_status rb_params_init(rb_params *p) {
   p->stream = nullptr;
   p->row0 = 0;
   p->nrows = -1;
+  p->value_codes = -1;
+  p->inplace = -1;
+  p->inplace_weight = 0.f;
+  p->gather = -1;
+  p->long_lists = -1;
+  p->dist_grid = 0;
+  p->host_threads = 0;
+  p->trace = 0;
   return RB_OK;
 }
 
@@ -188,6 +209,9 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
   H.K = K;
   H.alpha_num = p->alpha_num;
   H.alpha_den = p->alpha_den;
+  const ragb::Tuning tu = ragb::Tuning::from(p);
+  H.trace = tu.trace;
+  ragb::set_host_threads(tu.host_threads);
   int launches = 0;
   cudaError_t e;
   cudaEvent_t ev[4];
@@ -257,11 +281,12 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
   da.D_out = (p->flags & RB_EMIT_COUNTS) ? D_dev : nullptr;
   da.nnkey = reinterpret_cast<unsigned long long *>(sc + L.nnkey);
   da.lut = nullptr;
+  da.grid_cap = tu.dist_grid;
+  da.long_lists = tu.long_lists != 0;
   // complete linkage on 16-bit value codes whenever the tile
-  // path's Eq. 1 table exists; RAGB_CODES=0 keeps the fp32 matrices (testing)
-  const char *cenv = std::getenv("RAGB_CODES");
+  // path's Eq. 1 table exists; value_codes = 0 keeps the fp32 matrices (testing)
   const bool code_mode = linkage && p->linkage == RB_LINK_COMPLETE && N > 1 &&
-                         ragb::tile_path_ok(K, lens_d == nullptr) && !(cenv && std::atoi(cenv) == 0);
+                         ragb::tile_path_ok(K, lens_d == nullptr) && tu.value_codes != 0;
   ragb::CodeMode cm{};
   {
     int stride;
@@ -388,7 +413,8 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
             avail = upto;
           }
           cv.notify_one();
-        });
+        },
+        tu);
     {
       std::lock_guard<std::mutex> lk(mu);
       finished = true;
@@ -425,6 +451,8 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
   H.stats.merge_launches = lo.merge_launches;
   H.stats.merge_bytes = lo.merge_bytes;
   H.stats.value_codes = code_mode ? 1 : 0;
+  H.stats.max_level = lo.max_level;
+  H.stats.paths = (int32_t)lo.paths;
   H.stats.kernel_launches = launches;
 
   // ---- a6-a7: tree, orders, schedule (host) --------------------------------

@@ -435,8 +435,8 @@ rb_status build_index_dist(rb_dist *d, const uint32_t *ids_d, const uint8_t *len
   // code mode (as in the single-GPU build): each rank also
   // writes the 16-bit value codes of its rows (into its B buffer, the first
   // round's input) and the rounds run on codes
-  const char *cenv = std::getenv("RAGB_CODES");
-  const bool codes = N > 1 && tile_path_ok(K, lens_d == nullptr) && !(cenv && std::atoi(cenv) == 0);
+  const Tuning tu = Tuning::from(p);
+  const bool codes = N > 1 && tile_path_ok(K, lens_d == nullptr) && tu.value_codes != 0;
   for (int l = 0; l < nloc; ++l) {
     const int r = g0 + l;
     unsigned char *sc = d->scratch[r];
@@ -496,6 +496,10 @@ rb_status build_index_dist(rb_dist *d, const uint32_t *ids_d, const uint8_t *len
   }
 
   // ---- a5: complete linkage, rows sharded -----------------------------------
+  // every rank must have gathered the peers' f32 key slices before any rank
+  // rewrites its own slice as code keys below (a slow peer could
+  // otherwise read already-converted keys)
+  if (codes) DC(barrier(), "barrier");
   H.za.assign(std::max<int64_t>(N - 1, 0), 0);
   H.zb.assign(H.za.size(), 0);
   H.zh.assign(H.za.size(), 0.0f);

@@ -359,7 +359,7 @@ cudaError_t launch_one(const DistArgs &a, const SmemPlan &P, cudaStream_t st) {
   if (per_sm < 1) per_sm = 1;
   const int64_t ntiles = (a.nrows + R - 1) / R;
   int64_t grid = std::min<int64_t>(ntiles, (int64_t)sms * per_sm);
-  if (const char *g = std::getenv("RAGB_DIST_GRID")) grid = std::min<int64_t>(ntiles, std::atoll(g));
+  if (a.grid_cap > 0) grid = std::min<int64_t>(ntiles, a.grid_cap);
   kern<<<(unsigned)grid, NT, P.total, st>>>(a, P);
   return cudaGetLastError();
 }
@@ -461,7 +461,7 @@ cudaError_t launch_code_table(const float *lut, int32_t K, int stride, int64_t e
 cudaError_t launch_distance(const DistArgs &a, cudaStream_t st, int *launches) {
   ++*launches;
   if (tile_path_ok(a.K, a.lens == nullptr) && a.lut) return launch_distance_tile(a, st);
-  if (wide_path_ok(a.K, a.lens == nullptr) && !std::getenv("RAGB_NO_WIDE")) return launch_distance_wide(a, st);
+  if (wide_path_ok(a.K, a.lens == nullptr) && a.long_lists) return launch_distance_wide(a, st);
   // General path (variable lengths, K > 32): a table of d(s, D) when every
   // context has K docs (smem copy if small, else read through L1/L2), else the
   // exact division.

@@ -414,7 +414,7 @@ cudaError_t launch(const DistArgs &a, const Plan &P, cudaStream_t st) {
   if (per_sm < 1) per_sm = 1;
   const int64_t ntiles = (a.nrows + R - 1) / R;
   int64_t grid = std::min<int64_t>(ntiles, (int64_t)sms * per_sm);
-  if (const char *g = std::getenv("RAGB_DIST_GRID")) grid = std::min<int64_t>(ntiles, std::atoll(g));
+  if (a.grid_cap > 0) grid = std::min<int64_t>(ntiles, a.grid_cap);
   kern<<<(unsigned)grid, NT, P.total, st>>>(a, P);
   return cudaGetLastError();
 }

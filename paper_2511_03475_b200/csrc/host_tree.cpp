@@ -18,6 +18,7 @@
 #include <omp.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -51,9 +52,13 @@ inline bool in_sorted(const uint32_t *s, int n, uint32_t x) {
 
 }  // namespace
 
+static std::atomic<int> g_host_threads{0};
+
+void set_host_threads(int n) { g_host_threads.store(std::max(0, n)); }
+
 int host_threads() {
+  if (const int o = g_host_threads.load()) return o;
   static int n = [] {
-    if (const char *e = std::getenv("RAGB_HOST_THREADS")) return std::max(1, std::atoi(e));
     // one core is left to the side sorter / CUDA driver thread: a static OpenMP
     // schedule with one oversubscribed core stalls every barrier (measured:
     // 15 threads 8 ms, 16 threads 14-20 ms on a 16-core host at C4)
@@ -191,7 +196,7 @@ rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg) {
   const int32_t K = H.K;
   const bool uniform = H.lens.empty();
   const int nth = host_threads();
-  const bool trace = std::getenv("RAGB_TRACE") != nullptr;
+  const bool trace = H.trace;
   auto t_last = std::chrono::steady_clock::now();
   auto lap = [&](const char *what) {
     if (!trace) return;

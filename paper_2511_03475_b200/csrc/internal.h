@@ -38,6 +38,20 @@ struct ScratchLayout {
   static ScratchLayout make(int64_t N, int32_t K, bool keep_rows, bool linkage);
 };
 
+// Implementation strategy of one build (rb_params' strategy fields, ragb.h).
+// No result depends on it; the GPU tests compare every setting with the oracle.
+struct Tuning {
+  int value_codes = -1;         // -1 auto, 0 fp32 linkage matrices
+  int inplace = -1;             // -1 cost model, 0 never, 1 wherever allowed
+  float inplace_weight = 32.f;  // cost-model weight of a merge (row equivalents)
+  int gather = -1;              // -1 auto, 0 window compaction only
+  int long_lists = -1;          // -1 auto, 0 general kernel for 32 < K <= 128
+  int dist_grid = 0;            // 0 auto, > 0 grid cap of the distance kernel
+  int host_threads = 0;         // 0 auto
+  bool trace = false;           // per-round trace on stderr
+  static Tuning from(const rb_params *p);
+};
+
 // ----------------------------------------------------------------- kernels
 struct DistArgs {
   const uint32_t *ids;   // [N][K] row-major
@@ -56,6 +70,8 @@ struct DistArgs {
   const uint32_t *lutc;       // [lut entries] or nullptr
   const float *vals;          // [ncode] ascending distinct table values
   uint16_t *codes;            // [nrows][N] or nullptr
+  int grid_cap = 0;           // Tuning::dist_grid
+  bool long_lists = true;     // Tuning::long_lists != 0
 };
 
 // Order-preserving codes of the Eq. 1 table (distance.cu): lutc[e] = number
@@ -100,6 +116,8 @@ struct LinkageOut {
   float merge_ms = 0.f;     // CUDA-event time of the compaction (k_merge_rows) launches
   int merge_launches = 0;
   double merge_bytes = 0;   // their algorithmic bytes: live old rows read + new rows written
+  int max_level = 0;        // largest level list
+  unsigned paths = 0;       // RB_PATH_* bits
 };
 
 // a5: complete linkage on the full rows (rows ld = N) starting from the fused
@@ -121,7 +139,7 @@ cudaError_t run_linkage_intersection(float *rows, int64_t ld, int64_t N, int32_t
 cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void *scratch,
                         const ScratchLayout &L, bool keep_rows, const CodeMode *cm, cudaStream_t st,
                         int32_t *za, int32_t *zb, float *zh, int32_t *zs, LinkageOut *out, int *launches,
-                        const std::function<void(int64_t)> &on_round);
+                        const std::function<void(int64_t)> &on_round, const Tuning &tu);
 
 // ----------------------------------------------------------------- host
 struct DynTree;  // online (mutable) form of the tree, online.cpp
@@ -171,6 +189,7 @@ struct HostIndex {
   std::vector<int64_t> schedule;    // [N]
   rb_stats stats{};
   uint32_t alpha_num = 1, alpha_den = 200;
+  bool trace = false;       // Tuning::trace (host-stage laps on stderr)
   bool sort_merges = true;  // complete linkage: export ascending key (X9); intersection: merge order
   std::shared_ptr<DynTree> dyn;             // set by the first online update
 };
@@ -195,6 +214,7 @@ void dyn_order_all(const HostIndex &H, uint32_t *out_ids, uint8_t *out_prefix_le
 // orders and schedule (a6-a7).  Returns RB_OK or RB_EINVAL with msg.
 rb_status host_build(HostIndex &H, std::string *msg);
 int host_threads();
+void set_host_threads(int n);  // 0 = auto (Tuning::host_threads of the current build)
 
 // Incremental raw-tree replay, so the host tree can be built while the device
 // is still running later linkage rounds.

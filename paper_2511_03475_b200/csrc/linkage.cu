@@ -60,7 +60,8 @@ int occupancy_cached(F kern, int nth, size_t smem) {
   std::lock_guard<std::mutex> lk(mu);
   size_t &a = attr[key];
   if (smem > a) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return 0;  // the launch would fail: the caller reports it
     a = smem;
   }
   auto it = occ.find({key, nth, smem});
@@ -72,27 +73,51 @@ int occupancy_cached(F kern, int nth, size_t smem) {
   return per_sm;
 }
 
+// Dynamic shared memory a kernel may opt into: the per-block opt-in limit
+// minus the kernel's static shared memory (the static part counts
+// against the same 227 KB).
+template <typename F>
+size_t dyn_smem_limit(F kern) {
+  static std::mutex mu;
+  static std::map<const void *, size_t> lim;
+  const void *key = reinterpret_cast<const void *>(kern);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = lim.find(key);
+  if (it != lim.end()) return it->second;
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncAttributes fa{};
+  cudaFuncGetAttributes(&fa, kern);
+  const size_t l = (size_t)optin > fa.sharedSizeBytes ? (size_t)optin - fa.sharedSizeBytes : 0;
+  lim[key] = l;
+  return l;
+}
+
 // Compaction launch for element type T (see k_merge_rows): wide rows get
 // 1024-thread CTAs, one per SM, with a window of up to 56K columns; narrow
 // rows 256-thread CTAs so that several rows are in flight per SM.
 template <typename T>
 cudaError_t launch_merge(const T *cur, int64_t ld, int M, int Mn, const PrepArgs &pa, int sms, T *next,
-                         unsigned long long *keyn, cudaStream_t st) {
+                         unsigned long long *keyn, cudaStream_t st, const Tuning &tu, unsigned *paths) {
   constexpr int VW = Elem<T>::VW;
-  const char *genv = std::getenv("RAGB_GATHER");
-  if (sizeof(T) == 2 && pa.pmap && (size_t)((M + 7) / 8) * 16 <= 227 * 1024 && !(genv && std::atoi(genv) == 0)) {
+  const size_t row_bytes = (size_t)((M + 7) / 8) * 16;
+  const bool vec16 = ld % 8 == 0 && (reinterpret_cast<uintptr_t>(cur) & 15) == 0;
+  const bool wide16 = M > 16 * 1024;
+  auto gkern = wide16 ? (vec16 ? k_merge_gather<true, 1024> : k_merge_gather<false, 1024>)
+                      : (vec16 ? k_merge_gather<true, 256> : k_merge_gather<false, 256>);
+  const size_t glim = sizeof(T) == 2 && pa.pmap ? dyn_smem_limit(gkern) : 0;
+  if (sizeof(T) == 2 && pa.pmap && row_bytes <= glim && tu.gather != 0) {
     // code mode, old row fits in shared memory: gather form (k_merge_gather)
     const uint16_t *c16 = reinterpret_cast<const uint16_t *>(cur);
     uint16_t *n16 = reinterpret_cast<uint16_t *>(next);
-    const bool vec = ld % 8 == 0 && (reinterpret_cast<uintptr_t>(cur) & 15) == 0;
-    const size_t row_bytes = (size_t)((M + 7) / 8) * 16;
-    const int db = vec && 2 * row_bytes <= 227 * 1024 ? 1 : 0;  // double-buffered rows
+    const int db = vec16 && 2 * row_bytes <= glim ? 1 : 0;  // double-buffered rows
     const size_t smem = row_bytes * (1 + db);
-    const bool wide = M > 16 * 1024;
-    auto kern = wide ? (vec ? k_merge_gather<true, 1024> : k_merge_gather<false, 1024>)
-                     : (vec ? k_merge_gather<true, 256> : k_merge_gather<false, 256>);
-    const int nth = wide ? 1024 : 256;
+    auto kern = gkern;
+    const int nth = wide16 ? 1024 : 256;
     const int per_sm = occupancy_cached(kern, nth, smem);
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    *paths |= wide16 ? RB_PATH_GATHER_WIDE : RB_PATH_GATHER;
     const int grid = std::min<int>(Mn, sms * per_sm);
     kern<<<grid, nth, smem, st>>>(c16, ld, M, pa.Mn, pa.goff, pa.gmem, pa.pmap, n16, keyn, db);
     return cudaGetLastError();
@@ -107,6 +132,8 @@ cudaError_t launch_merge(const T *cur, int64_t ld, int M, int Mn, const PrepArgs
   auto kern = wide ? (vec ? k_merge_rows<true, 1024, T, LocalRows<T>> : k_merge_rows<false, 1024, T, LocalRows<T>>)
                    : (vec ? k_merge_rows<true, 256, T, LocalRows<T>> : k_merge_rows<false, 256, T, LocalRows<T>>);
   const int per_sm = occupancy_cached(kern, nth, smem);
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  *paths |= wide ? RB_PATH_WINDOW_WIDE : RB_PATH_WINDOW;
   const int grid = std::min<int>(Mn, sms * per_sm);
   kern<<<grid, nth, smem, st>>>(LocalRows<T>{cur, ld}, M, pa.Mn, pa.goff, pa.gmem, pa.colsrc, pa.cursor, W, 0, -1,
                                 next, keyn);
@@ -134,7 +161,7 @@ cudaError_t launch_inplace(T *cur, int64_t ld, int M, int max_groups, const Prep
 cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void *scratch,
                         const ScratchLayout &L, bool keep_rows, const CodeMode *cm, cudaStream_t st,
                         int32_t *za, int32_t *zb, float *zh, int32_t *zs, LinkageOut *out, int *launches,
-                        const std::function<void(int64_t)> &on_round) {
+                        const std::function<void(int64_t)> &on_round, const Tuning &tu) {
   out->rounds = 0;
   if (N <= 1) return cudaSuccess;
   int dev = 0, sms = 0;
@@ -188,7 +215,6 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
   }
 
   void *cur = codes ? static_cast<void *>(cm->codes) : static_cast<void *>(rows);
-  const void *original = cur;
   int64_t ld = N;
   int M = (int)N;   // rows of the current matrix (live + dead)
   int live = (int)N;  // live clusters
@@ -198,13 +224,11 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
   int *nmulti = counters + 12;
   int p = 0;
   void *next = matA;
-  // RAGB_TRACE=1: per-round timing on stderr (diagnostics only).
-  const bool trace = std::getenv("RAGB_TRACE") != nullptr;
-  // RAGB_INPLACE=0 / 1: never / always take in-place rounds (testing); unset: cost model
-  const char *ipm = std::getenv("RAGB_INPLACE");
-  const int inplace_mode = ipm ? std::atoi(ipm) : 2;
-  const char *ipw = std::getenv("RAGB_INPLACE_W");  // cost-model weight of a merge (row equivalents)
-  const double inplace_w = ipw ? std::atof(ipw) : 32.0;
+  // per-round timing on stderr (diagnostics only)
+  const bool trace = tu.trace;
+  // in-place rounds: 0 never, 1 wherever allowed (testing), -1 cost model
+  const int inplace_mode = tu.inplace < 0 ? 2 : tu.inplace;
+  const double inplace_w = tu.inplace_weight;  // cost-model weight of a merge (row equivalents)
   cudaEvent_t tev[3];
   if (trace)
     for (auto &x : tev) cudaEventCreate(&x);
@@ -242,7 +266,7 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (trace) cudaEventRecord(tev[1], st);
     int host_c[12] = {0};
-    if ((e = cudaMemcpyAsync(host_c, counters, (trace ? 12 : 2) * sizeof(int), cudaMemcpyDeviceToHost, st)) !=
+    if ((e = cudaMemcpyAsync(host_c, counters, (trace ? 12 : 3) * sizeof(int), cudaMemcpyDeviceToHost, st)) !=
         cudaSuccess)
       return e;
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
@@ -270,12 +294,15 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
     }
     const int Mn = host_c[1];
     if (Mn >= live || Mn < 1) return cudaErrorUnknown;  // no progress: invariant violated
+    out->max_level = std::max(out->max_level, host_c[2]);
+    if (host_c[2] >= 2) out->paths |= host_c[2] <= kWarpCliqueMaxN ? RB_PATH_CLIQUE_WARP : RB_PATH_CLIQUE_BLOCK;
     const int merges_round = host_c[0] - zprev;
     zprev = host_c[0];
     // in place when the merged rows, the rewritten columns (one scattered
     // 4-byte store per row and merge, ~30 row-equivalents per merge measured)
     // and the rescans cost less than rewriting the matrix (~live + Mn^2/M rows)
-    const bool inplace = Mn > 1 && cur != original && M <= kInplaceMaxM && inplace_mode != 0 &&
+    const int ivw = codes ? Elem<uint16_t>::VW : Elem<float>::VW;  // in-place kernels: 16-byte row vectors
+    const bool inplace = Mn > 1 && (codes || !keep_rows || cur != static_cast<void *>(rows)) && ld % ivw == 0 && (reinterpret_cast<uintptr_t>(cur) & 15) == 0 && M <= kInplaceMaxM && inplace_mode != 0 &&
                          (inplace_mode == 1 || inplace_w * merges_round < (double)live + (double)Mn * Mn / M);
     if (inplace) {
       if (!mask_ok) {
@@ -289,6 +316,7 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
                 : launch_inplace<float>(static_cast<float *>(cur), ld, M, merges_round, pa, sms, amask, mlist, nmulti,
                                         sz[p], key[p], st);
       *launches += 5;
+      out->paths |= RB_PATH_INPLACE;
       if (e != cudaSuccess) return e;
     } else if (Mn > 1) {
       cudaEvent_t me[2];
@@ -296,9 +324,9 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
       cudaEventCreateWithFlags(&me[1], cudaEventDefault);
       cudaEventRecord(me[0], st);
       e = codes ? launch_merge<uint16_t>(static_cast<const uint16_t *>(cur), ld, M, Mn, pa, sms,
-                                         static_cast<uint16_t *>(next), key[p ^ 1], st)
+                                         static_cast<uint16_t *>(next), key[p ^ 1], st, tu, &out->paths)
                 : launch_merge<float>(static_cast<const float *>(cur), ld, M, Mn, pa, sms, static_cast<float *>(next),
-                                      key[p ^ 1], st);
+                                      key[p ^ 1], st, tu, &out->paths);
       cudaEventRecord(me[1], st);
       mev.push_back(me[0]);
       mev.push_back(me[1]);

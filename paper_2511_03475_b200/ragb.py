@@ -22,6 +22,8 @@ RB_OK, RB_EINVAL, RB_EDUPDOC, RB_EALPHA, RB_ENOMEM, RB_ECUDA, RB_ENCCL, RB_EPATH
 RB_EMIT_COUNTS, RB_ALPHA_ANY, RB_KEEP_ROWS, RB_SKIP_LINKAGE = 1, 2, 4, 8
 RB_LINK_COMPLETE, RB_LINK_INTERSECTION = 0, 1
 RB_CACHE_APPENDED, RB_CACHE_ACCESSED, RB_CACHE_EVICTED = 0, 1, 2
+RB_PATH_GATHER, RB_PATH_GATHER_WIDE, RB_PATH_WINDOW, RB_PATH_WINDOW_WIDE, RB_PATH_INPLACE, \
+    RB_PATH_CLIQUE_WARP, RB_PATH_CLIQUE_BLOCK = 1, 2, 4, 8, 16, 32, 64
 
 STATUS_NAMES = {0: "RB_OK", -1: "RB_EINVAL", -2: "RB_EDUPDOC", -3: "RB_EALPHA", -4: "RB_ENOMEM",
                 -5: "RB_ECUDA", -6: "RB_ENCCL", -7: "RB_EPATH", -8: "RB_ESESSION", -9: "RB_ESTATE"}
@@ -48,7 +50,15 @@ class RagbError(RuntimeError):
 class Params(ctypes.Structure):
     _fields_ = [("alpha_num", ctypes.c_uint32), ("alpha_den", ctypes.c_uint32),
                 ("linkage", ctypes.c_int32), ("flags", ctypes.c_uint32),
-                ("stream", ctypes.c_void_p), ("row0", ctypes.c_int64), ("nrows", ctypes.c_int64)]
+                ("stream", ctypes.c_void_p), ("row0", ctypes.c_int64), ("nrows", ctypes.c_int64),
+                # implementation strategy (ragb.h): no result depends on it
+                ("value_codes", ctypes.c_int32), ("inplace", ctypes.c_int32),
+                ("inplace_weight", ctypes.c_float), ("gather", ctypes.c_int32),
+                ("long_lists", ctypes.c_int32), ("dist_grid", ctypes.c_int32),
+                ("host_threads", ctypes.c_int32), ("trace", ctypes.c_int32)]
+
+TUNING_FIELDS = ("value_codes", "inplace", "inplace_weight", "gather", "long_lists", "dist_grid",
+                 "host_threads", "trace")
 
 
 class Stats(ctypes.Structure):
@@ -58,7 +68,8 @@ class Stats(ctypes.Structure):
                 ("kernel_launches", ctypes.c_int32), ("n_virtual", ctypes.c_int64),
                 ("max_depth", ctypes.c_int64), ("merge_ms", ctypes.c_float),
                 ("merge_launches", ctypes.c_int32), ("merge_bytes", ctypes.c_double),
-                ("value_codes", ctypes.c_int32)]
+                ("value_codes", ctypes.c_int32), ("max_level", ctypes.c_int32),
+                ("paths", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -145,7 +156,10 @@ def alpha_rational(alpha) -> tuple[int, int]:
     return f.numerator, f.denominator
 
 
-def make_params(alpha=(1, 200), flags=0, stream=None, row0=0, nrows=-1, linkage=RB_LINK_COMPLETE) -> Params:
+def make_params(alpha=(1, 200), flags=0, stream=None, row0=0, nrows=-1, linkage=RB_LINK_COMPLETE,
+                tuning: dict | None = None) -> Params:
+    """tuning: implementation-strategy fields of rb_params (TUNING_FIELDS);
+    the library's automatic choice where absent."""
     p = Params()
     _check(lib().rb_params_init(ctypes.byref(p)))
     p.alpha_num, p.alpha_den = alpha_rational(alpha)
@@ -154,6 +168,10 @@ def make_params(alpha=(1, 200), flags=0, stream=None, row0=0, nrows=-1, linkage=
     p.stream = stream
     p.row0 = row0
     p.nrows = nrows
+    for k, v in (tuning or {}).items():
+        if k not in TUNING_FIELDS:
+            raise KeyError(f"unknown tuning field {k!r}")
+        setattr(p, k, v)
     return p
 
 
@@ -372,7 +390,7 @@ def _stream_ptr(stream):
 
 
 def build_index(ids, lens=None, *, alpha=(1, 200), flags=0, row0=0, nrows=-1, stream=None,
-                workspace: Workspace | None = None, linkage=RB_LINK_COMPLETE):
+                workspace: Workspace | None = None, linkage=RB_LINK_COMPLETE, tuning: dict | None = None):
     """Build the context index from device ids (torch.int32/uint32 CUDA tensor [N, K]).
 
     Returns (Index, Workspace); workspace.rows holds the distance rows (unless
@@ -384,7 +402,7 @@ def build_index(ids, lens=None, *, alpha=(1, 200), flags=0, row0=0, nrows=-1, st
         raise TypeError("ids must be int32/uint32 (bit pattern of uint32 DocIds)")
     ids = ids.contiguous()
     N, K = ids.shape
-    p = make_params(alpha, flags, _stream_ptr(stream), row0, nrows, linkage)
+    p = make_params(alpha, flags, _stream_ptr(stream), row0, nrows, linkage, tuning)
     ws = workspace or Workspace(N, K, p, device=ids.device)
     if lens is not None:
         lens = lens.contiguous()
@@ -399,11 +417,11 @@ def build_index(ids, lens=None, *, alpha=(1, 200), flags=0, row0=0, nrows=-1, st
 
 
 def build_index_host(ids, lens=None, *, alpha=(1, 200), flags=0, stream=None,
-                     workspace: Workspace | None = None, linkage=RB_LINK_COMPLETE):
+                     workspace: Workspace | None = None, linkage=RB_LINK_COMPLETE, tuning: dict | None = None):
     """End-to-end entry: ids/lens are host numpy arrays; H2D happens inside."""
     ids = np.ascontiguousarray(ids, dtype=np.uint32)
     N, K = ids.shape
-    p = make_params(alpha, flags, _stream_ptr(stream), linkage=linkage)
+    p = make_params(alpha, flags, _stream_ptr(stream), linkage=linkage, tuning=tuning)
     ws = workspace or Workspace(N, K, p)
     lens_a = None if lens is None else np.ascontiguousarray(lens, dtype=np.uint8)
     out = ctypes.c_void_p()
@@ -496,12 +514,11 @@ class DistBuilder:
             _lib.rb_dist_free(h)
             self._h = None
 
-    def build(self, ids, lens=None, *, alpha=(1, 200), flags=0, stream=None) -> Index:
-        import torch
+    def build(self, ids, lens=None, *, alpha=(1, 200), flags=0, stream=None, tuning: dict | None = None) -> Index:
         ids = ids.contiguous()
         N, K = ids.shape
         assert (N, K) == (self.N, self.K)
-        p = make_params(alpha, flags, _stream_ptr(stream))
+        p = make_params(alpha, flags, _stream_ptr(stream), tuning=tuning)
         out = ctypes.c_void_p()
         _check(lib().rb_build_index_dist(self._h, ctypes.c_void_p(ids.data_ptr()),
                                          None if lens is None else ctypes.c_void_p(lens.contiguous().data_ptr()),

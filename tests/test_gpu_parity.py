@@ -39,12 +39,17 @@ def oracle_linkage_tree(ids, lens, d_full):
     return Z, t, ordered, plen, o.schedule(t.path)
 
 
-def check_full(ids, lens=None, alpha=(1, 200), counts=True):
+def check_full(ids, lens=None, alpha=(1, 200), counts=True, tuning=None, dref=None):
+    """Every distance row, (s, D) rows, row NN, merge order, paths, ordered
+    contexts, prefix lengths and schedule vs the oracle; returns the index."""
     N, K = ids.shape
     flags = F.RB_KEEP_ROWS | (F.RB_EMIT_COUNTS if counts else 0)
-    idx, ws = dev_build(ids, lens, flags=flags, alpha=alpha)
+    idx, ws = dev_build(ids, lens, flags=flags, alpha=alpha, tuning=tuning)
     rows = ws.rows.cpu().numpy()
-    dref, sref, Dref = oc.pairwise_rows(ids, lens, alpha[0], alpha[1], counts=True)
+    if counts:
+        dref, sref, Dref = oc.pairwise_rows(ids, lens, alpha[0], alpha[1], counts=True)
+    elif dref is None:
+        dref = oc.pairwise_rows(ids, lens, alpha[0], alpha[1])
     if counts:
         assert np.array_equal(ws.s.cpu().numpy(), sref)
         assert np.array_equal(ws.D.cpu().numpy().view(np.uint16), Dref)
@@ -250,25 +255,66 @@ def test_full_size_configs(name):
     assert np.array_equal(idx2.order_contexts()[0], out)
 
 
-@pytest.mark.parametrize("codes", ["0", "1"])
-@pytest.mark.parametrize("mode", ["0", "1"])
+# ------------------------------------- the paths full-size builds take, vs the oracle
+# Inputs that reach, at sizes the oracle still finishes in about a minute, the
+# kernel variants C3/C4 run: level cliques on more than 4096 vertices (block
+# path), the 1024-thread row gather (M > 16K) and the 1024-thread window
+# compaction (M' > 20K; fp32 matrices, or codes with the gather off).  The
+# path bits of rb_stats prove each case reaches its path.
+BIG = {
+    "block10k": ((10000, 3, 100000, 5), None, F.RB_PATH_CLIQUE_BLOCK),
+    "gather20k": ((20000, 3, 100000, 43), None, F.RB_PATH_CLIQUE_BLOCK | F.RB_PATH_GATHER_WIDE),
+    "window24k_fp32": ((24000, 3, 100000, 45), dict(value_codes=0), F.RB_PATH_WINDOW_WIDE),
+    "window24k_codes": ((24000, 3, 100000, 45), dict(gather=0), F.RB_PATH_WINDOW_WIDE),
+    "ties20k_K4": ((20000, 4, 2000, 41), None, F.RB_PATH_GATHER_WIDE),
+}
+
+
+@pytest.mark.parametrize("case", list(BIG))
+def test_full_size_paths_vs_oracle(case):
+    (N, K, V, seed), tu, bits = BIG[case]
+    w = generate(N, K, V, seed)
+    idx = check_full(w.ids, counts=False, tuning=tu)
+    st = idx.stats()
+    assert st["paths"] & bits == bits, (case, hex(st["paths"]), st["max_level"])
+
+
+def test_C3_full_vs_oracle():
+    """C3 (N = 32,768, K = 15, 5-turn sessions) end to end against the oracle:
+    all 1.07e9 distances, row NN, merge order (C NN-chain over the oracle's
+    own rows), paths, document order and schedule (Python oracle tree); then
+    the bench launch configuration (rows consumed by the linkage) gives the
+    same merge order and document order."""
+    w = config("C3")
+    dref = oc.pairwise_rows(w.ids, None, 1, 200)
+    idx = check_full(w.ids, counts=False, dref=dref)
+    del dref
+    ref_link, ref_order = idx.linkage(), idx.order_contexts()
+    idx2, ws = dev_build(w.ids, flags=0)
+    for x, y in zip(ref_link + ref_order, idx2.linkage() + idx2.order_contexts()):
+        assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("codes", [0, -1])
+@pytest.mark.parametrize("mode", [0, 1])
 @pytest.mark.parametrize("case", ["C2", "var", "ties"])
-def test_round_strategy(mode, case, codes, monkeypatch):
-    """Linkage rounds in place (RAGB_INPLACE=1, forced wherever allowed) or
-    always compacting (0), on fp32 matrices (RAGB_CODES=0) or on 16-bit value
-    codes (default where the Eq. 1 table exists), give the oracle's merge order
-    (the strategy and the stored form are implementation choices, X7-X9 fix
-    the result)."""
-    monkeypatch.setenv("RAGB_INPLACE", mode)
-    monkeypatch.setenv("RAGB_CODES", codes)
+def test_round_strategy(mode, case, codes):
+    """Linkage rounds in place (inplace=1, forced wherever allowed) or always
+    compacting (0), on fp32 matrices (value_codes=0) or on 16-bit value codes
+    (default where the Eq. 1 table exists), give the oracle's merge order (the
+    strategy and the stored form are implementation choices, X7-X9 fix the
+    result)."""
+    tu = dict(inplace=mode, value_codes=codes)
     if case == "C2":
-        check_full(config("C2").ids, counts=False)
+        idx = check_full(config("C2").ids, counts=False, tuning=tu)
     elif case == "var":
         w = generate(2500, 12, 6000, 31, len_min=2)
-        check_full(w.ids, w.lens, counts=False)
+        idx = check_full(w.ids, w.lens, counts=False, tuning=tu)
     else:  # tie-heavy: tiny pool, short lists -> many equal heights and cliques
         w = generate(3000, 4, 300, 32)
-        check_full(w.ids, counts=False)
+        idx = check_full(w.ids, counts=False, tuning=tu)
+    if mode == 1:
+        assert idx.stats()["paths"] & F.RB_PATH_INPLACE
 
 
 @pytest.mark.parametrize("K", [7, 22, 23, 30, 32])
@@ -294,27 +340,24 @@ def test_wide_lists(K):
 
 
 @pytest.mark.parametrize("case", ["C2", "odd"])
-def test_code_window_compaction(case, monkeypatch):
+def test_code_window_compaction(case):
     """Code-mode compaction through the shared-memory window kernel
-    (RAGB_GATHER=0; the path for matrices too wide for the gather kernel)
-    gives the oracle's merge order, also for an odd N (scalar loads)."""
-    monkeypatch.setenv("RAGB_GATHER", "0")
-    monkeypatch.setenv("RAGB_CODES", "1")
+    (gather=0; the path for matrices too wide for the gather kernel) gives the
+    oracle's merge order, also for an odd N (scalar loads)."""
     ids = config("C2").ids if case == "C2" else generate(1029, 8, 3087, 1129).ids
-    check_full(ids, counts=False)
+    idx = check_full(ids, counts=False, tuning=dict(gather=0))
+    assert idx.stats()["paths"] & F.RB_PATH_WINDOW
 
 
-def test_round_strategy_full_size(monkeypatch):
+def test_round_strategy_full_size():
     """At C4 size (level cliques above 4096 vertices, block path) the merge
     order and the document order do not depend on the round strategy nor on
     the stored form of the matrices (fp32 values or 16-bit value codes)."""
     ids = config("C4").ids
     t = torch.from_numpy(ids.view(np.int32)).cuda()
     res = []
-    for mode, codes in (("0", "1"), ("2", "1"), ("2", "0")):
-        monkeypatch.setenv("RAGB_INPLACE", mode)
-        monkeypatch.setenv("RAGB_CODES", codes)
-        idx, ws = F.build_index(t)
+    for mode, codes in ((0, -1), (-1, -1), (-1, 0)):
+        idx, ws = F.build_index(t, tuning=dict(inplace=mode, value_codes=codes))
         res.append((idx.linkage(), idx.order_contexts()))
         del idx, ws
         torch.cuda.empty_cache()
@@ -386,15 +429,15 @@ def test_intersection_variable_lengths_and_consumed_rows():
     check_intersection(w.ids, w.lens, flags=0)
 
 
-def _dist_vs_single(ids, lens, world):
+def _dist_vs_single(ids, lens, world, tuning=None):
     t = torch.from_numpy(np.ascontiguousarray(ids).view(np.int32)).cuda()
     tl = None if lens is None else torch.from_numpy(np.ascontiguousarray(lens, dtype=np.uint8)).cuda()
     db = F.DistBuilder(world, ids.shape[0], ids.shape[1], local=True)
-    di = db.build(t, tl)
+    di = db.build(t, tl, tuning=tuning)
     res_d = (di.linkage(), di.nn(), di.order_contexts(), di.paths())
     del db, di
     torch.cuda.empty_cache()
-    si, ws = F.build_index(t, tl)
+    si, ws = F.build_index(t, tl, tuning=tuning)
     res_s = (si.linkage(), si.nn(), si.order_contexts(), si.paths())
     del si, ws
     torch.cuda.empty_cache()
@@ -416,13 +459,13 @@ def test_row_sharded_build_matches_single_gpu(world):
 
 
 @pytest.mark.parametrize("world", [2, 3])
-def test_row_sharded_fp32_matrices(world, monkeypatch):
-    """The sharded rounds on fp32 matrices (RAGB_CODES=0; the code-mode rounds
+def test_row_sharded_fp32_matrices(world):
+    """The sharded rounds on fp32 matrices (value_codes=0; the code-mode rounds
     are the default for uniform K <= 32) give the same index."""
-    monkeypatch.setenv("RAGB_CODES", "0")
-    _dist_vs_single(config("C2").ids, None, world)
+    tu = dict(value_codes=0)
+    _dist_vs_single(config("C2").ids, None, world, tu)
     w = generate(1500, 4, 200, 78)
-    _dist_vs_single(w.ids, None, world)
+    _dist_vs_single(w.ids, None, world, tu)
 
 
 def test_row_sharded_tiny_and_vs_oracle():

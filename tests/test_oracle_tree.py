@@ -136,3 +136,19 @@ def test_single_context():
     assert t.path == [[0]]
     ordered, plen = o.offline_order([[5, 6]], t)
     assert ordered == [[5, 6]] and plen == [0]
+
+
+def test_deep_collapsed_caterpillar():
+    """All-disjoint contexts merged as one caterpillar (0 absorbs 1, 2, ...):
+    every virtual node's set is the empty set = the root's, so all N-1 virtual
+    nodes collapse (X11) and every leaf hangs off the root in rep order (X12)
+    with path [i] and its original order.  N = 5000 nests deeper
+    than Python's default recursion limit."""
+    N = 5000
+    ctxs = o.validate(edge("disjoint", N, 3).ids, None)
+    Z = [(0, i, 1.0, i + 1) for i in range(1, N)]
+    t = o.build_tree(ctxs, Z)
+    assert t.path == [[i] for i in range(N)]
+    ordered, plen = o.offline_order(ctxs, t)
+    assert ordered == [list(c) for c in ctxs] and plen == [0] * N
+    assert o.schedule(t.path) == list(range(N))
