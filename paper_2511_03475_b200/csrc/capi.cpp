@@ -102,6 +102,7 @@ ScratchLayout ScratchLayout::make(int64_t N, int32_t K, bool keep_rows, bool lin
     L.lut = take(o, (size_t)std::max<int64_t>(entries, 1) * 4);
     L.lutc = take(o, (size_t)std::max<int64_t>(entries, 1) * 4);
     L.vals = take(o, (size_t)std::max<int64_t>(entries, 1) * 4);
+    L.ptab = take(o, (size_t)tile_ptab_entries(K) * 8);
   }
   if (linkage && N > 1) {
     L.key0 = L.nnkey;
@@ -298,18 +299,23 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
                                    &launches),
               "eq1 table");
       da.lut = lut;
-      if (code_mode) {
+      if (ragb::tile_path_ok(K, lens_d == nullptr)) {
+        // the tile kernel's packed table carries the order-preserving codes
+        // (its row minimum runs on them); code mode also stores them
         uint32_t *lutc = reinterpret_cast<uint32_t *>(sc + L.lutc);
         float *vals = reinterpret_cast<float *>(sc + L.vals);
         int *ncode = reinterpret_cast<int *>(sc + L.err + 16);
         RB_CUDA(ragb::launch_code_table(lut, K, stride, entries, lutc, vals, ncode, st, &launches), "code table");
         da.lutc = lutc;
         da.vals = vals;
-        da.codes = reinterpret_cast<uint16_t *>(sc + L.codes);
-        cm.codes = da.codes;
-        cm.mat16 = reinterpret_cast<uint16_t *>(sc + L.mat16);
-        cm.vals = vals;
-        cm.ncode = ncode;
+        da.ptab = reinterpret_cast<const uint2 *>(sc + L.ptab);
+        if (code_mode) {
+          da.codes = reinterpret_cast<uint16_t *>(sc + L.codes);
+          cm.codes = da.codes;
+          cm.mat16 = reinterpret_cast<uint16_t *>(sc + L.mat16);
+          cm.vals = vals;
+          cm.ncode = ncode;
+        }
       }
     }
   }

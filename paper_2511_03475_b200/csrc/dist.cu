@@ -47,7 +47,7 @@ size_t take(size_t &o, size_t bytes) {
 }
 
 struct DistLayout {
-  size_t err, counters, table, idsT, lut, lutc, vals, key0, key1, rep0, rep1, sz0, sz1, leader, aux0, aux1, aux2, aux3,
+  size_t err, counters, table, idsT, lut, lutc, vals, ptab, key0, key1, rep0, rep1, sz0, sz1, leader, aux0, aux1, aux2, aux3,
       aux4, alive, za, zb, zh, zs, adj, matA, matB, total;
   int64_t S0;  // rows per rank of the distance matrix
   static DistLayout make(int64_t N, int32_t K, int world) {
@@ -65,6 +65,7 @@ struct DistLayout {
       L.lut = take(o, (size_t)std::max<int64_t>(entries, 1) * 4);
       L.lutc = take(o, (size_t)std::max<int64_t>(entries, 1) * 4);
       L.vals = take(o, (size_t)std::max<int64_t>(entries, 1) * 4);
+      L.ptab = take(o, (size_t)tile_ptab_entries(K) * 8);
     }
     L.key0 = take(o, (size_t)(N + world) * 8);
     L.key1 = take(o, (size_t)(N + world) * 8);
@@ -460,13 +461,14 @@ rb_status build_index_dist(rb_dist *d, const uint32_t *ids_d, const uint8_t *len
       DC(launch_eq1_lut(at<float>(sc, L.lut), K, stride, entries, p->alpha_num, p->alpha_den, st, &launches),
          "eq1 table");
       da.lut = at<float>(sc, L.lut);
-      if (codes) {
+      if (tile_path_ok(K, lens_d == nullptr)) {
         DC(launch_code_table(da.lut, K, stride, entries, at<uint32_t>(sc, L.lutc), at<float>(sc, L.vals),
                              at<int>(sc, L.err + 16), st, &launches),
            "code table");
         da.lutc = at<uint32_t>(sc, L.lutc);
         da.vals = at<float>(sc, L.vals);
-        da.codes = at<uint16_t>(sc, L.matB);
+        da.ptab = at<const uint2>(sc, L.ptab);
+        if (codes) da.codes = at<uint16_t>(sc, L.matB);
       }
     }
     if (da.nrows > 0) DC(launch_distance(da, st, &launches), "distance kernel");

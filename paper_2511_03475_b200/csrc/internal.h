@@ -35,6 +35,7 @@ struct ScratchLayout {
       alive, za, zb, zh, zs, amask, mlist, counters, matA, matB, total;
   size_t pmap;         // code mode: int2 [N + 8] new column -> (leader, pair member)
   size_t codes, mat16;  // code mode (inside matA): [N][N] codes, then the first compacted code matrix
+  size_t ptab;          // tile path: packed Eq. 1 table (value, code << 16) [(K+1) * (K*K/2+1)]
   static ScratchLayout make(int64_t N, int32_t K, bool keep_rows, bool linkage);
 };
 
@@ -70,6 +71,7 @@ struct DistArgs {
   const uint32_t *lutc;       // [lut entries] or nullptr
   const float *vals;          // [ncode] ascending distinct table values
   uint16_t *codes;            // [nrows][N] or nullptr
+  const uint2 *ptab = nullptr;  // tile path: packed (value bits, code << 16) table, filled by the launch
   int grid_cap = 0;           // Tuning::dist_grid
   bool long_lists = true;     // Tuning::long_lists != 0
 };
@@ -101,6 +103,7 @@ cudaError_t launch_eq1_lut(float *lut, int32_t K, int stride, int64_t entries, u
 bool tile_path_ok(int32_t K, bool uniform);
 int tile_lut_shift(int32_t K);
 int64_t tile_lut_entries(int32_t K);
+int64_t tile_ptab_entries(int32_t K);
 cudaError_t launch_distance_tile(const DistArgs &a, cudaStream_t st);
 // Long lists (distance_wide.cu): uniform contexts with 32 < K <= 128.
 bool wide_path_ok(int32_t K, bool uniform);
