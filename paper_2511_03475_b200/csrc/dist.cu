@@ -84,7 +84,8 @@ struct DistLayout {
     L.zb = take(o, (size_t)N * 4);
     L.zh = take(o, (size_t)N * 4);
     L.zs = take(o, (size_t)N * 4);
-    L.adj = take(o, (size_t)N * (size_t)((N + 31) / 32) * 4);  // level adjacency (n x ceil(n/32) words)
+    // level adjacency (n x ceil(n/32) words), then the sweep's candidate sets and arrays (linkage_kernels.cuh)
+    L.adj = take(o, (2 * (size_t)N * (size_t)((N + 31) / 32) + 6 * (size_t)N) * 4);
     const size_t mat = (size_t)L.S0 * (size_t)((N + 3) & ~3ll) * 4;
     L.matA = take(o, mat);
     L.matB = take(o, mat);
@@ -610,7 +611,7 @@ rb_status build_index_dist(rb_dist *d, const uint32_t *ids_d, const uint8_t *len
       k_adj_gather<<<sms * 4, 256, 0, st>>>(pa[l], at<uint32_t>(sc, L.adj),
                                             reinterpret_cast<const uint32_t *const *>(table(r, TADJ)), world, r, S);
       const size_t m1 = std::min<size_t>((size_t)M, 1024);
-      const size_t smem = std::max(2 * (size_t)((M + 31) / 32), m1 * ((m1 + 31) / 32)) * 4;
+      const size_t smem = m1 * ((m1 + 31) / 32) * 4;  // the staged adjacency of levels <= 1024
       if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_level_cliques, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       k_level_cliques<<<1, CT, smem, st>>>(pa[l], at<uint32_t>(sc, L.adj));

@@ -256,7 +256,7 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
       k_level_adj<float><<<sms * 4, 256, 0, st>>>(pa, adj);
     {
       const size_t m1 = std::min<size_t>((size_t)M, 1024);
-      const size_t smem = std::max(2 * (size_t)((M + 31) / 32), m1 * ((m1 + 31) / 32)) * 4;
+      const size_t smem = m1 * ((m1 + 31) / 32) * 4;  // the staged adjacency of levels <= 1024
       if (smem > 48 * 1024)
         occupancy_cached(k_level_cliques, CT, smem);
       k_level_cliques<<<1, CT, smem, st>>>(pa, adj);

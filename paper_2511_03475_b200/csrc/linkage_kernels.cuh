@@ -356,63 +356,299 @@ __device__ int cliques_warp(const PrepArgs &a, const uint32_t *adj, int n, int W
 constexpr int kWarpCliqueMaxN = 32 * 32 * 4;
 
 constexpr int CT = 512;  // threads of k_level_cliques (128 registers for the pick chain)
+
+// Levels of more than kWarpCliqueMaxN vertices (C4's h = 1.0 level: 16,082
+// vertices, ~2,150 cliques, 13,927 merges): the greedy clique sequence as a
+// sweep over the vertices.  Reformulation: in the greedy
+// process a vertex v is offered to the cliques in creation order and joins
+// the first one whose members (all smaller than v) are all adjacent to it;
+// if none takes it, v starts the next clique.  Clique j's candidate set
+// I_j = AND of its members' adjacency rows is kept, for the words after the
+// current block, in global memory (reductions with AND); a block of 128
+// vertices is decided by one warp from the candidate masks of the cliques
+// that have candidates in it (a chain per clique: the smallest undecided
+// candidate, then the smallest one adjacent to it, ...), then new cliques
+// start among the vertices still undecided.  The decisions are emitted in
+// greedy order (clique, then vertex) by a counting sort.
+constexpr int kSweepB = 128;      // vertices per block (4 words)
+constexpr int kSweepCap = 1024;   // cliques with candidates examined per pass
+
+__device__ __forceinline__ uint4 and4(uint4 x, uint4 y) { return make_uint4(x.x & y.x, x.y & y.y, x.z & y.z, x.w & y.w); }
+__device__ __forceinline__ bool any4(uint4 x) { return (x.x | x.y | x.z | x.w) != 0u; }
+__device__ __forceinline__ int ffs4(uint4 x) {  // first set bit (0..127), x != 0
+  return x.x ? __ffs(x.x) - 1 : x.y ? 31 + __ffs(x.y) : x.z ? 63 + __ffs(x.z) : 95 + __ffs(x.w);
+}
+__device__ __forceinline__ uint4 above4(int p) {  // bits > p of a 128-bit mask
+  const uint32_t m[4] = {p < 0 ? ~0u : (p < 31 ? ~0u << (p + 1) : 0u),
+                         p < 32 ? ~0u : (p < 63 ? ~0u << (p - 31) : 0u),
+                         p < 64 ? ~0u : (p < 95 ? ~0u << (p - 63) : 0u),
+                         p < 96 ? ~0u : (p < 127 ? ~0u << (p - 95) : 0u)};
+  return make_uint4(m[0], m[1], m[2], m[3]);
+}
+__device__ __forceinline__ uint4 clear4(uint4 x, int p) {
+  const uint32_t b = ~(1u << (p & 31));
+  const int q = p >> 5;
+  return make_uint4(q == 0 ? x.x & b : x.x, q == 1 ? x.y & b : x.y, q == 2 ? x.z & b : x.z, q == 3 ? x.w & b : x.w);
+}
+
+// Returns the number of merges; seq / seqs (greedy order) as the other paths.
+__device__ int cliques_sweep(const PrepArgs &a, const uint32_t *__restrict__ adj, int n, int W, int *seq, int *seqs) {
+  __shared__ uint4 s_adjB[kSweepB];    // block adjacency: row v0 + i, words [wb, wb + 4)
+  __shared__ uint4 s_lm[kSweepCap];    // candidate masks of the listed cliques
+  __shared__ int s_lj[kSweepCap];      // their clique ids (ascending)
+  __shared__ int s_bj[kSweepB], s_bv[kSweepB];  // this block's decisions (clique, vertex), new starts marked
+  __shared__ int s_wcnt[CT / 32];
+  __shared__ int s_J, s_nd, s_nb, s_nl, s_done;
+  __shared__ uint4 s_und;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  // work area after the adjacency (n x W words): I [n][W], then per-decision and per-clique arrays
+  const int WI = (W + 3) & ~3;  // I row stride: 16-byte rows (4-word block loads)
+  uint32_t *I = const_cast<uint32_t *>(adj) + (((size_t)n * W + 3) & ~(size_t)3);
+  int *dec_j = reinterpret_cast<int *>(I + (size_t)n * WI);  // [n] clique of decision d (sweep order)
+  int *dec_v = dec_j + n;                                    // [n] its vertex
+  int *dec_r = dec_v + n;                                    // [n] rank within the clique
+  int *cstart = dec_r + n;                                   // [n] start vertex of clique j
+  int *ccnt = cstart + n;                                    // [n + 1] merges per clique, then offsets
+  if (tid == 0) {
+    s_J = 0;
+    s_nd = 0;
+  }
+  __syncthreads();
+  long long tk[6] = {0, 0, 0, 0, 0, 0};
+  long long nlist = 0;
+  long long c0 = clock64();
+  for (int v0 = 0; v0 < n; v0 += kSweepB) {
+    const int wb = v0 >> 5;
+    // -- block adjacency and the undecided set ----------------------------------
+    if (tid < kSweepB) {
+      const int v = v0 + tid;
+      uint32_t w4[4] = {0u, 0u, 0u, 0u};
+      if (v < n) {
+        const uint32_t *r = adj + (size_t)v * W + wb;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) w4[q] = wb + q < W ? __ldg(r + q) : 0u;
+      }
+      s_adjB[tid] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+    }
+    if (tid == 0) {
+      const int nv = min(kSweepB, n - v0);
+      s_und = above4(-1);
+      if (nv < kSweepB) s_und = and4(s_und, make_uint4(nv >= 32 ? ~0u : (1u << nv) - 1u, nv >= 64 ? ~0u : nv > 32 ? (1u << (nv - 32)) - 1u : 0u,
+                                                       nv >= 96 ? ~0u : nv > 64 ? (1u << (nv - 64)) - 1u : 0u,
+                                                       nv > 96 ? (1u << (nv - 96)) - 1u : 0u));
+      s_nb = 0;
+      s_done = 0;
+    }
+    __syncthreads();
+    { const long long c1 = clock64(); tk[0] += c1 - c0; c0 = c1; }
+    const int J0 = s_J;
+    // -- existing cliques, in creation order, that have candidates here ---------
+    for (int j0 = 0; j0 < J0 && !s_done; j0 += kSweepCap) {
+      const uint4 und = s_und;
+      const int j = j0 + tid * 2;  // two cliques per thread (kSweepCap = 2 x CT)
+      uint4 m0 = make_uint4(0u, 0u, 0u, 0u), m1 = m0;
+      if (j < J0) m0 = and4(__ldcg(reinterpret_cast<const uint4 *>(I + (size_t)j * WI + wb)), und);
+      if (j + 1 < J0) m1 = and4(__ldcg(reinterpret_cast<const uint4 *>(I + (size_t)(j + 1) * WI + wb)), und);
+      const int c = (any4(m0) ? 1 : 0) + (any4(m1) ? 1 : 0);
+      const int pos = block_excl_scan<CT>(c, s_wcnt);
+      if (any4(m0)) {
+        s_lj[pos] = j;
+        s_lm[pos] = m0;
+      }
+      if (any4(m1)) {
+        s_lj[pos + (any4(m0) ? 1 : 0)] = j + 1;
+        s_lm[pos + (any4(m0) ? 1 : 0)] = m1;
+      }
+      if (tid == CT - 1) s_nl = pos + c;
+      __syncthreads();
+      { const long long c1 = clock64(); tk[1] += c1 - c0; c0 = c1; }
+      nlist += s_nl;
+      if (wid == 0) {  // the listed cliques take their chains, in order; 32 at a time
+        uint4 u = s_und;
+        int nb = s_nb;
+        const int nl = s_nl;
+        for (int g = 0; g < nl && any4(u); g += 32) {
+          const int t = g + lane;
+          uint4 m = t < nl ? s_lm[t] : make_uint4(0u, 0u, 0u, 0u);
+          while (true) {
+            // the first clique of the group that still has an undecided candidate
+            const uint32_t b = __ballot_sync(0xffffffffu, any4(and4(m, u)));
+            if (b == 0u) break;
+            const int L = __ffs(b) - 1;
+            if (lane == L) {
+              uint4 cm = and4(m, u);
+              const int j = s_lj[t];
+              while (any4(cm)) {
+                const int p = ffs4(cm);
+                s_bj[nb] = j;
+                s_bv[nb] = p;
+                ++nb;
+                u = clear4(u, p);
+                cm = and4(and4(cm, s_adjB[p]), above4(p));
+              }
+            }
+            u.x = __shfl_sync(0xffffffffu, u.x, L);
+            u.y = __shfl_sync(0xffffffffu, u.y, L);
+            u.z = __shfl_sync(0xffffffffu, u.z, L);
+            u.w = __shfl_sync(0xffffffffu, u.w, L);
+            nb = __shfl_sync(0xffffffffu, nb, L);
+            if (lane <= L) m = make_uint4(0u, 0u, 0u, 0u);
+          }
+        }
+        if (lane == 0) {
+          s_und = u;
+          s_nb = nb;
+          s_done = any4(u) ? 0 : 1;
+        }
+      }
+      __syncthreads();
+      { const long long c1 = clock64(); tk[2] += c1 - c0; c0 = c1; }
+    }
+    // -- new cliques among the vertices still undecided --------------------------
+    const int nb_join = s_nb;  // decisions [0, nb_join) join existing cliques
+    if (tid == 0) {
+      uint4 u = s_und;
+      int nb = s_nb, J = s_J;
+      while (any4(u)) {
+        const int p = ffs4(u);
+        u = clear4(u, p);
+        cstart[J] = v0 + p;
+        s_bj[nb] = J;
+        s_bv[nb] = p | 0x10000;  // start of clique J (not a merge)
+        ++nb;
+        uint4 cm = and4(and4(u, s_adjB[p]), above4(p));
+        while (any4(cm)) {
+          const int q = ffs4(cm);
+          s_bj[nb] = J;
+          s_bv[nb] = q;
+          ++nb;
+          u = clear4(u, q);
+          cm = and4(and4(cm, s_adjB[q]), above4(q));
+        }
+        ++J;
+      }
+      s_J = J;
+      s_nb = nb;
+    }
+    __syncthreads();
+    { const long long c1 = clock64(); tk[3] += c1 - c0; c0 = c1; }
+    const int nb = s_nb;
+    // -- record the merges; eager candidate sets for the words after the block ----
+    const int wn = wb + 4;  // first word after the block
+    const int nw = W - wn;
+    {  // decision t of the block -> global arrays, rank within its clique
+      const int nd0 = s_nd;
+      if (tid < nb) {
+        const int j = s_bj[tid];
+        const bool start = (s_bv[tid] & 0x10000) != 0;
+        int before = 0, dbefore = 0, last = 1;  // same-clique merges before t in this block
+        for (int t2 = 0; t2 < nb; ++t2) {
+          const bool sm = s_bj[t2] == j && !(s_bv[t2] & 0x10000);
+          before += (t2 < tid && sm) ? 1 : 0;
+          last &= (t2 > tid && sm) ? 0 : 1;
+        }
+        for (int t2 = 0; t2 < tid; ++t2) dbefore += (s_bv[t2] & 0x10000) ? 0 : 1;
+        const bool fresh = j >= J0;  // created in this block: no earlier merges
+        const int old = fresh ? 0 : ccnt[j];
+        if (!start) {
+          const int d = nd0 + dbefore;
+          dec_j[d] = j;
+          dec_v[d] = v0 + s_bv[tid];
+          dec_r[d] = old + before;
+          if (last) ccnt[j] = old + before + 1;
+        } else if (last) {  // a start with no merges in this block
+          ccnt[j] = 0;
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        int c = 0;
+        for (int t = 0; t < nb; ++t) c += (s_bv[t] & 0x10000) ? 0 : 1;
+        s_nd = nd0 + c;
+      }
+    }
+    if (nw > 0) {
+      // one warp per decision, 4 words per lane (16-byte loads of the row)
+      const int wn4 = wb + 4;  // == wn, a multiple of 4: I rows are 16-byte aligned there
+      // new cliques: I_J = the start's row (plain stores), then every member ANDs
+      for (int t = nb_join + wid; t < nb; t += CT / 32) {
+        if (!(s_bv[t] & 0x10000)) continue;
+        const uint32_t *src = adj + (size_t)(v0 + (s_bv[t] & 0xffff)) * W;
+        uint32_t *dst = I + (size_t)s_bj[t] * WI;
+        for (int w = wn4 + 4 * lane; w < W; w += 128)
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (w + q < W) dst[w + q] = __ldg(src + w + q);
+      }
+      __syncthreads();
+      for (int t = wid; t < nb; t += CT / 32) {
+        if (s_bv[t] & 0x10000) continue;
+        const uint32_t *src = adj + (size_t)(v0 + s_bv[t]) * W;
+        uint32_t *dst = I + (size_t)s_bj[t] * WI;
+        for (int w = wn4 + 4 * lane; w < W; w += 128) {
+          uint32_t x[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) x[q] = w + q < W ? __ldg(src + w + q) : 0xffffffffu;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (w + q < W && x[q] != 0xffffffffu) atomicAnd(dst + w + q, x[q]);
+        }
+      }
+    }
+    __threadfence();  // the reductions are at L2 before the next block reads I (ld.cg)
+    __syncthreads();
+    { const long long c1 = clock64(); tk[4] += c1 - c0; c0 = c1; }
+  }
+  if (tid == 0 && a.cstat) {
+    a.cstat[0] = s_J;
+    a.cstat[1] = (int)nlist;
+    a.cstat[2] = (int)(tk[0] >> 10);
+    a.cstat[3] = (int)(tk[1] >> 10);
+    a.cstat[5] = (int)(tk[2] >> 10);
+    a.cstat[6] = (int)(tk[3] >> 10);
+    a.cstat[7] = (int)(tk[4] >> 10);
+  }
+  // -- greedy order: counting sort of the decisions by clique --------------------
+  const int J = s_J, nd = s_nd;
+  __syncthreads();
+  {
+    __shared__ int s_carry;
+    if (tid == 0) s_carry = 0;
+    __syncthreads();
+    for (int j0 = 0; j0 < J; j0 += CT) {
+      const int j = j0 + tid;
+      const int c = j < J ? ccnt[j] : 0;
+      const int pre = block_excl_scan<CT>(c, s_wcnt);
+      const int carry = s_carry;
+      if (j < J) ccnt[j] = carry + pre;  // offsets
+      __syncthreads();
+      if (tid == CT - 1) s_carry = carry + pre + c;
+      __syncthreads();
+    }
+  }
+  for (int d = tid; d < nd; d += CT) {
+    const int j = dec_j[d];
+    const int pos = ccnt[j] + dec_r[d];
+    seq[pos] = dec_v[d];
+    seqs[pos] = cstart[j];
+  }
+  __syncthreads();
+  return nd;
+}
+
 __global__ void __launch_bounds__(CT, 1) k_level_cliques(PrepArgs a,
                                                          const uint32_t *__restrict__ adj) {
-  extern __shared__ uint32_t bits[];  // [2][W]: alive, candidates
-  __shared__ int s_p[64];     // next candidates (list positions), ascending
-  __shared__ int s_pick[32];  // picks of the batch (list positions)
-  __shared__ uint32_t s_m[32];  // candidate r: bit j set <=> p_j adjacent to p_r (j < r)
-  __shared__ int s_wsum[CT / 32];
-  __shared__ int s_npick, s_last, s_nseq;
+  extern __shared__ __align__(16) uint32_t bits[];  // staged adjacency of levels <= 1024
+  __shared__ int s_p[64];     // next candidates (list positions), ascending (warp paths)
+  __shared__ int s_nseq;
   __shared__ int s_sv[CT / 32], s_sf[CT / 32];
   const int n = a.level[0];
   if (n < 2) return;
   const float hf = a.vals ? a.vals[a.level[1]] : __uint_as_float((unsigned)a.level[1]);
   const int W = (n + 31) >> 5;
-  uint32_t *A = bits, *C = bits + W;
   int *seq = a.candA, *seqs = a.candB;  // pick list position, its clique's start position
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  for (int w = tid; w < W; w += CT) {
-    const int rem = n - w * 32;
-    A[w] = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
-  }
-  __syncthreads();
-  // C[w] = f(w) for w >= w0 (every such word), and the first <= 32 set bits
-  // of C from w0 on -> s_p (ascending); returns their total count (uniform)
-  auto pass_collect = [&](int w0, auto f) {
-    int got = 0;
-    for (int wb = w0; wb < W; wb += CT) {
-      const int w = wb + tid;
-      uint32_t x = w < W ? f(w) : 0u;
-      if (w < W) C[w] = x;
-      const int cnt = __popc(x);
-      int incl = cnt;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        incl += lane >= o ? y : 0;
-      }
-      if (lane == 31) s_wsum[wid] = incl;
-      __syncthreads();
-      int before = 0, tot = 0;
-#pragma unroll
-      for (int q = 0; q < CT / 32; ++q) {
-        const int v = s_wsum[q];
-        before += q < wid ? v : 0;
-        tot += v;
-      }
-      int slot = got + before + incl - cnt;
-      while (x != 0u && slot < 32) {
-        s_p[slot++] = w * 32 + __ffs(x) - 1;
-        x &= x - 1u;
-      }
-      got += tot;
-      __syncthreads();  // s_p complete; s_wsum reusable
-    }
-    return got;
-  };
-  int nseq = 0;  // warp 0: picks recorded so far
-  long long st_starts = 0, st_batches = 0, st_picks = 0, st_cands = 0, st_w0 = 0, st_pass = 0, st_col = 0;
+  int nseq = 0;  // picks recorded (greedy order)
   if (n <= kWarpCliqueMaxN) {
     if (n <= 1024) {  // stage the adjacency (n x W <= 32K words) in shared memory
       for (int i = tid; i < n * W; i += CT) bits[i] = __ldg(adj + i);
@@ -421,90 +657,8 @@ __global__ void __launch_bounds__(CT, 1) k_level_cliques(PrepArgs a,
     } else if (wid == 0) {
       nseq = cliques_warp<4>(a, adj, n, W, s_p, seq, seqs);
     }
-  } else
-  for (int ia = 0; ia < n; ++ia) {
-    if (!((A[ia >> 5] >> (ia & 31)) & 1u)) continue;  // absorbed earlier (uniform)
-    const int w0 = ia >> 5;
-    const uint32_t gt = (ia & 31) == 31 ? 0u : (0xffffffffu << ((ia & 31) + 1));
-    const uint32_t *row = adj + (int64_t)ia * W;
-    long long c0 = clock64();
-    // C = adj(ia) & alive above ia, by the block (coalesced row loads), and
-    // its first candidates
-    int got = pass_collect(w0, [&](int w) {
-      const uint32_t c = __ldg(row + w) & A[w];
-      return w == w0 ? (c & gt) : c;
-    });
-    st_pass += clock64() - c0;
-    if (got == 0) continue;  // no h-neighbour left: stays a singleton at h (uniform)
-    ++st_starts;
-    while (true) {
-      c0 = clock64();
-      ++st_batches;
-      const int k = min(got, 32);
-      // -- 2. mutual adjacency of the candidates: warp r (and r + 16) tests
-      //       row p_r against p_j, j < r (the words of one row: few sectors)
-      for (int r = wid; r < k; r += CT / 32) {
-        const int pr = s_p[r];
-        bool bit = false;
-        if (lane < r) {
-          const int pj = s_p[lane];
-          bit = (__ldg(adj + (int64_t)pr * W + (pj >> 5)) >> (pj & 31)) & 1u;
-        }
-        const uint32_t m = __ballot_sync(0xffffffffu, bit);
-        if (lane == 0) s_m[r] = m;
-      }
-      __syncthreads();
-      // -- 3. the pick chain (warp 0): p_1, then the smallest remaining
-      //       candidate adjacent to every pick so far
-      if (wid == 0) {
-        int npick = 0;
-        if (k > 0) {
-          const int pi = lane < k ? s_p[lane] : 0;
-          const uint32_t m = lane < k ? s_m[lane] : 0u;
-          uint32_t ch = 1u;
-          uint32_t rem = __ballot_sync(0xffffffffu, lane < k && (m & 1u));
-          while (rem != 0u) {
-            const int j = __ffs(rem) - 1;
-            ch |= 1u << j;
-            rem &= __ballot_sync(0xffffffffu, (m >> j) & 1u) & ~((2u << j) - 1u);
-          }
-          const bool picked = lane < k && ((ch >> lane) & 1u);
-          npick = __popc(ch);
-          const int rank = __popc(ch & ((1u << lane) - 1u));
-          if (picked) {
-            seq[nseq + rank] = pi;
-            seqs[nseq + rank] = ia;
-            atomicAnd(&A[pi >> 5], ~(1u << (pi & 31)));
-            s_pick[rank] = pi;
-          }
-        }
-        nseq += npick;
-        st_picks += npick;
-        st_cands += k;
-        if (lane == 0) {
-          s_npick = npick;
-          s_last = got > 32 || (got == 32 && k > 0) ? s_p[31] : -1;
-        }
-      }
-      __syncthreads();
-      st_w0 += clock64() - c0;
-      c0 = clock64();
-      const int last = s_last;
-      if (last < 0) break;  // every candidate was considered (uniform)
-      const int npick = s_npick;
-      const int wl = last >> 5;
-      const uint32_t above = (last & 31) == 31 ? 0u : (0xffffffffu << ((last & 31) + 1));
-      // fold the picks into C above the last candidate, collect the next ones
-      got = pass_collect(wl, [&](int w) {
-        uint32_t c = C[w];
-        c &= w == wl ? above : 0xffffffffu;
-        for (int t = 0; t < npick; ++t) c &= __ldg(adj + (int64_t)s_pick[t] * W + w);
-        return c;
-      });
-      st_pass += clock64() - c0;
-      if (got == 0) break;
-    }
-    __syncthreads();
+  } else {
+    nseq = cliques_sweep(a, adj, n, W, seq, seqs);
   }
   if (tid == 0) s_nseq = nseq;
   __syncthreads();
@@ -561,16 +715,6 @@ __global__ void __launch_bounds__(CT, 1) k_level_cliques(PrepArgs a,
   }
   if (tid == 0) {
     *a.zcount = zbase + ns;
-    if (a.cstat) {
-      a.cstat[0] = (int)st_starts;
-      a.cstat[1] = (int)st_batches;
-      a.cstat[2] = (int)st_picks;
-      a.cstat[3] = (int)st_cands;
-      a.cstat[4] = n;
-      a.cstat[5] = (int)(st_w0 >> 10);
-      a.cstat[6] = (int)(st_pass >> 10);
-      a.cstat[7] = (int)(st_col >> 10);
-    }
   }
 }
 
