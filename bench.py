@@ -169,12 +169,32 @@ def oracle_build_time(ids):
     return t3 - t0, {"distance_s": t1 - t0, "linkage_s": t2 - t1, "tree_order_s": t3 - t2}
 
 
+def cpu_model():
+    """Host CPU model (lscpu "Model name", else /proc/cpuinfo)."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.lower().startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline(w, n_s):
     from oracle import oracle_c as oc
     ids = np.ascontiguousarray(w.ids[:n_s])
     secs, parts = oracle_build_time(ids)
     pairs = n_s * (n_s - 1) / 2
     return {"value": pairs / secs, "unit": "context-pairs/s", "cores": oc.num_threads(), "kind": "oracle",
+            "cpu_model": cpu_model(),
             "sample": f"first {n_s} contexts of the workload, full build (a1-a7) once",
             "seconds": secs, "stages_s": parts}
 
@@ -202,7 +222,7 @@ def run_reference(args, ws, rank):
             "scaling": "weak", "vs_baseline": None, "dtype": "u32+f32", "data": "synthetic",
             "config": {"workload": workload_desc(args.config, w) + f"; oracle sample = first {n_s} contexts"},
             "cpu_baseline": {"value": value, "unit": "context-pairs/s", "cores": oc.num_threads(),
-                             "kind": "oracle", "sample": f"first {n_s} contexts per step"},
+                             "kind": "oracle", "cpu_model": cpu_model(), "sample": f"first {n_s} contexts per step"},
             "e2e": {"value": value, "unit": "context-pairs/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -319,10 +339,17 @@ def run_ours(args, ws, rank, local):
     dist_bytes = (6.0 if codes else 4.0) * rows_here * N + 4.0 * N * K
     dist_gbs = dist_bytes / (mean["distance_ms"] * 1e-3) / 1e9
     traffic = load_traffic(args.config)
+    # the method's own output alone: fp32 rows (4 B per entry) + ids read
+    rows_bytes = 4.0 * rows_here * N + 4.0 * N * K
     roof_dist = {"kernel": "k_dist_tile (a2-a4, distance rows + fused row NN)", "bound": "hbm",
                  "achieved": dist_gbs, "peak": hbm, "unit": "GB/s", "frac": dist_gbs / hbm,
                  "traffic": traffic.get("k_dist_tile") if traffic and not sharded else None, "peak_source": peak_src,
                  "algorithmic_bytes_per_launch": dist_bytes, "launches_per_step": 1,
+                 "algorithmic_bytes_note": ("4 B fp32 row + 2 B value code" if codes else "4 B fp32 row") +
+                 " per entry + 4 N K B of ids",
+                 "fp32_rows_only": {"algorithmic_bytes_per_launch": rows_bytes,
+                                    "achieved": rows_bytes / (mean["distance_ms"] * 1e-3) / 1e9,
+                                    "frac": rows_bytes / (mean["distance_ms"] * 1e-3) / 1e9 / hbm},
                  "share_of_step": mean["distance_ms"] / ms}
     mb = mean["merge_bytes"] / max(mean["merge_launches"], 1)
     merge_gbs = mean["merge_bytes"] / (mean["merge_ms"] * 1e-3) / 1e9 if mean["merge_ms"] > 0 else 0.0

@@ -54,8 +54,13 @@ enum rb_status_code {
   RB_EALPHA = -3,    /* alpha outside [1/1000, 1/100] without
                         RB_ALPHA_ANY, or alpha_den == 0 / > 1000                 */
   RB_ENOMEM = -4,    /* host allocation failed                                   */
-  RB_ECUDA = -5,     /* CUDA runtime error (no device, launch failure, ...)      */
-  RB_ENCCL = -6,     /* reserved: collective failure                             */
+  RB_ECUDA = -5,     /* CUDA runtime error (no device, launch failure, ...).
+                        A sticky error (a faulting kernel) poisons the process:
+                        every later device entry returns RB_ECUDA at once,
+                        naming the first error.  An RB_ECUDA from
+                        rb_build_index_dist also poisons that rb_dist handle.  */
+  RB_ENCCL = -6,     /* reserved (the sharded build exchanges over peer memory,
+                        DESIGN.md §8; no collective library on the data path)  */
   RB_EPATH = -7,     /* invalid search path / row index          */
   RB_ESESSION = -8,  /* unknown / null session                        */
   RB_ESTATE = -9     /* precondition, e.g. a stage that was skipped             */

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdlib>
 #include <condition_variable>
@@ -35,8 +36,43 @@ rb_status fail(rb_status code, const std::string &msg) {
   return code;
 }
 
+// A sticky CUDA error (a faulting kernel) leaves the context unusable: the
+// library records it and every later device call fails fast with RB_ECUDA
+// naming the first error, instead of reaching the driver again.
+std::atomic<int> g_sticky{0};
+
+bool is_sticky(cudaError_t e) {
+  switch (e) {
+    case cudaErrorIllegalAddress:
+    case cudaErrorLaunchFailure:
+    case cudaErrorMisalignedAddress:
+    case cudaErrorIllegalInstruction:
+    case cudaErrorInvalidAddressSpace:
+    case cudaErrorInvalidPc:
+    case cudaErrorHardwareStackError:
+    case cudaErrorAssert:
+    case cudaErrorLaunchTimeout:
+    case cudaErrorECCUncorrectable:
+    case cudaErrorContextIsDestroyed:
+      return true;
+    default:
+      return false;
+  }
+}
+
 rb_status cuda_fail(cudaError_t e, const char *where) {
+  if (is_sticky(e)) {
+    int none = 0;
+    g_sticky.compare_exchange_strong(none, (int)e);
+  }
   return fail(RB_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+rb_status check_poisoned() {
+  const int e = g_sticky.load();
+  if (e == 0) return RB_OK;
+  return fail(RB_ECUDA, std::string("device poisoned by an earlier CUDA error (") +
+                            cudaGetErrorString((cudaError_t)e) + "); restart the process");
 }
 
 constexpr size_t kAlign = 256;
@@ -143,8 +179,10 @@ ScratchLayout ScratchLayout::make(int64_t N, int32_t K, bool keep_rows, bool lin
 
 extern "C" {
 
-// error helper for the other host translation units (hidden: not an rb_ entry)
+// error helpers for the other host translation units (hidden: not rb_ entries)
 rb_status ragb_fail_msg(rb_status code, const char *msg) { return fail(code, msg); }
+rb_status ragb_cuda_fail(int e, const char *msg) { return cuda_fail((cudaError_t)e, msg); }
+rb_status ragb_check_poisoned(void) { return check_poisoned(); }
 
 const char *rb_version(void) { return "ragb 0.1.0 (sm_100a)"; }
 
@@ -190,6 +228,7 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
   using clock = std::chrono::steady_clock;
   const auto t_start = clock::now();
   if (!out) return fail(RB_EINVAL, "out is NULL");
+  if (check_poisoned() != RB_OK) return RB_ECUDA;
   int64_t row0, nrows;
   rb_status s = check_params(N, K, p, &row0, &nrows);
   if (s != RB_OK) return s;

@@ -187,6 +187,7 @@ struct rb_dist {
   unsigned *my_bar = nullptr;            // cudaMalloc'd by this process (real mode)
   unsigned epoch = 0;
   std::vector<void *> opened;            // IPC mappings to close
+  int poison = 0;                        // first CUDA error of a build: the handle is unusable
 };
 
 namespace {
@@ -220,6 +221,8 @@ struct HandleBlob {
 }  // namespace
 
 extern "C" rb_status ragb_fail_msg(rb_status code, const char *msg);  // capi.cpp
+extern "C" rb_status ragb_cuda_fail(int e, const char *msg);           // capi.cpp (records sticky errors)
+extern "C" rb_status ragb_check_poisoned(void);                        // capi.cpp
 
 namespace {
 rb_status dfail(rb_status code, const std::string &msg) { return ragb_fail_msg(code, msg.c_str()); }
@@ -352,6 +355,7 @@ rb_status build_index_dist(rb_dist *d, const uint32_t *ids_d, const uint8_t *len
   do {                                                              \
     if ((e = (call)) != cudaSuccess) {                              \
       *msg = std::string(where) + ": " + cudaGetErrorString(e);     \
+      d->poison = (int)e;                                           \
       return RB_ECUDA;                                              \
     }                                                               \
   } while (0)
@@ -789,7 +793,15 @@ extern "C" rb_status rb_build_index_dist(rb_dist *d, const uint32_t *ids_dev, co
     if (n * 1000 < dd || n * 100 > dd) return ragb_fail_msg(RB_EALPHA, "alpha outside [0.001, 0.01]");
   }
   if (p->linkage != RB_LINK_COMPLETE) return ragb_fail_msg(RB_EINVAL, "the sharded build runs complete linkage");
+  if (ragb_check_poisoned() != RB_OK) return RB_ECUDA;
+  if (d->poison)
+    return ragb_fail_msg(RB_ECUDA, (std::string("handle poisoned by an earlier CUDA error (") +
+                                    cudaGetErrorString((cudaError_t)d->poison) + ")").c_str());
   std::string msg;
   const rb_status s = ragb::build_index_dist(d, ids_dev, lens_dev, N, K, p, out, &msg);
+  if (s == RB_ECUDA) {
+    if (!d->poison) d->poison = (int)cudaErrorUnknown;  // a timed-out barrier or a lost peer
+    return ragb_cuda_fail(d->poison, msg.c_str());
+  }
   return s == RB_OK ? s : ragb_fail_msg(s, msg.c_str());
 }
