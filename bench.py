@@ -323,6 +323,22 @@ def run_ours(args, ws, rank, local):
     if ws > 1:
         e2e_ms = allreduce_max(e2e_ms, dev)
 
+    # ---- NEXT-1: online ordering of new contexts against the built index ---
+    online = None
+    if not sharded and args.config == "C4":
+        from synth.workload import generate
+        q = generate(10_000, K, 1_000_000, 4004).ids
+        online = {"workload": "10,000 new contexts (K=20, V=1e6, seed 4004) searched + inserted + ordered "
+                              "into the C4 index (rb_order_contexts, ids != NULL)"}
+        for mode, key in ((1, "device_root_scores"), (0, "host_only")):
+            oi = build(ids_dev)
+            torch.cuda.synchronize()
+            oi.set_online(mode)
+            t0 = time.perf_counter()
+            oi.order_new(q)
+            online[key] = {"contexts_per_s": 10_000 / (time.perf_counter() - t0)}
+            del oi
+
     if rank != 0:
         return
     mean = {k: statistics.mean(s[k] for s in stats) for k in stats[0]}
@@ -392,6 +408,8 @@ def run_ours(args, ws, rank, local):
         "clocks": clocks,
         "paper_context": PAPER_CONTEXT,
     }
+    if online:
+        line["online_order"] = online
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(w, min(args.cpu_sample, N))
     print(json.dumps(line), flush=True)

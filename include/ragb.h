@@ -260,6 +260,17 @@ RB_API rb_status rb_order_contexts(rb_index *idx, const uint32_t *ids, const uin
                                    int32_t K, uint32_t *out_ids, uint8_t *out_prefix_len,
                                    int64_t *out_schedule);
 
+/* Where the online search (rb_order_contexts with ids != NULL) scores the
+ * root's children, the level whose fan-out reaches thousands: device = 1 on
+ * the GPU (one kernel per sub-batch of up to 2048 queries computes Eq. 1 of
+ * every query against every child of the root as it was when the sub-batch
+ * started; children replaced or appended by earlier queries of the sub-batch
+ * are scored on the host, so the results equal the sequential host search bit
+ * for bit), 0 on the host, -1 (default) the GPU for batches of >= 64 queries
+ * against a root of >= 256 children.  The device buffers are owned by the index
+ * (freed by rb_index_free).  Errors: RB_EINVAL, RB_ECUDA (poisoned device). */
+RB_API rb_status rb_index_set_online(rb_index *idx, int32_t device);
+
 /* Set the Eq. 1 alpha used by online ordering (an index built from a merge
  * list defaults to 1/200, X1).  Errors: RB_EALPHA. */
 RB_API rb_status rb_index_set_alpha(rb_index *idx, uint32_t alpha_num, uint32_t alpha_den);

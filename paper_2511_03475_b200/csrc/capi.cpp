@@ -712,6 +712,14 @@ rb_status rb_order_contexts(rb_index *idx, const uint32_t *ids, const uint8_t *l
   return RB_OK;
 }
 
+rb_status rb_index_set_online(rb_index *idx, int32_t device) {
+  if (!idx) return fail(RB_EINVAL, "NULL index");
+  if (device < -1 || device > 1) return fail(RB_EINVAL, "device must be -1, 0 or 1");
+  if (device == 1 && check_poisoned() != RB_OK) return RB_ECUDA;
+  idx->H.online_device = device;
+  return RB_OK;
+}
+
 rb_status rb_index_set_alpha(rb_index *idx, uint32_t alpha_num, uint32_t alpha_den) {
   if (!idx) return fail(RB_EINVAL, "NULL index");
   if (alpha_den == 0 || alpha_den > 1000 || alpha_num > alpha_den)

@@ -146,6 +146,16 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
 
 // ----------------------------------------------------------------- host
 struct DynTree;  // online (mutable) form of the tree, online.cpp
+struct OnlineDevState;  // device buffers of the online root scores, online_dev.cu
+void online_dev_free(OnlineDevState *s);
+// NEXT-1 device step: Eq. 1 of M queries (host [M][K], lens or NULL) against
+// the root's children (ordered contexts as CSR coff [F+1] / cdocs, leaf flags
+// [F]); returns, per query, the eligible children (X15, X20) as (child index,
+// d bits) in ent[q * cap ...], their count in cnt[q] (> cap: overflow).
+cudaError_t online_root_scores(OnlineDevState **state, const uint32_t *qids, const uint8_t *qlens, int M, int K,
+                               const std::vector<int32_t> &coff, const std::vector<uint32_t> &cdocs,
+                               const std::vector<uint8_t> &cleaf, uint32_t an, uint32_t ad, int cap,
+                               std::vector<int> *cnt, std::vector<uint2> *ent);
 
 // std::allocator without value-initialisation on resize (large host outputs
 // that a parallel loop fills completely: no sequential zero-fill first).
@@ -195,6 +205,13 @@ struct HostIndex {
   bool trace = false;       // Tuning::trace (host-stage laps on stderr)
   bool sort_merges = true;  // complete linkage: export ascending key (X9); intersection: merge order
   std::shared_ptr<DynTree> dyn;             // set by the first online update
+  int online_device = -1;                   // NEXT-1 root scores: -1 auto, 0 host, 1 device
+  OnlineDevState *odev = nullptr;           // their device buffers (freed with the index)
+  int64_t online_stats[2] = {0, 0};         // queries scored on the device, (reserved)
+  HostIndex() = default;
+  HostIndex(const HostIndex &) = delete;
+  HostIndex &operator=(const HostIndex &) = delete;
+  ~HostIndex() { if (odev) online_dev_free(odev); }
 };
 
 // NEXT-1: online search + insert + ordering of M new contexts (online.cpp).

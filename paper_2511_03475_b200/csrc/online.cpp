@@ -12,7 +12,10 @@
 // Readings: X15 (eligibility, tie and stop rule), X20 (a virtual
 // child must be contained in the query), X21 (leaf match), canonical fp32 Eq. 1
 // distances against each child's ordered context (X6).
+#include <cuda_runtime.h>
+
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <set>
@@ -153,9 +156,26 @@ static void candidates(DynTree &T, int32_t node, const std::vector<uint32_t> &q,
   out->erase(std::unique(out->begin(), out->end()), out->end());
 }
 
-// X15 search; returns the matched node and the descent path.
+// Distances of one query against the root's children from the device
+// (online_dev.cu), for a sub-batch of queries and the root as it was when the
+// sub-batch started; children changed since (replaced by an X21 node, or
+// appended) are scored on the host.
+struct RootScores {
+  int F = 0, cap = 0;
+  // children replaced or appended since the snapshot, by doc (host-scored
+  // candidates: only those sharing a doc with the query can be eligible)
+  std::unordered_map<uint32_t, std::vector<int32_t>> dinv;
+  std::vector<int> cnt;          // [queries] eligible children (> cap: overflow, host scores that query)
+  std::vector<uint2> ent;        // [queries][cap] (child index, d bits)
+  std::vector<uint8_t> dirty;    // [F] child replaced since the snapshot
+  std::vector<int32_t> dirty_idx;
+};
+
+// X15 search; returns the matched node and the descent path.  rs / qi: the
+// device's root distances of this query (nullptr: host only).
 static int32_t dyn_search(DynTree &T, const std::vector<uint32_t> &q, const QueryView &qv,
-                          uint32_t an, uint32_t ad, std::vector<int32_t> *path) {
+                          uint32_t an, uint32_t ad, std::vector<int32_t> *path, const RootScores *rs = nullptr,
+                          int qi = 0) {
   int32_t node = 0;
   path->clear();
   std::vector<int32_t> cand;
@@ -165,25 +185,45 @@ static int32_t dyn_search(DynTree &T, const std::vector<uint32_t> &q, const Quer
     int32_t idx;
   };
   std::vector<C> el;
-  while (T.leaf[node] < 0) {
-    candidates(T, node, q, &cand);
-    el.clear();
-    for (int32_t idx : cand) {
-      const int32_t c = T.kids[node][idx];
-      const auto &oc = T.ord[c];
-      uint32_t s = 0, D = 0;
-      for (size_t p = 0; p < oc.size(); ++p) {
-        const int pq = qv.pos_of(oc[p]);
-        if (pq >= 0) {
-          ++s;
-          D += (uint32_t)(pq > (int)p ? pq - (int)p : (int)p - pq);
-        }
+  auto score = [&](int32_t idx) {  // child idx of node: eligible -> el
+    const int32_t c = T.kids[node][idx];
+    const auto &oc = T.ord[c];
+    uint32_t s = 0, D = 0;
+    for (size_t p = 0; p < oc.size(); ++p) {
+      const int pq = qv.pos_of(oc[p]);
+      if (pq >= 0) {
+        ++s;
+        D += (uint32_t)(pq > (int)p ? pq - (int)p : (int)p - pq);
       }
-      if (s == 0) continue;
-      const bool isleaf = T.leaf[c] >= 0;
-      if (!isleaf && s != oc.size()) continue;  // X20: virtual child contained in the query
-      const uint32_t m = (uint32_t)std::max<size_t>(oc.size(), (size_t)qv.len);
-      el.push_back({eq1_host(s, D, m, an, ad), isleaf ? 1 : 0, idx});
+    }
+    if (s == 0) return;
+    const bool isleaf = T.leaf[c] >= 0;
+    if (!isleaf && s != oc.size()) return;  // X20: virtual child contained in the query
+    const uint32_t m = (uint32_t)std::max<size_t>(oc.size(), (size_t)qv.len);
+    el.push_back({eq1_host(s, D, m, an, ad), isleaf ? 1 : 0, idx});
+  };
+  while (T.leaf[node] < 0) {
+    el.clear();
+    if (node == 0 && rs && rs->cnt[qi] <= rs->cap) {
+      const uint2 *e = rs->ent.data() + (size_t)qi * rs->cap;
+      for (int z = 0; z < rs->cnt[qi]; ++z) {
+        const int32_t idx = (int32_t)e[z].x;
+        if (rs->dirty[idx]) continue;
+        float d;
+        std::memcpy(&d, &e[z].y, 4);
+        el.push_back({d, T.leaf[T.kids[0][idx]] >= 0 ? 1 : 0, idx});
+      }
+      cand.clear();
+      for (uint32_t d : q) {
+        auto f = rs->dinv.find(d);
+        if (f != rs->dinv.end()) cand.insert(cand.end(), f->second.begin(), f->second.end());
+      }
+      std::sort(cand.begin(), cand.end());
+      cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
+      for (int32_t idx : cand) score(idx);
+    } else {
+      candidates(T, node, q, &cand);
+      for (int32_t idx : cand) score(idx);
     }
     if (el.empty()) break;
     bool all_same = el.size() >= 2;
@@ -217,7 +257,57 @@ rb_status online_order(HostIndex &H, const uint32_t *ids, const uint8_t *lens, i
   DynTree &T = *H.dyn;
   std::vector<std::vector<int32_t>> paths(M);
   std::vector<int32_t> path;
+  // device scores of the root's children (mode: 0 host, 1 device, -1 auto =
+  // device for batches of >= 64 queries against a root of >= 256 children)
+  const int mode = H.online_device;
+  RootScores rs;
+  int64_t sb_end = 0;  // end of the current device sub-batch
+  constexpr int64_t kSub = 2048;
   for (int64_t i = 0; i < M; ++i) {
+    if (i == sb_end) {
+      sb_end = std::min<int64_t>(M, i + kSub);
+      const size_t F = T.kids[0].size();
+      int ndev = 0;
+      const bool dev = mode == 1 || (mode < 0 && M >= 64 && F >= 256 && cudaGetDeviceCount(&ndev) == cudaSuccess &&
+                                     ndev > 0);
+      rs.F = 0;
+      rs.cnt.clear();
+      if (dev) {
+        std::vector<int32_t> coff(F + 1, 0);
+        std::vector<uint32_t> cdocs;
+        std::vector<uint8_t> cleaf(F);
+        for (size_t c = 0; c < F; ++c) {
+          const int32_t k = T.kids[0][c];
+          cdocs.insert(cdocs.end(), T.ord[k].begin(), T.ord[k].end());
+          coff[c + 1] = (int32_t)cdocs.size();
+          cleaf[c] = T.leaf[k] >= 0 ? 1 : 0;
+        }
+        rs.F = (int)F;
+        rs.cap = (int)std::min<size_t>(F, 1024);
+        rs.dirty.assign(F, 0);
+        rs.dirty_idx.clear();
+        rs.dinv.clear();
+        const cudaError_t ce = online_root_scores(&H.odev, ids + i * K, lens ? lens + i : nullptr,
+                                                  (int)(sb_end - i), K, coff, cdocs, cleaf, an, ad,
+                                                  std::max(rs.cap, 1), &rs.cnt, &rs.ent);
+        if (ce != cudaSuccess) {
+          *msg = std::string("online root scores: ") + cudaGetErrorString(ce);
+          return RB_ECUDA;
+        }
+        H.online_stats[0] += sb_end - i;
+        if (H.trace) {
+          int64_t tot = 0, mx = 0, over = 0;
+          for (int c : rs.cnt) {
+            tot += c;
+            mx = std::max<int64_t>(mx, c);
+            over += c > rs.cap ? 1 : 0;
+          }
+          std::fprintf(stderr, "[ragb online] sub-batch %lld queries, root fan-out %zu, eligible mean %.1f max %lld, over cap %lld\n",
+                       (long long)(sb_end - i), F, (double)tot / std::max<size_t>(rs.cnt.size(), 1), (long long)mx,
+                       (long long)over);
+        }
+      }
+    }
     const int L = lens ? lens[i] : K;
     if (L < 1 || L > K) {
       *msg = "context length not in [1, K]";
@@ -238,7 +328,9 @@ rb_status online_order(HostIndex &H, const uint32_t *ids, const uint8_t *lens, i
         *msg = "reserved DocId 0xFFFFFFFF";
         return RB_EINVAL;
       }
-    int32_t node = dyn_search(T, q, qv, an, ad, &path);
+    const bool have_rs = !rs.cnt.empty();
+    int32_t node = dyn_search(T, q, qv, an, ad, &path, have_rs ? &rs : nullptr,
+                              have_rs ? (int)(i - (sb_end - (int64_t)rs.cnt.size())) : 0);
     int32_t parent = node;
     if (T.leaf[node] >= 0) {  // leaf match (X21)
       const int32_t Lnode = node, P = T.parent[node];
@@ -262,6 +354,13 @@ rb_status online_order(HostIndex &H, const uint32_t *ids, const uint8_t *lens, i
         const int32_t V = dyn_new_node(T, P, inter, vord, -1);
         auto &pk = T.kids[P];
         const int32_t pos = T.cidx[Lnode];
+        if (P == 0 && !rs.cnt.empty()) {  // the device score of pos is stale: the host scores V there
+          if (pos < rs.F && !rs.dirty[pos]) {
+            rs.dirty[pos] = 1;
+            rs.dirty_idx.push_back(pos);
+          }
+          for (uint32_t d : vord) rs.dinv[d].push_back(pos);
+        }
         pk[pos] = V;
         T.cidx[V] = pos;
         T.kids[V].push_back(Lnode);
@@ -289,6 +388,8 @@ rb_status online_order(HostIndex &H, const uint32_t *ids, const uint8_t *lens, i
     T.kids[parent].push_back(k);
     T.cidx[k] = (int32_t)T.kids[parent].size() - 1;
     inv_add(T, parent, T.cidx[k]);
+    if (parent == 0 && !rs.cnt.empty())  // appended at the root after the snapshot: host-scored
+      for (uint32_t d : ordq) rs.dinv[d].push_back(T.cidx[k]);
     T.leaf_node.push_back(k);
     if (out_ids) {
       std::memcpy(out_ids + i * K, ordq.data(), 4 * ordq.size());

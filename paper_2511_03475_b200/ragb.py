@@ -33,7 +33,7 @@ EXPORTED = [
     "rb_build_index_host", "rb_index_from_linkage", "rb_index_size", "rb_index_stats", "rb_index_nn",
     "rb_index_linkage", "rb_index_tree_info", "rb_index_tree", "rb_order_contexts", "rb_session_open",
     "rb_session_open_docs", "rb_dedup_turn", "rb_session_turn", "rb_session_free", "rb_index_free",
-    "rb_index_set_alpha", "rb_session_context", "rb_dedup_batch",
+    "rb_index_set_alpha", "rb_index_set_online", "rb_session_context", "rb_dedup_batch",
     "rb_index_cache_event", "rb_index_cache_state", "rb_cache_create", "rb_cache_prefill",
     "rb_cache_prefill_batch", "rb_cache_resident", "rb_cache_free",
     "rb_dist_create", "rb_dist_workspace_size", "rb_dist_attach", "rb_dist_export", "rb_dist_import",
@@ -104,6 +104,7 @@ def lib():
         "rb_index_tree": ([P, P, P, P, P, P, P, P], i32),
         "rb_order_contexts": ([P, P, P, i64, i32, P, P, P], i32),
         "rb_index_set_alpha": ([P, u32, u32], i32),
+        "rb_index_set_online": ([P, i32], i32),
         "rb_session_context": ([P, P, i32, ctypes.POINTER(i32)], i32),
         "rb_dedup_batch": ([P, i64, P, P, P, i64, i32, P, P, P, P, P], i32),
         "rb_index_cache_event": ([P, i32, P, i32, i64, ctypes.POINTER(i64)], i32),
@@ -254,6 +255,10 @@ class Index:
         last = np.empty(n, dtype=np.int64)
         _check(lib().rb_index_cache_state(self._h, _np_ptr(seq), _np_ptr(last)))
         return seq, last
+
+    def set_online(self, device: int):
+        """NEXT-1 root scoring: 1 GPU, 0 host, -1 auto (rb_index_set_online)."""
+        _check(lib().rb_index_set_online(self._h, int(device)))
 
     def set_alpha(self, alpha):
         an, ad = alpha_rational(alpha)
