@@ -78,22 +78,31 @@ void host_begin(HostIndex &H, TreeBuild &T) {
   T.rpar.assign((size_t)(N + std::max<int64_t>(N - 1, 0)), -1);
   T.keep.assign((size_t)std::max<int64_t>(N - 1, 0), 1);
   if (H.sort_merges) T.zk.reserve((size_t)std::max<int64_t>(N - 1, 0));
-  // sorted leaf sets (parallel)
+  // sorted leaf sets, in parallel on plain threads that exit afterwards: this
+  // runs while the device rounds are launched from another thread, and an
+  // OpenMP team would keep spinning on the cores that thread needs
   T.lset.resize((size_t)N * K);
-#pragma omp parallel for num_threads(nth) schedule(static)
-  for (int64_t i = 0; i < N; ++i) {
-    uint32_t *d = T.lset.data() + i * K;
-    const uint32_t *src = H.ids.data() + i * K;
-    const int L = uniform ? K : H.lens[i];
-    for (int k = 0; k < L; ++k) {  // insertion sort (K <= 255, typically 5-20)
-      const uint32_t x = src[k];
-      int q = k;
-      while (q > 0 && d[q - 1] > x) {
-        d[q] = d[q - 1];
-        --q;
-      }
-      d[q] = x;
-    }
+  {
+    const int nt = std::max(1, std::min<int>(nth, (int)(N / 4096) + 1));
+    std::vector<std::thread> pool;
+    for (int w = 0; w < nt; ++w)
+      pool.emplace_back([&, w] {
+        for (int64_t i = N * w / nt; i < N * (w + 1) / nt; ++i) {
+          uint32_t *d = T.lset.data() + i * K;
+          const uint32_t *src = H.ids.data() + i * K;
+          const int L = uniform ? K : H.lens[i];
+          for (int k = 0; k < L; ++k) {  // insertion sort (K <= 255, typically 5-20)
+            const uint32_t x = src[k];
+            int q = k;
+            while (q > 0 && d[q - 1] > x) {
+              d[q] = d[q - 1];
+              --q;
+            }
+            d[q] = x;
+          }
+        }
+      });
+    for (auto &t : pool) t.join();
   }
   const int64_t nz = std::max<int64_t>(N - 1, 0);
   T.voff.assign(nz + 1, 0);
