@@ -185,7 +185,7 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
   cudaError_t e;
   k_init_state<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(rep[0], sz[0], N);
   ++*launches;
-  if ((e = cudaMemsetAsync(counters, 0, 2 * sizeof(int), st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(counters, 0, 16 * sizeof(int), st)) != cudaSuccess) return e;
 
   PrepArgs pa{};
   pa.leader = at<int>(scratch, L.leader);
@@ -206,6 +206,7 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
   pa.zcount = counters;
   pa.Mn = counters + 1;
   pa.level = counters + 2;
+  pa.sweep_ctl = counters + 14;  // 0 between launches (reset by the sweep's CTA 0)
   pa.cstat = counters + 4;
   pa.vals = codes ? cm->vals : nullptr;
   pa.pmap = codes ? at<int2>(scratch, L.pmap) : nullptr;
@@ -259,7 +260,9 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
       const size_t smem = m1 * ((m1 + 31) / 32) * 4;  // the staged adjacency of levels <= 1024
       if (smem > 48 * 1024)
         occupancy_cached(k_level_cliques, CT, smem);
-      k_level_cliques<<<1, CT, smem, st>>>(pa, adj);
+      // CTA 0 decides; with a level above 4096 vertices the other CTAs
+      // (one per SM, all resident) update the clique candidate sets
+      k_level_cliques<<<std::min(sms, 1 + kSweepHelpers), CT, smem, st>>>(pa, adj);
     }
     launch_prep_compact(pa, sms, st, launches);
     *launches += 2;

@@ -84,6 +84,7 @@ struct PrepArgs {
   int2 *pmap;  // [Mn + 8] new column -> (leader, other member of a pair | -1 singleton | -2 larger), or nullptr
   int *level;  // [0] level list length, [1] h bits
   int *cstat;  // clique diagnostics: starts, batches, picks, candidates, level n, clk/1k (warp0, pass)
+  int *sweep_ctl;  // level-clique sweep with helper CTAs: published block count (0 between launches), or nullptr
 };
 
 struct BlockScratch {
@@ -372,6 +373,7 @@ constexpr int CT = 512;  // threads of k_level_cliques (128 registers for the pi
 // greedy order (clique, then vertex) by a counting sort.
 constexpr int kSweepB = 128;      // vertices per block (4 words)
 constexpr int kSweepCap = 1024;   // cliques with candidates examined per pass
+constexpr int kSweepHelpers = 32; // helper CTAs of the sweep (candidate-set updates)
 
 __device__ __forceinline__ uint4 and4(uint4 x, uint4 y) { return make_uint4(x.x & y.x, x.y & y.y, x.z & y.z, x.w & y.w); }
 __device__ __forceinline__ bool any4(uint4 x) { return (x.x | x.y | x.z | x.w) != 0u; }
@@ -389,6 +391,93 @@ __device__ __forceinline__ uint4 clear4(uint4 x, int p) {
   const uint32_t b = ~(1u << (p & 31));
   const int q = p >> 5;
   return make_uint4(q == 0 ? x.x & b : x.x, q == 1 ? x.y & b : x.y, q == 2 ? x.z & b : x.z, q == 3 ? x.w & b : x.w);
+}
+
+// Eager candidate-set update of block v0's decisions (s_bj / s_bv, nb of them;
+// starts marked 0x10000) for the words [w0, w1): a new clique's set is its
+// start's row ANDed with its members in the block (one store per word), an
+// existing clique's set is ANDed with each new member's row (reductions).
+// Work items (decision, 128-word chunk) over nwarps warps, 4 words per lane.
+__device__ __forceinline__ void sweep_update(const uint32_t *__restrict__ adj, int W, uint32_t *I, int WI, int v0,
+                                             const int *bj, const int *bv, int nb, int w0, int w1, int gw,
+                                             int nwarps, int lane) {
+  const int nch = (w1 - w0 + 127) / 128;
+  for (int it = gw; it < nb * nch; it += nwarps) {
+    const int t = it / nch, w = w0 + (it - t * nch) * 128 + 4 * lane;
+    const int j = bj[t], v = bv[t];
+    uint32_t *dst = I + (size_t)j * WI;
+    if (v & 0x10000) {  // new clique: start row AND its members that follow it in the block
+      uint32_t x[4];
+      const uint32_t *src = adj + (size_t)(v0 + (v & 0xffff)) * W;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) x[q] = w + q < w1 ? __ldg(src + w + q) : 0u;
+      for (int t2 = t + 1; t2 < nb && bj[t2] == j && !(bv[t2] & 0x10000); ++t2) {
+        const uint32_t *m = adj + (size_t)(v0 + bv[t2]) * W;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) x[q] &= w + q < w1 ? __ldg(m + w + q) : 0u;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (w + q < w1) dst[w + q] = x[q];
+    } else {
+      // a member of an existing clique (a member of a new one is folded into its start's item)
+      bool fresh = false;
+      for (int t2 = t - 1; t2 >= 0 && bj[t2] == j; --t2) fresh |= (bv[t2] & 0x10000) != 0;
+      if (fresh) continue;
+      const uint32_t *src = adj + (size_t)(v0 + v) * W;
+      uint32_t x[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) x[q] = w + q < w1 ? __ldg(src + w + q) : 0xffffffffu;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (x[q] != 0xffffffffu) atomicAnd(dst + w + q, x[q]);
+    }
+  }
+}
+
+// Helper CTAs of the sweep (blockIdx.x >= 1): block b's decisions, once CTA 0
+// has published them, applied to the candidate-set words after block b + 1.
+__device__ void sweep_helper(const PrepArgs &a, const uint32_t *__restrict__ adj, int n, int W) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int WI = (W + 3) & ~3;
+  uint32_t *I = const_cast<uint32_t *>(adj) + (((size_t)n * W + 3) & ~(size_t)3);
+  int *ccnt = reinterpret_cast<int *>(I + (size_t)n * WI) + 4 * n;
+  const int nblk = (n + kSweepB - 1) / kSweepB;
+  const int2 *logb = reinterpret_cast<const int2 *>(ccnt + ((n + 2) & ~1));
+  const int *logn = reinterpret_cast<const int *>(logb + (size_t)nblk * kSweepB);
+  int *hcnt = const_cast<int *>(logn) + nblk;
+  __shared__ int s_bj2[kSweepB], s_bv2[kSweepB];
+  __shared__ int s_nb2;
+  const int nhelp = (int)gridDim.x - 1, h = (int)blockIdx.x - 1;
+  for (int b = 0; b < nblk; ++b) {
+    if (tid == 0) {
+      const volatile int *pub = a.sweep_ctl;
+      while (*pub <= b) __nanosleep(128);
+      __threadfence();
+      s_nb2 = __ldcg(logn + b);
+    }
+    __syncthreads();
+    const int nb = s_nb2;
+    for (int t = tid; t < nb; t += CT) {
+      const int2 e = __ldcg(logb + (size_t)b * kSweepB + t);
+      s_bj2[t] = e.x;
+      s_bv2[t] = e.y;
+    }
+    __syncthreads();
+    const int w0 = (b * kSweepB >> 5) + 8;  // after block b + 1 (CTA 0 writes that one)
+    if (w0 < W) sweep_update(adj, W, I, WI, b * kSweepB, s_bj2, s_bv2, nb, w0, W, h * (CT / 32) + wid, nhelp * (CT / 32), lane);
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      atomicAdd(hcnt + b, 1);
+      // every helper finishes block b before any starts b + 1 (a new clique's
+      // stores of block b come before reductions of block b + 1 on its words)
+      const volatile int *c = hcnt + b;
+      while (*c < nhelp) __nanosleep(64);
+      __threadfence();
+    }
+    __syncthreads();
+  }
 }
 
 // Returns the number of merges; seq / seqs (greedy order) as the other paths.
@@ -409,10 +498,18 @@ __device__ int cliques_sweep(const PrepArgs &a, const uint32_t *__restrict__ adj
   int *dec_r = dec_v + n;                                    // [n] rank within the clique
   int *cstart = dec_r + n;                                   // [n] start vertex of clique j
   int *ccnt = cstart + n;                                    // [n + 1] merges per clique, then offsets
+  const int nblk = (n + kSweepB - 1) / kSweepB;
+  int2 *logb = reinterpret_cast<int2 *>(ccnt + ((n + 2) & ~1));  // [nblk][kSweepB] decisions of block b (helpers)
+  int *logn = reinterpret_cast<int *>(logb + (size_t)nblk * kSweepB);  // [nblk] their count
+  int *hcnt = logn + nblk;                                   // [nblk] helpers done with block b
+  const bool helpers = a.sweep_ctl != nullptr && gridDim.x > 1;
+  const int nhelp = (int)gridDim.x - 1;
   if (tid == 0) {
     s_J = 0;
     s_nd = 0;
   }
+  if (helpers)
+    for (int i = tid; i < nblk; i += CT) hcnt[i] = 0;
   __syncthreads();
   long long tk[6] = {0, 0, 0, 0, 0, 0};
   long long nlist = 0;
@@ -567,37 +664,39 @@ __device__ int cliques_sweep(const PrepArgs &a, const uint32_t *__restrict__ adj
         s_nd = nd0 + c;
       }
     }
-    if (nw > 0) {
-      // one warp per decision, 4 words per lane (16-byte loads of the row)
-      const int wn4 = wb + 4;  // == wn, a multiple of 4: I rows are 16-byte aligned there
-      // new cliques: I_J = the start's row (plain stores), then every member ANDs
-      for (int t = nb_join + wid; t < nb; t += CT / 32) {
-        if (!(s_bv[t] & 0x10000)) continue;
-        const uint32_t *src = adj + (size_t)(v0 + (s_bv[t] & 0xffff)) * W;
-        uint32_t *dst = I + (size_t)s_bj[t] * WI;
-        for (int w = wn4 + 4 * lane; w < W; w += 128)
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (w + q < W) dst[w + q] = __ldg(src + w + q);
+    // eager candidate sets: CTA 0 updates the next block's words itself; with
+    // helper CTAs, the words after it are theirs (sweep_update), lagging one
+    // block behind — published through the decision log of the block
+    const int wend = helpers ? min(W, wn + 4) : W;
+    if (helpers && v0 >= kSweepB) {
+      // the helpers are done with block b - 1: they wrote words >= wn of its
+      // new cliques (plain stores this block's reductions must not precede),
+      // and every word this block's listing read
+      if (tid == 0) {
+        const volatile int *c = hcnt + (v0 / kSweepB - 1);
+        while (*c < nhelp) __nanosleep(64);
+        __threadfence();
       }
       __syncthreads();
-      for (int t = wid; t < nb; t += CT / 32) {
-        if (s_bv[t] & 0x10000) continue;
-        const uint32_t *src = adj + (size_t)(v0 + s_bv[t]) * W;
-        uint32_t *dst = I + (size_t)s_bj[t] * WI;
-        for (int w = wn4 + 4 * lane; w < W; w += 128) {
-          uint32_t x[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) x[q] = w + q < W ? __ldg(src + w + q) : 0xffffffffu;
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (w + q < W && x[q] != 0xffffffffu) atomicAnd(dst + w + q, x[q]);
-        }
-      }
+    }
+    if (helpers) {
+      for (int t = tid; t < nb; t += CT) logb[(size_t)(v0 / kSweepB) * kSweepB + t] = make_int2(s_bj[t], s_bv[t]);
+      if (tid == 0) logn[v0 / kSweepB] = nb;
+    }
+    if (wend > wn) sweep_update(adj, W, I, WI, v0, s_bj, s_bv, nb, wn, wend, wid, CT / 32, lane);
+    if (helpers) {
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) atomicExch(a.sweep_ctl, v0 / kSweepB + 1);  // block published
     }
     __threadfence();  // the reductions are at L2 before the next block reads I (ld.cg)
     __syncthreads();
     { const long long c1 = clock64(); tk[4] += c1 - c0; c0 = c1; }
+  }
+  if (helpers && tid == 0) {  // every helper is done: the control word goes back to 0 for the next launch
+    const volatile int *c = hcnt + (nblk - 1);
+    while (*c < nhelp) __nanosleep(64);
+    atomicExch(a.sweep_ctl, 0);
   }
   if (tid == 0 && a.cstat) {
     a.cstat[0] = s_J;
@@ -646,6 +745,10 @@ __global__ void __launch_bounds__(CT, 1) k_level_cliques(PrepArgs a,
   if (n < 2) return;
   const float hf = a.vals ? a.vals[a.level[1]] : __uint_as_float((unsigned)a.level[1]);
   const int W = (n + 31) >> 5;
+  if (blockIdx.x > 0) {  // helper CTAs: the sweep's candidate-set updates
+    if (n > kWarpCliqueMaxN && a.sweep_ctl) sweep_helper(a, adj, n, W);
+    return;
+  }
   int *seq = a.candA, *seqs = a.candB;  // pick list position, its clique's start position
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   int nseq = 0;  // picks recorded (greedy order)
