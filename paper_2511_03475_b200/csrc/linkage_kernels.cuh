@@ -559,8 +559,8 @@ __device__ int cliques_sweep(const PrepArgs &a, const uint32_t *__restrict__ adj
       if (tid == CT - 1) s_nl = pos + c;
       __syncthreads();
       { const long long c1 = clock64(); tk[1] += c1 - c0; c0 = c1; }
-      nlist += s_nl;
       if (wid == 0) {  // the listed cliques take their chains, in order; 32 at a time
+        nlist += s_nl;  // (diagnostics; read by warp 0 only, which alone rewrites the neighbouring s_nb)
         uint4 u = s_und;
         int nb = s_nb;
         const int nl = s_nl;
@@ -592,6 +592,7 @@ __device__ int cliques_sweep(const PrepArgs &a, const uint32_t *__restrict__ adj
             if (lane <= L) m = make_uint4(0u, 0u, 0u, 0u);
           }
         }
+        __syncwarp();  // every lane has read s_und / s_nb before lane 0 rewrites them
         if (lane == 0) {
           s_und = u;
           s_nb = nb;
