@@ -235,7 +235,13 @@ RB_API rb_status rb_index_tree_info(const rb_index *idx, int64_t *n_nodes, int64
  * index or -1 for the root / virtual nodes), rep[n_nodes] (smallest leaf
  * index below; -1 for root), prefix_off[n_nodes+1] / prefix_ids[prefix_total]
  * = each node's ordered context (X10), path_off[N+1] / path[path_total] =
- * each leaf's search path.  Any output may be NULL. */
+ * each leaf's search path.  Any output may be NULL.
+ * Node numbering: 0 = root; 1..V = the kept virtual nodes in decreasing order
+ * of their merge in the linkage's emission order (round by round; within a
+ * round the reciprocal-nearest-neighbour pairs by row, then the level cliques
+ * in greedy order), so every parent precedes its children; V+1+i = context i.
+ * The emission order is deterministic: the same input gives the same numbers
+ * on every run (after online insertions, new nodes are appended). */
 RB_API rb_status rb_index_tree(const rb_index *idx, int32_t *parent, int32_t *leaf, int32_t *rep,
                                int64_t *prefix_off, uint32_t *prefix_ids, int64_t *path_off,
                                int32_t *path);

@@ -170,13 +170,20 @@ def test_consumed_rows_linkage_equals_kept():
         assert np.array_equal(x, y)
 
 
-def test_deterministic_repeat():
-    w = generate(2000, 20, 20000, 77)
+@pytest.mark.parametrize("case", ["random", "ties"])
+def test_deterministic_repeat(case):
+    """Repeated builds give the same bytes: merge order, schedule and the
+    exported tree numbering (parent, rep, prefixes; ragb.h rb_index_tree)."""
+    w = generate(2000, 20, 20000, 77) if case == "random" else generate(6000, 3, 60000, 5)
     runs = [dev_build(w.ids, flags=0)[0] for _ in range(3)]
+    t0 = runs[0].tree()
     for r in runs[1:]:
         for x, y in zip(r.linkage(), runs[0].linkage()):
             assert np.array_equal(x, y)
         assert np.array_equal(r.order_contexts()[2], runs[0].order_contexts()[2])
+        t = r.tree()
+        for k in t0:
+            assert np.array_equal(t[k], t0[k]), k
 
 
 # ------------------------------------------------------------- full sizes
