@@ -49,7 +49,7 @@ constexpr int QCAP = 256;     // candidate-queue window per warp (entries); drai
 typedef unsigned long long u64;
 
 struct Plan {
-  int R, T, logT, S, K;
+  int R, T, logT, S, K, nseg;
   bool tab_smem, scale8;
   size_t off_tab, off_acc, off_stage, off_key, off_cb, off_plist, off_filter, off_q, off_inc, off_bar, total;
 };
@@ -87,8 +87,26 @@ __global__ void __launch_bounds__(NT, 1) k_dist_tile(DistArgs a, Plan P) {
   const int64_t N = a.N, Npad = a.Npad;
   const int64_t ntiles = (a.nrows + R - 1) / R;
   const int nch = (int)((N + CH - 1) / CH);
-  const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int64_t total = my_tiles * nch;  // chunks this CTA streams
+  // work units: row tile x column segment (nseg segments of cps chunks; more
+  // units than CTAs x waves keeps the last wave short).  A segment's row
+  // minima are combined across segments with a 64-bit atomicMin.
+  const int nseg = P.nseg, cps = (nch + nseg - 1) / nseg;
+  const int nunits = (int)(ntiles * nseg);
+  auto seg_lo = [&](int sg) { return sg * cps; };
+  auto seg_hi = [&](int sg) { return min(nch, (sg + 1) * cps); };
+  // this CTA's chunk sequence, two ahead of the one being processed (the
+  // ring prefetch): (unit, chunk) cursor
+  int la_u = (int)blockIdx.x;
+  int la_c = la_u < nunits ? seg_lo(la_u % nseg) : 0;
+  auto la_next = [&]() {  // chunk of the lookahead cursor, then advance it; -1 past the end
+    if (la_u >= nunits) return -1;
+    const int c = la_c;
+    if (++la_c >= seg_hi(la_u % nseg)) {
+      la_u += (int)gridDim.x;
+      if (la_u < nunits) la_c = seg_lo(la_u % nseg);
+    }
+    return c;
+  };
   constexpr uint32_t unit = SCALE8 ? 8u : 1u;  // accumulator unit: byte offset (8-byte entries) or index
   const uint32_t sv = (uint32_t)P.S * unit;     // one shared doc adds S (+ displacement)
   uint32_t *ring = stg + (size_t)w * 2 * K * 32;  // this warp's [2][K][32]
@@ -110,8 +128,12 @@ __global__ void __launch_bounds__(NT, 1) k_dist_tile(DistArgs a, Plan P) {
     for (int i = tid; i < (K + 1) * P.S; i += NT) reinterpret_cast<uint2 *>(smem)[i] = a.ptab[i];
   for (int i = tid; i < R * ACCW; i += NT) acc[i] = 0u;
   __syncthreads();
-  if (total > 0) issue(0, 0);
-  if (total > 1) issue(1 % nch, 1);
+  {
+    const int c0 = la_next();
+    if (c0 >= 0) issue(c0, 0);
+    const int c1 = la_next();
+    if (c1 >= 0) issue(c1, 1);
+  }
 
   uint16_t *myq = qall + w * QCAP;
   uint2 *cinfo = cinfo_all + w * 32;
@@ -122,7 +144,9 @@ __global__ void __launch_bounds__(NT, 1) k_dist_tile(DistArgs a, Plan P) {
   const uint32_t lanes_le = 0xffffffffu >> (31 - lane);
   int64_t g = 0;  // position in this CTA's chunk sequence
 
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  for (int un = (int)blockIdx.x; un < nunits; un += (int)gridDim.x) {
+    const int64_t tile = un / nseg;
+    const int sg = un - (int)tile * nseg;
     const int64_t r0 = a.row0 + tile * R;
     const int64_t rem = a.row0 + a.nrows - r0;
     const int rcount = rem < R ? (int)rem : R;
@@ -182,7 +206,7 @@ __global__ void __launch_bounds__(NT, 1) k_dist_tile(DistArgs a, Plan P) {
 #pragma unroll
     for (int q = 0; q < R / 4; ++q) bk[q] = 0xffffffffu;
 
-    for (int ch = 0; ch < nch; ++ch, ++g) {
+    for (int ch = seg_lo(sg); ch < seg_hi(sg); ++ch, ++g) {
       const int b = (int)(g & 1);
       const int64_t c0 = (int64_t)ch * CH;
       const uint32_t *sb = ring + b * K * 32;
@@ -274,9 +298,12 @@ __global__ void __launch_bounds__(NT, 1) k_dist_tile(DistArgs a, Plan P) {
       }
       // the warp is done with stage b: refill it with its chunk g + 2
       __syncwarp();
-      if (g + 2 < total) {
-        fence_proxy_async_smem();
-        issue((ch + 2) % nch, b);
+      {
+        const int cn = la_next();  // this warp's chunk g + 2 of the CTA's sequence
+        if (cn >= 0) {
+          fence_proxy_async_smem();
+          issue(cn, b);
+        }
       }
 
       // ---- finalize: lane = 4 columns x rows rr + 4q --------------------------
@@ -367,7 +394,10 @@ __global__ void __launch_bounds__(NT, 1) k_dist_tile(DistArgs a, Plan P) {
       for (int v = 0; v < NW; ++v) best = umin64(best, reinterpret_cast<const u64 *>(qall + v * QCAP)[tid]);
       if (best != ~0ull)
         best = ((u64)__float_as_uint(__ldg(a.vals + (best >> 32))) << 32) | (best & 0xffffffffull);
-      a.nnkey[r0 + tid] = best;
+      if (nseg == 1)
+        a.nnkey[r0 + tid] = best;
+      else if (best != ~0ull)
+        atomicMin(a.nnkey + r0 + tid, best);  // (value bits, column) order = (value, column) order
     }
   }
 }
@@ -418,9 +448,19 @@ cudaError_t launch(const DistArgs &a, const Plan &P, cudaStream_t st) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t ntiles = (a.nrows + R - 1) / R;
-  int64_t grid = std::min<int64_t>(ntiles, (int64_t)sms);  // one persistent CTA per SM
+  const int nch = (int)((a.N + CH - 1) / CH);
+  int64_t grid = (int64_t)sms;  // one persistent CTA per SM
   if (a.grid_cap > 0) grid = std::min<int64_t>(grid, a.grid_cap);
-  kern<<<(unsigned)grid, NT, P.total, st>>>(a, P);
+  // column segments: at least ~16 units per CTA (short last wave), segments
+  // of at least 8 chunks
+  Plan Q = P;
+  Q.nseg = (int)std::max<int64_t>(1, std::min<int64_t>((16 * grid + ntiles - 1) / ntiles, nch / 8));
+  grid = std::min<int64_t>(grid, ntiles * Q.nseg);
+  if (Q.nseg > 1) {  // partial row minima meet in a 64-bit atomicMin
+    cudaError_t e2 = cudaMemsetAsync(a.nnkey + a.row0, 0xff, (size_t)a.nrows * 8, st);
+    if (e2 != cudaSuccess) return e2;
+  }
+  kern<<<(unsigned)grid, NT, P.total, st>>>(a, Q);
   return cudaGetLastError();
 }
 

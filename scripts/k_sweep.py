@@ -1,7 +1,7 @@
 """C5 K sweep: the distance stage (a2-a4) at N = 16,384 for
 K in 5..100 -- device time (CUDA events around the library call, best of 5,
 linkage skipped), bytes written, fraction of the measured HBM copy bandwidth,
-and the full build time.  Writes profiles/r01_k_sweep.json.
+and the full build time.  Writes gpurun_out/k_sweep.json (copied to profiles/r02_k_sweep.json).
 
     python scripts/k_sweep.py
 """
