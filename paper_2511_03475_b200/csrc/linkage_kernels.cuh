@@ -653,36 +653,31 @@ __device__ int cliques_sweep(const PrepArgs &a, const uint32_t *__restrict__ adj
     // -- record the merges; eager candidate sets for the words after the block ----
     const int wn = wb + 4;  // first word after the block
     const int nw = W - wn;
-    {  // decision t of the block -> global arrays, rank within its clique
+    {  // decision t of the block -> global arrays, rank within its clique (a
+       // clique's decisions of the block are contiguous: one chain each)
       const int nd0 = s_nd;
+      const bool isd = tid < nb && !(s_bv[tid] & 0x10000);
+      const int dbefore = block_excl_scan<CT>(isd ? 1 : 0, s_wcnt);  // merges before t
+      int old = 0, newc = -1;
       if (tid < nb) {
         const int j = s_bj[tid];
         const bool start = (s_bv[tid] & 0x10000) != 0;
-        int before = 0, dbefore = 0, last = 1;  // same-clique merges before t in this block
-        for (int t2 = 0; t2 < nb; ++t2) {
-          const bool sm = s_bj[t2] == j && !(s_bv[t2] & 0x10000);
-          before += (t2 < tid && sm) ? 1 : 0;
-          last &= (t2 > tid && sm) ? 0 : 1;
-        }
-        for (int t2 = 0; t2 < tid; ++t2) dbefore += (s_bv[t2] & 0x10000) ? 0 : 1;
+        int before = 0;
+        for (int t2 = tid - 1; t2 >= 0 && s_bj[t2] == j; --t2) before += (s_bv[t2] & 0x10000) ? 0 : 1;
+        const bool last = tid + 1 >= nb || s_bj[tid + 1] != j;
         const bool fresh = j >= J0;  // created in this block: no earlier merges
-        const int old = fresh ? 0 : ccnt[j];
+        old = fresh ? 0 : ccnt[j];
         if (!start) {
           const int d = nd0 + dbefore;
           dec_j[d] = j;
           dec_v[d] = v0 + s_bv[tid];
           dec_r[d] = old + before;
-          if (last) ccnt[j] = old + before + 1;
-        } else if (last) {  // a start with no merges in this block
-          ccnt[j] = 0;
         }
+        newc = last ? old + before + (start ? 0 : 1) : -1;
       }
-      __syncthreads();
-      if (tid == 0) {
-        int c = 0;
-        for (int t = 0; t < nb; ++t) c += (s_bv[t] & 0x10000) ? 0 : 1;
-        s_nd = nd0 + c;
-      }
+      if (tid == CT - 1) s_nd = nd0 + dbefore + (isd ? 1 : 0);
+      __syncthreads();  // every thread has read its clique's count before any is rewritten
+      if (newc >= 0) ccnt[s_bj[tid]] = newc;
     }
     // eager candidate sets: CTA 0 updates the next block's words itself; with
     // helper CTAs, the words after it are theirs (sweep_update), lagging one
@@ -692,18 +687,49 @@ __device__ int cliques_sweep(const PrepArgs &a, const uint32_t *__restrict__ adj
       // the helpers are done with block b - 1: they wrote words >= wn of its
       // new cliques (plain stores this block's reductions must not precede),
       // and every word this block's listing read
+      const long long cw = clock64();
       if (tid == 0) {
         const volatile int *c = hcnt + (v0 / kSweepB - 1);
         while (*c < nhelp) __nanosleep(64);
         __threadfence();
       }
       __syncthreads();
+      tk[5] += clock64() - cw;
     }
     if (helpers) {
       for (int t = tid; t < nb; t += CT) logb[(size_t)(v0 / kSweepB) * kSweepB + t] = make_int2(s_bj[t], s_bv[t]);
       if (tid == 0) logn[v0 / kSweepB] = nb;
     }
-    if (wend > wn) sweep_update(adj, W, I, WI, v0, s_bj, s_bv, nb, wn, wend, wid, CT / 32, lane);
+    if (helpers) {
+      // the next block's 4 words: one thread per decision (16-byte store of a
+      // new clique's words; reductions for a member of an existing clique)
+      if (tid < nb && wn < W) {
+        const int j = s_bj[tid], v = s_bv[tid];
+        uint32_t *dst = I + (size_t)j * WI + wn;
+        if (v & 0x10000) {
+          const uint32_t *src = adj + (size_t)(v0 + (v & 0xffff)) * W + wn;
+          uint32_t x[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) x[q] = wn + q < W ? __ldg(src + q) : 0u;
+          for (int t2 = tid + 1; t2 < nb && s_bj[t2] == j; ++t2) {
+            const uint32_t *m = adj + (size_t)(v0 + s_bv[t2]) * W + wn;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) x[q] &= wn + q < W ? __ldg(m + q) : 0u;
+          }
+          *reinterpret_cast<uint4 *>(dst) = make_uint4(x[0], x[1], x[2], x[3]);
+        } else if (j < J0) {  // members of a clique new in this block are folded into its start's store
+          const uint32_t *src = adj + (size_t)(v0 + v) * W + wn;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (wn + q < W) {
+              const uint32_t xv = __ldg(src + q);
+              if (xv != 0xffffffffu) atomicAnd(dst + q, xv);
+            }
+        }
+      }
+    } else if (wend > wn) {
+      sweep_update(adj, W, I, WI, v0, s_bj, s_bv, nb, wn, wend, wid, CT / 32, lane);
+    }
     if (helpers) {
       __threadfence();
       __syncthreads();
@@ -726,6 +752,7 @@ __device__ int cliques_sweep(const PrepArgs &a, const uint32_t *__restrict__ adj
     a.cstat[5] = (int)(tk[2] >> 10);
     a.cstat[6] = (int)(tk[3] >> 10);
     a.cstat[7] = (int)(tk[4] >> 10);
+    a.cstat[4] = (int)(tk[5] >> 10);  // waits for the helpers (inside tk[4])
   }
   // -- greedy order: counting sort of the decisions by clique --------------------
   const int J = s_J, nd = s_nd;
