@@ -407,6 +407,7 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
     std::mutex mu;
     std::condition_variable cv;
     int64_t avail = 0;
+    std::vector<int64_t> ends;  // merge count at the end of every round so far (the replay sorts round by round)
     bool finished = false;
     cudaError_t copy_err = cudaSuccess;
     int cur_dev = 0;
@@ -419,6 +420,8 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
       cudaStream_t cs = nullptr;
       cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
       int64_t have = 0;
+      size_t ne = 0;
+      std::vector<int64_t> my_ends;
       for (;;) {
         int64_t upto;
         bool fin;
@@ -427,6 +430,8 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
           cv.wait(lk, [&] { return avail > T.done || finished; });
           upto = avail;
           fin = finished;
+          my_ends.assign(ends.begin() + ne, ends.end());
+          ne = ends.size();
         }
         if (upto > have) {
           const size_t n = (size_t)(upto - have);
@@ -445,6 +450,7 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
           }
           have = upto;
         }
+        for (int64_t e : my_ends) ragb::host_replay(H, T, e);  // round by round
         ragb::host_replay(H, T, upto);
         if (!T.ok || (fin && T.done >= upto)) break;
       }
@@ -456,6 +462,7 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
           {
             std::lock_guard<std::mutex> lk(mu);
             avail = upto;
+            ends.push_back(upto);
           }
           cv.notify_one();
         },

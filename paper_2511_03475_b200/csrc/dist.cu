@@ -549,9 +549,12 @@ rb_status build_index_dist(rb_dist *d, const uint32_t *ids_d, const uint8_t *len
   std::mutex mu;
   std::condition_variable cv;
   int64_t avail = 0;
+  std::vector<int64_t> ends;  // merge count at the end of every round (the replay sorts round by round)
   bool finished = false;
   std::thread worker([&] {
     host_begin(H, T);
+    size_t ne = 0;
+    std::vector<int64_t> my_ends;
     for (;;) {
       int64_t upto;
       bool fin;
@@ -560,7 +563,10 @@ rb_status build_index_dist(rb_dist *d, const uint32_t *ids_d, const uint8_t *len
         cv.wait(lk, [&] { return avail > T.done || finished; });
         upto = avail;
         fin = finished;
+        my_ends.assign(ends.begin() + ne, ends.end());
+        ne = ends.size();
       }
+      for (int64_t e2 : my_ends) host_replay(H, T, e2);
       host_replay(H, T, upto);
       if (!T.ok || (fin && T.done >= upto)) break;
     }
@@ -647,6 +653,7 @@ rb_status build_index_dist(rb_dist *d, const uint32_t *ids_d, const uint8_t *len
       {
         std::lock_guard<std::mutex> lk(mu);
         avail = zdone;
+        ends.push_back(zdone);
       }
       cv.notify_one();
     }

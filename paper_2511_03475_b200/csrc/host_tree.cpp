@@ -123,6 +123,24 @@ void host_replay(HostIndex &H, TreeBuild &T, int64_t upto) {
   const int32_t K = H.K;
   const bool uniform = H.lens.empty();
   const int64_t t_from = T.done;
+  // a round's merges arrive in the device's emission order, which is not
+  // deterministic (reciprocal pairs are appended with atomics).  Sorted by key
+  // (X9) they are still a valid replay order — the round's reciprocal pairs
+  // are disjoint, and a level clique's picks merge into its start with
+  // increasing keys — and the same on every run, so are the raw node numbers
+  // and the exported tree numbering (ragb.h rb_index_tree).
+  if (H.sort_merges && upto > t_from + 1) {
+    std::vector<MergeKey> b((size_t)(upto - t_from));
+    for (int64_t t = t_from; t < upto; ++t) b[t - t_from] = {H.zh[t], H.za[t], H.zb[t], H.zs[t]};
+    std::sort(b.begin(), b.end(), key_less);
+    for (int64_t t = t_from; t < upto; ++t) {
+      const MergeKey &m = b[t - t_from];
+      H.zh[t] = m.h;
+      H.za[t] = m.a;
+      H.zb[t] = m.b;
+      H.zs[t] = m.size;
+    }
+  }
   for (int64_t t = T.done; t < upto && T.ok; ++t) {
     const int32_t a = H.za[t], b = H.zb[t];
     if (a < 0 || b >= N || a >= b || T.cur[a] < 0 || T.cur[b] < 0 ||
@@ -183,8 +201,7 @@ void host_replay(HostIndex &H, TreeBuild &T, int64_t upto) {
   // only merges the sorted runs
   if (T.ok && H.sort_merges && T.done > t_from) {
     if (T.runs.empty()) T.runs.push_back(0);
-    for (int64_t t = t_from; t < T.done; ++t) T.zk.push_back({H.zh[t], H.za[t], H.zb[t], H.zs[t]});
-    std::sort(T.zk.begin() + t_from, T.zk.end(), key_less);
+    for (int64_t t = t_from; t < T.done; ++t) T.zk.push_back({H.zh[t], H.za[t], H.zb[t], H.zs[t]});  // sorted above
     T.runs.push_back((int64_t)T.zk.size());
   }
 }

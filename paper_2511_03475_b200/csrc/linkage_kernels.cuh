@@ -181,14 +181,17 @@ __global__ void k_prep_rnn(PrepArgs a) {
     const bool dead = kx == kDead;  // row merged away by an in-place round
     int lead = dead ? -1 : x;
     a.alive[x] = (!dead && hx == h) ? 1 : 0;
-    int emit = 0;  // x < y of an RNN pair: emitted by k_prep_list in row order (deterministic)
     if (!dead && hx > h && (int)(a.key[y] & 0xffffffffu) == x) {
-      if (y < x)
+      if (y < x) {
         lead = y;
-      else
-        emit = 1;
+      } else {  // emission order within the round is arbitrary: the host replays each round sorted by key
+        const int pos = atomicAdd(a.zcount, 1);
+        a.za[pos] = a.rep[x];
+        a.zb[pos] = a.rep[y];
+        a.zh[pos] = a.vals ? a.vals[hx] : __uint_as_float(hx);
+        a.zs[pos] = a.sz[x] + a.sz[y];
+      }
     }
-    a.candB[x] = emit;
     a.leader[x] = lead;
   }
 }
@@ -198,29 +201,7 @@ __global__ void __launch_bounds__(PT, 1) k_prep_list(PrepArgs a) {
   const uint8_t *alive = a.alive;
   const int nlist = block_compact(
       a.M, [&](int i) { return alive[i] != 0; }, [&](int i) { return i; }, a.list, S);
-  // the round's RNN pairs, emitted in row order after the merges so far (a
-  // deterministic emission order: the replay, and the tree's node numbering
-  // that follows it, are the same on every run)
-  const int z0 = *a.zcount;
-  const int *emit = a.candB;
-  const int nr = block_scan_all(
-      a.M, [&](int i) { return emit[i]; },
-      [&](int x, int pre) {
-        if (!emit[x]) return;
-        const u64 kx = a.key[x];
-        const unsigned hx = (unsigned)(kx >> 32);
-        const int y = (int)(kx & 0xffffffffu);
-        const int pos = z0 + pre;
-        a.za[pos] = a.rep[x];
-        a.zb[pos] = a.rep[y];
-        a.zh[pos] = a.vals ? a.vals[hx] : __uint_as_float(hx);
-        a.zs[pos] = a.sz[x] + a.sz[y];
-      },
-      S);
-  if (threadIdx.x == 0) {
-    a.level[0] = nlist;
-    *a.zcount = z0 + nr;
-  }
+  if (threadIdx.x == 0) a.level[0] = nlist;
 }
 
 // Round step 2 (grid): adjacency bits of the level graph, adj[i][w] bit j <=>
