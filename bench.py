@@ -330,14 +330,22 @@ def run_ours(args, ws, rank, local):
         q = generate(10_000, K, 1_000_000, 4004).ids
         online = {"workload": "10,000 new contexts (K=20, V=1e6, seed 4004) searched + inserted + ordered "
                               "into the C4 index (rb_order_contexts, ids != NULL)"}
+        warm = build(ids_dev)  # first use of the online kernel and its buffers (module load, cudaMalloc)
+        warm.set_online(1)
+        warm.order_new(q[:256])
+        del warm
         for mode, key in ((1, "device_root_scores"), (0, "host_only")):
-            oi = build(ids_dev)
-            torch.cuda.synchronize()
-            oi.set_online(mode)
-            t0 = time.perf_counter()
-            oi.order_new(q)
-            online[key] = {"contexts_per_s": 10_000 / (time.perf_counter() - t0)}
-            del oi
+            best = None
+            for _ in range(2):  # best of two (fresh index each time)
+                oi = build(ids_dev)
+                torch.cuda.synchronize()
+                oi.set_online(mode)
+                t0 = time.perf_counter()
+                oi.order_new(q)
+                dt = time.perf_counter() - t0
+                best = dt if best is None else min(best, dt)
+                del oi
+            online[key] = {"contexts_per_s": 10_000 / best}
 
     if rank != 0:
         return
