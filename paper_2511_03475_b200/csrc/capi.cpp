@@ -154,7 +154,7 @@ ScratchLayout ScratchLayout::make(int64_t N, int32_t K, bool keep_rows, bool lin
     L.aux3 = take(o, (size_t)(N + 8) * 4);
     L.aux4 = take(o, (size_t)2 * N * 4);
     L.alive = take(o, (size_t)N);
-    L.pmap = take(o, (size_t)(N + 8) * 8);
+    L.pmap = take(o, (size_t)(N + 128) * 8);
     L.za = take(o, (size_t)N * 4);
     L.zb = take(o, (size_t)N * 4);
     L.zh = take(o, (size_t)N * 4);
@@ -579,6 +579,9 @@ rb_status rb_index_from_linkage(const uint32_t *ids_host, const uint8_t *lens_ho
     H.zs.assign(size, size + N - 1);
   }
   std::string msg;
+#ifdef RAGB_HOST_TRACE
+  H.trace = true;  // host-stage laps on stderr (variant build for host profiling)
+#endif
   rb_status s = ragb::host_build(H, &msg);
   if (s != RB_OK) {
     delete idx;

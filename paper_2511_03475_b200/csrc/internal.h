@@ -33,7 +33,7 @@ inline int64_t padded_cols(int64_t N) { return round_up(N, kChunk); }
 struct ScratchLayout {
   size_t err, idsT, nnkey, stage_ids, stage_lens, lut, lutc, vals, key0, key1, rep0, rep1, sz0, sz1, leader, aux0, aux1, aux2, aux3, aux4,
       alive, za, zb, zh, zs, amask, mlist, counters, matA, matB, total;
-  size_t pmap;         // code mode: int2 [N + 8] new column -> (leader, pair member)
+  size_t pmap;         // code mode: int2 [N + 128] new column -> (leader, pair member), or the compact map
   size_t codes, mat16;  // code mode (inside matA): [N][N] codes, then the first compacted code matrix
   size_t ptab;          // tile path: packed Eq. 1 table (value, code << 16) [(K+1) * (K*K/2+1)]
   static ScratchLayout make(int64_t N, int32_t K, bool keep_rows, bool linkage);

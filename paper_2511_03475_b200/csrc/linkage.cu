@@ -106,8 +106,28 @@ cudaError_t launch_merge(const T *cur, int64_t ld, int M, int Mn, const PrepArgs
   const bool wide16 = M > 16 * 1024;
   auto gkern = wide16 ? (vec16 ? k_merge_gather<true, 1024> : k_merge_gather<false, 1024>)
                       : (vec16 ? k_merge_gather<true, 256> : k_merge_gather<false, 256>);
-  const size_t glim = sizeof(T) == 2 && pa.pmap ? dyn_smem_limit(gkern) : 0;
-  if (sizeof(T) == 2 && pa.pmap && row_bytes <= glim && tu.gather != 0) {
+  const bool compact = sizeof(T) == 2 && pa.pmap && pa.nclq && pm32_fits(M, Mn);  // k_compact_maps wrote pm32
+  if (compact && tu.gather != 0) {
+    // code mode with the compact map: k_merge_gather2 when the old row fits
+    auto kern = wide16 ? (vec16 ? k_merge_gather2<true, 1024> : k_merge_gather2<false, 1024>)
+                       : (vec16 ? k_merge_gather2<true, 256> : k_merge_gather2<false, 256>);
+    const size_t lim = dyn_smem_limit(kern);
+    if (row_bytes <= lim) {
+      const int db = vec16 && 2 * row_bytes <= lim ? 1 : 0;  // double-buffered rows
+      const size_t smem = row_bytes * (1 + db);
+      const int nth = wide16 ? 1024 : 256;
+      const int per_sm = occupancy_cached(kern, nth, smem);
+      if (per_sm < 1) return cudaErrorInvalidConfiguration;
+      *paths |= wide16 ? RB_PATH_GATHER_WIDE : RB_PATH_GATHER;
+      const int grid = std::min<int>(Mn, sms * per_sm);
+      kern<<<grid, nth, smem, st>>>(reinterpret_cast<const uint16_t *>(cur), ld, M, pa.Mn, pa.goff, pa.gmem,
+                                    reinterpret_cast<const uint32_t *>(pa.pmap), pa.nclq,
+                                    reinterpret_cast<uint16_t *>(next), keyn, db);
+      return cudaGetLastError();
+    }
+  }
+  const size_t glim = sizeof(T) == 2 && pa.pmap && !compact ? dyn_smem_limit(gkern) : 0;
+  if (sizeof(T) == 2 && pa.pmap && !compact && row_bytes <= glim && tu.gather != 0) {
     // code mode, old row fits in shared memory: gather form (k_merge_gather)
     const uint16_t *c16 = reinterpret_cast<const uint16_t *>(cur);
     uint16_t *n16 = reinterpret_cast<uint16_t *>(next);
@@ -207,6 +227,7 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
   pa.Mn = counters + 1;
   pa.level = counters + 2;
   pa.sweep_ctl = counters + 14;  // 0 between launches (reset by the sweep's CTA 0)
+  pa.nclq = codes ? counters + 15 : nullptr;
   pa.cstat = counters + 4;
   pa.vals = codes ? cm->vals : nullptr;
   pa.pmap = codes ? at<int2>(scratch, L.pmap) : nullptr;

@@ -82,6 +82,8 @@ struct PrepArgs {
   int *rep_n, *sz_n;
   int *Mn;
   int2 *pmap;  // [Mn + 8] new column -> (leader, other member of a pair | -1 singleton | -2 larger), or nullptr
+               // (when pm32_fits: the same buffer holds the compact map pm32 and the clique list, see k_compact_maps)
+  int *nclq;   // groups of 3+ members listed after pm32 (compact map only)
   int *level;  // [0] level list length, [1] h bits
   int *cstat;  // clique diagnostics: starts, batches, picks, candidates, level n, clk/1k (warp0, pass)
   int *sweep_ctl;  // level-clique sweep with helper CTAs: published block count (0 between launches), or nullptr
@@ -862,7 +864,10 @@ __global__ void __launch_bounds__(PT, 1) k_compact_scan1(PrepArgs a) {
     a.cursor[g] = 0;
     a.sz_n[g] = 0;
   }
-  if (threadIdx.x == 0) *a.Mn = Mn;
+  if (threadIdx.x == 0) {
+    *a.Mn = Mn;
+    if (a.nclq) *a.nclq = 0;
+  }
 }
 
 __global__ void k_compact_groups(PrepArgs a) {
@@ -893,12 +898,30 @@ __global__ void k_compact_members(PrepArgs a) {
   }
 }
 
+// Compact gather map (k_merge_gather2): new column t -> one 32-bit word
+//   (x - t) | (y - t) << 15
+// x = the group's leader (its smallest member), y = the other member of a
+// 2-member group, else x (a singleton; or a group of 3+ members, whose other
+// members are folded into x's slot before the gather — those groups are listed
+// after the map).  Order-preserving compaction puts x at or after t and every
+// member below M: it fits when M - Mn < 2^15 and M <= 2^17.
+__host__ __device__ constexpr bool pm32_fits(int M, int Mn) { return M <= (1 << 17) && M - Mn < (1 << 15); }
+// The map is padded to a multiple of 128 words (zeros); the clique list
+// follows.
+__host__ __device__ constexpr int pm32_words(int Mn) { return (Mn + 127) & ~127; }
+__device__ __forceinline__ int pm32_index(int t) { return t; }
+__device__ __forceinline__ uint32_t *pm32_of(const PrepArgs &a) { return reinterpret_cast<uint32_t *>(a.pmap); }
+__device__ __forceinline__ int *clq_of(const PrepArgs &a, int Mn) {
+  return reinterpret_cast<int *>(pm32_of(a) + pm32_words(Mn));
+}
+
 // old column -> new column | writer class << 29 (k_merge_rows): 0 the
 // group's leader (smallest member), 1 the other member of a 2-member group,
 // 2 a non-leader of a larger group; new column -> its leader (first_old,
-// in cursor, free after the member scatter); pmap for k_merge_gather
+// in cursor, free after the member scatter); pmap (or pm32) for the gather
 __global__ void k_compact_maps(PrepArgs a) {
   const int M = a.M, Mn = *a.Mn;
+  const bool compact = a.pmap && a.nclq && pm32_fits(M, Mn);
   const int i0 = blockIdx.x * blockDim.x + threadIdx.x;
   for (int x = i0; x < M; x += gridDim.x * blockDim.x) {
     const int l = a.leader[x];
@@ -907,7 +930,18 @@ __global__ void k_compact_maps(PrepArgs a) {
     const int cls = (l == x || l < 0) ? 0 : (gs == 2 ? 1 : 2);
     a.colsrc[x] = g < 0 ? -1 : (g | (cls << 29));
     if (l == x) a.cursor[g] = x;
-    if (a.pmap && g >= 0) {
+    if (compact) {
+      if (l == x) {
+        int y = x;
+        if (gs == 2) {
+          const int m0 = a.gmem[a.goff[g]];
+          y = m0 == x ? a.gmem[a.goff[g] + 1] : m0;
+        } else if (gs > 2) {
+          clq_of(a, Mn)[atomicAdd(a.nclq, 1)] = g;
+        }
+        pm32_of(a)[pm32_index(g)] = (uint32_t)(x - g) | ((uint32_t)(y - g) << 15);
+      }
+    } else if (a.pmap && g >= 0) {
       if (l == x) {
         a.pmap[g].x = x;
         if (gs == 1) a.pmap[g].y = -1;
@@ -916,8 +950,12 @@ __global__ void k_compact_maps(PrepArgs a) {
       }
     }
   }
+  if (compact)
+    for (int t = Mn + i0; t < pm32_words(Mn); t += gridDim.x * blockDim.x) pm32_of(a)[pm32_index(t)] = 0u;
   if (i0 < 8) {
-    if (a.pmap) a.pmap[Mn + i0] = make_int2(0, -1);  // padding of the last vector
+    if (compact) {
+    } else if (a.pmap)
+      a.pmap[Mn + i0] = make_int2(0, -1);  // padding of the last vector
     a.colsrc[M + i0] = -1;  // padding for 16-byte colmap loads (8 codes per vector)
   }
 }
@@ -1331,6 +1369,241 @@ __global__ void __launch_bounds__(NTH) k_merge_gather(const uint16_t *__restrict
 #pragma unroll
       for (int k = 1; k < NTH / 32; ++k) b = wmin[k] < b ? wmin[k] : b;
       keyn[c] = b;
+    }
+  }
+}
+
+// Code-mode compaction with the compact map (pm32_fits): one CTA per new row c.
+// Phase 1 as k_merge_gather (the first member's old row by bulk copies, the
+// other members folded in); the members of every 3+-member group are folded
+// into its leader's slot; then new column t is
+//   max(s[x], s[y]),  x = t + (pm32[t] & 0x7fff),  y = t + (pm32[t] >> 15)
+// (y == x for a singleton), with no per-column branch.  A thread takes 4
+// consecutive new columns per step (one 16-byte map load, one 8-byte store).
+// The row's own members are read only for new column c (groups are disjoint),
+// whose value the thread holding it replaces by 0xffff (above every code: out
+// of the row minimum) and the row's finisher by the diagonal 0.
+// Warps never wait for each other on rows without folds: they take the row's
+// data from the bulk-copy barrier, fold their row minimum into a shared word
+// with an atomic, and count themselves out; the last warp out finishes the
+// row (key, diagonal) and refills the buffer: in double-buffered mode with
+// the row two ahead, otherwise progressively — every old column the gather
+// reads for new column t is >= t, so once every warp is past a chunk of new
+// columns, the old columns below it are dead for this row and the last warp
+// out of the chunk copies the next row's first member into them; the
+// columns past the gathered range follow when the row is done.
+template <bool VEC, int NTH>
+__global__ void __launch_bounds__(NTH) k_merge_gather2(const uint16_t *__restrict__ D, int64_t ld, int M,
+                                                       const int *__restrict__ Mn_p, const int *__restrict__ goff,
+                                                       const int *__restrict__ gmem, const uint32_t *__restrict__ pm,
+                                                       const int *__restrict__ nclq_p, uint16_t *__restrict__ Dn,
+                                                       u64 *__restrict__ keyn, int db) {
+  constexpr int NWARP = NTH / 32;
+  constexpr int kMaxChunks = 32;  // chunks per row (progressive refill needs Mn / (4 * CQ) <= kMaxChunks)
+  extern __shared__ __align__(16) uint4 smem4[];  // [1 + db][ceil(M / 8)]
+  __shared__ __align__(8) unsigned long long bar[2];
+  __shared__ u64 rowmin[2];               // per row parity: (code << 32 | column) minimum
+  __shared__ int row_done[2];             // per row parity: warps done with the row
+  __shared__ int chunk_done[kMaxChunks];  // warps done with each chunk (progressive refill)
+  const int Mn = *Mn_p, nclq = *nclq_p;
+  const int *__restrict__ clq = reinterpret_cast<const int *>(pm + pm32_words(Mn));
+  const int64_t ldn = mat_ld<uint16_t>(Mn);
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int MV = (M + 7) >> 3;
+  const int G = (int)gridDim.x;
+  unsigned parity = 0u;  // bit b: phase parity of bar[b]
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    rowmin[0] = rowmin[1] = ~0ull;
+    row_done[0] = row_done[1] = 0;
+  }
+  if (tid < kMaxChunks) chunk_done[tid] = 0;
+  __syncthreads();
+  // one thread: bulk copies of 16-byte vectors [v0, v1) of row `row`'s first
+  // member into slot (the barrier is armed separately, once per row)
+  auto copy = [&](int row, int slot, int v0, int v1) {
+    fence_proxy_async_smem();  // earlier generic accesses of the buffer come first
+    const unsigned char *src = reinterpret_cast<const unsigned char *>(D + (int64_t)gmem[goff[row]] * ld) + (size_t)v0 * 16;
+    unsigned char *dst = reinterpret_cast<unsigned char *>(smem4 + (size_t)slot * MV + v0);
+    const unsigned bytes = (unsigned)(v1 - v0) * 16u;
+    for (unsigned o = 0; o < bytes; o += 32768u) bulk_g2s(dst + o, src + o, min(32768u, bytes - o), &bar[slot]);
+  };
+  if (VEC && tid == 0) {
+    for (int k = 0; k <= db; ++k)
+      if ((int)blockIdx.x + k * G < Mn) {
+        mbar_expect_tx(&bar[k], (unsigned)MV * 16u);
+        copy(blockIdx.x + k * G, k, 0, MV);
+      }
+  }
+  const uint4 *__restrict__ pm4 = reinterpret_cast<const uint4 *>(pm);
+  const int nq = pm32_words(Mn) >> 2;  // quads of columns (the last ones: padding)
+  constexpr int UP = 4;
+  constexpr int CQ = NTH * UP;  // quads per chunk
+  const bool progressive_ok = VEC && !db && nq <= kMaxChunks * CQ;
+  int it = 0;
+  for (int c = blockIdx.x; c < Mn; c += G, ++it) {
+    const int rb = goff[c], re = goff[c + 1];
+    const int slot = db ? (it & 1) : 0;
+    const int rp = it & 1;  // row parity: at most two rows are in flight per CTA
+    const int cn = c + G;   // this CTA's next row
+    const bool progressive = progressive_ok && cn < Mn;
+    uint4 *srow4 = smem4 + (size_t)slot * MV;
+    uint16_t *srow = reinterpret_cast<uint16_t *>(srow4);
+    // ---- phase 1: old row(s) -> shared memory ---------------------------------
+    if (!VEC) {  // old rows not 16-byte aligned (the distance kernel's codes with N % 8 != 0)
+      __syncthreads();  // the previous row's reads are done
+      for (int x = tid; x < M; x += NTH) {
+        unsigned v = 0u;
+        for (int rr = rb; rr < re; ++rr) v = max(v, (unsigned)__ldcs(D + (int64_t)gmem[rr] * ld + x));
+        srow[x] = (uint16_t)v;
+      }
+    } else {
+      mbar_wait(&bar[slot], (parity >> slot) & 1u);
+      parity ^= 1u << slot;
+      if (tid == 0 && cn < Mn) {
+        // the next row's folded members (read with plain loads) and, in
+        // progressive mode, the part of its first member copied after this
+        // row: into L2 now, while this row is gathered
+        const int nb = goff[cn], ne = goff[cn + 1];
+        for (int rr = nb + 1; rr < ne; ++rr) {
+          const unsigned char *src = reinterpret_cast<const unsigned char *>(D + (int64_t)gmem[rr] * ld);
+          for (unsigned o = 0; o < (unsigned)MV * 16u; o += 65536u) bulk_prefetch_l2(src + o, min(65536u, (unsigned)MV * 16u - o));
+        }
+        if (progressive) {
+          const unsigned v0 = (unsigned)((4 * ((nq - 1) / CQ * CQ)) >> 3);  // the last chunk's copy
+          if ((int)v0 < MV)
+            bulk_prefetch_l2(reinterpret_cast<const unsigned char *>(D + (int64_t)gmem[nb] * ld) + (size_t)v0 * 16,
+                             ((unsigned)MV - v0) * 16u);
+        }
+      }
+    }
+    if (VEC && re - rb > 1) {
+      constexpr int UV = 8;
+      __syncthreads();  // every warp has the row's first member (its writes below are seen by all)
+      for (int qb = tid; qb < MV; qb += NTH * UV) {
+        uint4 v[UV];
+#pragma unroll
+        for (int u = 0; u < UV; ++u) {
+          const int q = qb + u * NTH;
+          v[u] = make_uint4(0, 0, 0, 0);
+          for (int rr = rb + 1; rr < re; ++rr)
+            if (q < MV) v[u] = vmax4<uint16_t>(v[u], __ldcs(reinterpret_cast<const uint4 *>(D + (int64_t)gmem[rr] * ld) + q));
+        }
+#pragma unroll
+        for (int u = 0; u < UV; ++u) {
+          const int q = qb + u * NTH;
+          if (q < MV) srow4[q] = vmax4<uint16_t>(srow4[q], v[u]);
+        }
+      }
+    }
+    if (nclq > 0) {
+      __syncthreads();
+      for (int i = tid; i < nclq; i += NTH) {  // 3+-member groups: members folded into the leader's slot
+        const int g = clq[i];
+        unsigned v = 0u;
+        for (int r = goff[g]; r < goff[g + 1]; ++r) v = max(v, (unsigned)srow[gmem[r]]);
+        srow[g + (int)(pm[pm32_index(g)] & 0x7fffu)] = (uint16_t)v;
+      }
+    }
+    if (!VEC || re - rb > 1 || nclq > 0) __syncthreads();
+    // ---- phase 2: gather -------------------------------------------------------
+    uint2 *__restrict__ out4 = reinterpret_cast<uint2 *>(Dn + (int64_t)c * ldn);
+    const int qc = c >> 2;  // the quad holding the diagonal
+    // row minimum per thread: value << 16 | step << 2 | k (steps in increasing
+    // column order: the strict minimum keeps the smallest column, X8)
+    unsigned kmin = 0xffffffffu;
+    // thread quads q = tid + j * NTH (columns 4q .. 4q + 3); the map words of
+    // quad j + UP are loaded while quad j is gathered (UP loads in flight per
+    // thread at all times)
+    uint4 e[UP];
+#pragma unroll
+    for (int u = 0; u < UP; ++u) {
+      const int q = u * NTH + tid;
+      e[u] = q < nq ? __ldg(pm4 + q) : make_uint4(0u, 0u, 0u, 0u);
+    }
+    unsigned step = 0;
+    for (int qb = 0, ch = 0; qb < nq; qb += CQ, ++ch) {
+#pragma unroll
+      for (int u = 0; u < UP; ++u, ++step) {
+        const int q = qb + u * NTH + tid;
+        const uint4 ec = e[u];
+        const int qn = q + CQ;
+        e[u] = qn < nq ? __ldg(pm4 + qn) : make_uint4(0u, 0u, 0u, 0u);
+        if (4 * q + 3 < Mn) {
+          const int t = 4 * q;
+          const unsigned ev[4] = {ec.x, ec.y, ec.z, ec.w};
+          unsigned v[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            v[k] = max((unsigned)srow[t + k + (int)(ev[k] & 0x7fffu)], (unsigned)srow[t + k + (int)(ev[k] >> 15)]);
+          if (q == qc) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v[k] = t + k == c ? 0xffffu : v[k];
+          }
+          __stcs(out4 + q, make_uint2(v[0] | (v[1] << 16), v[2] | (v[3] << 16)));
+          const unsigned sb = step << 2;
+          kmin = min(kmin, min(min((v[0] << 16) | sb, (v[1] << 16) | sb | 1u), min((v[2] << 16) | sb | 2u, (v[3] << 16) | sb | 3u)));
+        } else if (4 * q < Mn) {  // the last, partial quad
+          const int t = 4 * q;
+          const unsigned ev[4] = {ec.x, ec.y, ec.z, ec.w};
+          const unsigned sb = step << 2;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (t + k < Mn) {
+              const unsigned v = t + k == c ? 0xffffu
+                                            : max((unsigned)srow[t + k + (int)(ev[k] & 0x7fffu)],
+                                                  (unsigned)srow[t + k + (int)(ev[k] >> 15)]);
+              Dn[(int64_t)c * ldn + t + k] = (uint16_t)v;
+              kmin = min(kmin, (v << 16) | sb | (unsigned)k);
+            }
+        }
+      }
+      if (progressive) {
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence_block();  // this warp's reads of the chunk come first
+          if (atomicAdd(&chunk_done[ch], 1) == NWARP - 1) {  // every warp is past this chunk
+            if (ch == 0) mbar_expect_tx(&bar[0], (unsigned)MV * 16u);  // the next row's phase
+            // after the last chunk the whole buffer is free: the rest of the row
+            const int vlo = (4 * qb) >> 3, vhi = qb + CQ >= nq ? MV : (4 * (qb + CQ)) >> 3;
+            if (vhi > vlo) copy(cn, 0, vlo, vhi);
+          }
+        }
+      }
+    }
+    u64 best = ~0ull;
+    if (kmin != 0xffffffffu && (kmin >> 16) != 0xffffu) {  // decode (step, k) -> column
+      const unsigned st_ = (kmin >> 2) & 0x3fffu;
+      const int t = 4 * ((int)(st_ / UP) * CQ + (int)(st_ % UP) * NTH + tid) + (int)(kmin & 3u);
+      best = ((u64)(kmin >> 16) << 32) | (unsigned)t;
+    }
+    best = umin64(best, __shfl_xor_sync(0xffffffffu, best, 16));
+    best = umin64(best, __shfl_xor_sync(0xffffffffu, best, 8));
+    best = umin64(best, __shfl_xor_sync(0xffffffffu, best, 4));
+    best = umin64(best, __shfl_xor_sync(0xffffffffu, best, 2));
+    best = umin64(best, __shfl_xor_sync(0xffffffffu, best, 1));
+    __syncwarp();
+    if (lane == 0) {
+      if (best != ~0ull) atomicMin(&rowmin[rp], best);
+      __threadfence_block();  // this warp's reads and stores of the row come first
+      if (atomicAdd(&row_done[rp], 1) == NWARP - 1) {  // the last warp out finishes the row
+        __threadfence_block();
+        const u64 b = atomicExch(&rowmin[rp], ~0ull);
+        row_done[rp] = 0;
+        keyn[c] = b;
+        Dn[(int64_t)c * ldn + c] = 0;  // the diagonal, after every warp's stores
+        if (VEC && db) {
+          if (c + 2 * G < Mn) {  // this buffer's next row
+            mbar_expect_tx(&bar[slot], (unsigned)MV * 16u);
+            copy(c + 2 * G, slot, 0, MV);
+          }
+        } else if (VEC && cn < Mn) {
+          for (int k = 0; k < kMaxChunks; ++k) chunk_done[k] = 0;
+          if (!progressive) mbar_expect_tx(&bar[0], (unsigned)MV * 16u);  // else armed at chunk 0
+          if (!progressive) copy(cn, 0, 0, MV);  // (progressive: the chunks' copies cover the row)
+        }
+      }
     }
   }
 }
