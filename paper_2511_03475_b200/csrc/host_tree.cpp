@@ -294,8 +294,6 @@ rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg) {
   // 1..V in decreasing merge index, so every parent precedes its children.
   std::vector<int64_t> vraw;
   std::vector<int32_t> vpar;
-  vraw.reserve(nz);
-  vpar.reserve(nz);
   H.lparent.assign(N, 0);
   {
     // raw parents and collapse flags come from the replay; the top merge (no
@@ -310,17 +308,57 @@ rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg) {
           keep[t] = n1 == 0 ? 0 : 1;
         }
     }
+    // kept node ids in decreasing merge index (a suffix count of the flags,
+    // chunked over the threads)
     std::vector<int32_t> eff(nz);  // kept node id standing for raw merge t
-    for (int64_t t = nz - 1; t >= 0; --t) {
-      const int64_t p = rpar[N + t];
-      const int32_t pe = p < 0 ? 0 : eff[p - N];
-      if (keep[t]) {
-        vraw.push_back(N + t);
-        vpar.push_back(pe);
-        eff[t] = (int32_t)vraw.size();
-      } else {
-        eff[t] = pe;
+    const int nc = std::max(1, std::min<int>(nth, (int)(nz / 8192) + 1));
+    std::vector<int64_t> ccount(nc + 1, 0);
+#pragma omp parallel for num_threads(nc) schedule(static, 1)
+    for (int c = 0; c < nc; ++c) {  // chunk c covers t in [hi - ..., hi) from the top
+      const int64_t t1 = nz - nz * c / nc, t0 = nz - nz * (c + 1) / nc;
+      int64_t k = 0;
+      for (int64_t t = t0; t < t1; ++t) k += keep[t];
+      ccount[c + 1] = k;
+    }
+    for (int c = 0; c < nc; ++c) ccount[c + 1] += ccount[c];
+    const int64_t V0 = ccount[nc];
+    vraw.resize(V0);
+    vpar.resize(V0);
+    // up[t]: t itself if kept (or top), else its raw parent merge; pointer
+    // doubling gives every merge its nearest kept ancestor-or-self
+    std::vector<int64_t> up(nz);
+#pragma omp parallel for num_threads(nc) schedule(static, 1)
+    for (int c = 0; c < nc; ++c) {
+      const int64_t t1 = nz - nz * c / nc, t0 = nz - nz * (c + 1) / nc;
+      int32_t id = (int32_t)ccount[c];
+      for (int64_t t = t1 - 1; t >= t0; --t) {
+        if (keep[t]) {
+          eff[t] = ++id;
+          vraw[id - 1] = N + t;
+        }
+        const int64_t p = rpar[N + t];
+        up[t] = (keep[t] || p < 0) ? t : p - N;
       }
+    }
+    for (bool more = true; more;) {
+      more = false;
+#pragma omp parallel for num_threads(nth) schedule(static) reduction(|| : more)
+      for (int64_t t = 0; t < nz; ++t) {
+        const int64_t u = up[t], uu = up[u];
+        if (uu != u) {
+          up[t] = uu;
+          more = true;
+        }
+      }
+    }
+    // eff of a collapsed merge: its nearest kept ancestor (0: the root)
+#pragma omp parallel for num_threads(nth) schedule(static)
+    for (int64_t t = 0; t < nz; ++t)
+      if (!keep[t]) eff[t] = keep[up[t]] ? eff[up[t]] : 0;
+#pragma omp parallel for num_threads(nth) schedule(static)
+    for (int64_t k = 0; k < V0; ++k) {
+      const int64_t p = rpar[vraw[k]];
+      vpar[k] = p < 0 ? 0 : eff[p - N];
     }
 #pragma omp parallel for num_threads(nth) schedule(static)
     for (int64_t i = 0; i < N; ++i) {
@@ -344,24 +382,53 @@ rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg) {
   H.kids.assign(V + N, 0);
   std::vector<int32_t> child_idx(1 + V + N, 0);
   {
-    // nodes in ascending rep order, then appended to their parents' lists:
-    // every child list comes out sorted (X12).  Leaf i is the rep of itself
-    // and of the chain of kept ancestors whose smallest leaf it is, so walking
-    // up from each leaf in index order visits every node once, by rep (a node
-    // and its leftmost descendants share a rep but are never siblings).
-    std::vector<int64_t> fill(H.kids_off.begin(), H.kids_off.end() - 1);
-    auto put = [&](int32_t x, int32_t par) {
-      child_idx[x] = (int32_t)(fill[par] - H.kids_off[par]);
-      H.kids[fill[par]++] = x;
-    };
-    for (int64_t i = 0; i < N; ++i) {
-      int32_t y = H.lparent[i];
-      put((int32_t)(V + 1 + i), y);
-      while (y > 0 && rep_of[y] == (int32_t)i) {
-        const int32_t py = vpar[y - 1];
-        put(y, py);
-        y = py;
+    // Nodes in ascending rep order, appended to their parents' lists, give
+    // every child list sorted by rep (X12).  Leaf i is the rep of itself and of
+    // the chain of kept ancestors whose smallest leaf it is, so walking up from
+    // each leaf in index order visits every node once, by rep (a node and its
+    // leftmost descendants share a rep but are never siblings).  The walk runs
+    // in leaf chunks: per-chunk counts per parent, their prefix over the
+    // chunks, then every chunk places its nodes.
+    const int nc = std::max(1, std::min<int>(nth, (int)(N / 4096) + 1));
+    const int64_t P = V + 1;
+    lap("ch:csr");
+    std::vector<int32_t> off((size_t)nc * P);
+    auto walk = [&](int c, auto &&visit) {
+      for (int64_t i = N * c / nc; i < N * (c + 1) / nc; ++i) {
+        int32_t y = H.lparent[i];
+        visit((int32_t)(V + 1 + i), y);
+        while (y > 0 && rep_of[y] == (int32_t)i) {
+          const int32_t py = vpar[y - 1];
+          visit(y, py);
+          y = py;
+        }
       }
+    };
+#pragma omp parallel for num_threads(nc) schedule(static, 1)
+    for (int c = 0; c < nc; ++c) {
+      int32_t *o = off.data() + (size_t)c * P;
+      std::fill(o, o + P, 0);
+      walk(c, [&](int32_t, int32_t par) { ++o[par]; });
+    }
+    lap("ch:count");
+#pragma omp parallel for num_threads(nc) schedule(static)
+    for (int64_t p = 0; p < P; ++p) {
+      int32_t run = 0;
+      for (int c = 0; c < nc; ++c) {
+        const int32_t k = off[(size_t)c * P + p];
+        off[(size_t)c * P + p] = run;
+        run += k;
+      }
+    }
+    lap("ch:prefix");
+#pragma omp parallel for num_threads(nc) schedule(static, 1)
+    for (int c = 0; c < nc; ++c) {
+      int32_t *o = off.data() + (size_t)c * P;
+      walk(c, [&](int32_t x, int32_t par) {
+        const int32_t k = o[par]++;
+        child_idx[x] = k;
+        H.kids[H.kids_off[par] + k] = x;
+      });
     }
   }
   lap("children");
@@ -441,27 +508,31 @@ rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg) {
   lap("leaves");
 
   // ---- schedule: counting sort by (group of first appearance, -len, index) -
+  // The group of leaf i is the root child on its path; the first leaf of a
+  // group (in index order) is the group's rep, and root children are ordered
+  // by rep (X12), so groups rank by child index.  Buckets (group, length):
+  // atomic counts and placement, then each bucket sorted by index.
   {
     const int64_t G = H.kids_off[1] - H.kids_off[0];  // root children
-    std::vector<int64_t> grank(G, -1);
-    int64_t ng = 0;
-    std::vector<int64_t> key(N);
     const int64_t LMAX = max_depth + 1;
-    for (int64_t i = 0; i < N; ++i) {  // group ranks by first appearance (sequential, cheap)
-      const int32_t g = H.path[H.path_off[i]];
-      if (grank[g] < 0) grank[g] = ng++;
-    }
+    const int64_t nb = G * LMAX;
+    std::vector<int64_t> key(N);
+    std::vector<int32_t> cnt(nb + 1, 0);
 #pragma omp parallel for num_threads(nth) schedule(static)
     for (int64_t i = 0; i < N; ++i) {
       const int32_t g = H.path[H.path_off[i]];
       const int64_t len = H.path_off[i + 1] - H.path_off[i];
-      key[i] = grank[g] * LMAX + (LMAX - len);  // length descending within a group
+      key[i] = g * LMAX + (LMAX - len);  // length descending within a group
+      __atomic_fetch_add(&cnt[key[i] + 1], 1, __ATOMIC_RELAXED);
     }
-    std::vector<int64_t> cnt(ng * LMAX + 1, 0);
-    for (int64_t i = 0; i < N; ++i) ++cnt[key[i] + 1];
-    for (size_t z = 1; z < cnt.size(); ++z) cnt[z] += cnt[z - 1];
+    for (int64_t z = 1; z <= nb; ++z) cnt[z] += cnt[z - 1];
+    std::vector<int32_t> cur(cnt.begin(), cnt.end() - 1);
     H.schedule.resize(N);
-    for (int64_t i = 0; i < N; ++i) H.schedule[cnt[key[i]]++] = i;  // stable: index order
+#pragma omp parallel for num_threads(nth) schedule(static)
+    for (int64_t i = 0; i < N; ++i) H.schedule[__atomic_fetch_add(&cur[key[i]], 1, __ATOMIC_RELAXED)] = i;
+#pragma omp parallel for num_threads(nth) schedule(dynamic, 1024)
+    for (int64_t z = 0; z < nb; ++z)
+      if (cnt[z + 1] - cnt[z] > 1) std::sort(H.schedule.begin() + cnt[z], H.schedule.begin() + cnt[z + 1]);  // index ties
   }
   lap("schedule");
 

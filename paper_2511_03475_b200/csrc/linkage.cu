@@ -228,6 +228,7 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
   pa.level = counters + 2;
   pa.sweep_ctl = counters + 14;  // 0 between launches (reset by the sweep's CTA 0)
   pa.nclq = codes ? counters + 15 : nullptr;
+  pa.lpos = pa.newidx;  // free between the level list and the compaction map
   pa.cstat = counters + 4;
   pa.vals = codes ? cm->vals : nullptr;
   pa.pmap = codes ? at<int2>(scratch, L.pmap) : nullptr;
@@ -272,10 +273,22 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
     pa.sz_n = sz[p ^ 1];
     launch_prep_mark(pa, sms, st, launches);
     uint32_t *adj = reinterpret_cast<uint32_t *>(next);  // free until the merge writes it
-    if (codes)
-      k_level_adj<uint16_t><<<sms * 4, 256, 0, st>>>(pa, adj);
-    else
-      k_level_adj<float><<<sms * 4, 256, 0, st>>>(pa, adj);
+    {
+      // level rows streamed whole (k_level_adj_rows); W words of bits per row
+      // in shared memory (the level has at most M vertices)
+      const bool vec = ld % (codes ? 8 : 4) == 0 && (reinterpret_cast<uintptr_t>(cur) & 15) == 0;
+      const size_t smem = (size_t)((M + 31) / 32) * 4;
+      const int grid = std::min(M, sms * 8);
+      if (codes) {
+        auto kern = vec ? k_level_adj_rows<uint16_t, true> : k_level_adj_rows<uint16_t, false>;
+        if (smem > 48 * 1024) occupancy_cached(kern, 256, smem);
+        kern<<<grid, 256, smem, st>>>(pa, adj);
+      } else {
+        auto kern = vec ? k_level_adj_rows<float, true> : k_level_adj_rows<float, false>;
+        if (smem > 48 * 1024) occupancy_cached(kern, 256, smem);
+        kern<<<grid, 256, smem, st>>>(pa, adj);
+      }
+    }
     {
       const size_t m1 = std::min<size_t>((size_t)M, 1024);
       const size_t smem = m1 * ((m1 + 31) / 32) * 4;  // the staged adjacency of levels <= 1024

@@ -84,6 +84,7 @@ struct PrepArgs {
   int2 *pmap;  // [Mn + 8] new column -> (leader, other member of a pair | -1 singleton | -2 larger), or nullptr
                // (when pm32_fits: the same buffer holds the compact map pm32 and the clique list, see k_compact_maps)
   int *nclq;   // groups of 3+ members listed after pm32 (compact map only)
+  int *lpos;   // [M] level position of each column (-1: not in the level), or nullptr (k_prep_list)
   int *level;  // [0] level list length, [1] h bits
   int *cstat;  // clique diagnostics: starts, batches, picks, candidates, level n, clk/1k (warp0, pass)
   int *sweep_ctl;  // level-clique sweep with helper CTAs: published block count (0 between launches), or nullptr
@@ -201,8 +202,15 @@ __global__ void k_prep_rnn(PrepArgs a) {
 __global__ void __launch_bounds__(PT, 1) k_prep_list(PrepArgs a) {
   __shared__ BlockScratch S;
   const uint8_t *alive = a.alive;
-  const int nlist = block_compact(
-      a.M, [&](int i) { return alive[i] != 0; }, [&](int i) { return i; }, a.list, S);
+  int *lpos = a.lpos;
+  const int nlist = block_scan_all(
+      a.M, [&](int i) { return alive[i] != 0 ? 1 : 0; },
+      [&](int i, int pre) {
+        const bool in = alive[i] != 0;
+        if (in) a.list[pre] = i;
+        if (lpos) lpos[i] = in ? pre : -1;
+      },
+      S);
   if (threadIdx.x == 0) a.level[0] = nlist;
 }
 
@@ -227,6 +235,54 @@ __global__ void k_level_adj(PrepArgs a, uint32_t *__restrict__ adj) {
     if (j < n && j != i) bit = Elem<T>::bits(__ldg(D + (int64_t)a.list[i] * a.ld + a.list[j])) == hb;
     const unsigned word = __ballot_sync(0xffffffffu, bit);
     if (lane == 0) adj[q] = word;
+  }
+}
+
+// Round step 2, row form (single GPU): one CTA per level row i streams the
+// whole matrix row list[i] (16-byte loads) and sets bit lpos[c] of its
+// adjacency row for every column c holding h.  Every such column is a level
+// vertex (its row minimum is <= h, the global minimum); columns outside the
+// level (lpos -1: other rows, rows merged away by in-place rounds) are skipped.
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(256) k_level_adj_rows(PrepArgs a, uint32_t *__restrict__ adj) {
+  extern __shared__ uint32_t wbits[];  // [W]
+  const int n = a.level[0];
+  if (n < 2) return;
+  typedef Elem<T> E;
+  constexpr int VW = E::VW;
+  const unsigned hb = (unsigned)a.level[1];
+  const T *D = static_cast<const T *>(a.D);
+  const int W = (n + 31) >> 5, M = a.M;
+  const int *__restrict__ lpos = a.lpos;
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    for (int w = threadIdx.x; w < W; w += blockDim.x) wbits[w] = 0u;
+    __syncthreads();
+    const int r = a.list[i];
+    const T *row = D + (int64_t)r * a.ld;
+    if (VEC) {
+      const uint4 *row4 = reinterpret_cast<const uint4 *>(row);
+      for (int q = threadIdx.x; q * VW < M; q += blockDim.x) {
+        unsigned v[VW];
+        E::unpack(__ldg(row4 + q), v);
+#pragma unroll
+        for (int k = 0; k < VW; ++k) {
+          const int c = q * VW + k;
+          if (v[k] == hb && c < M && c != r) {
+            const int j = lpos[c];
+            if (j >= 0) atomicOr(&wbits[j >> 5], 1u << (j & 31));
+          }
+        }
+      }
+    } else {
+      for (int c = threadIdx.x; c < M; c += blockDim.x)
+        if (E::bits(__ldg(row + c)) == hb && c != r) {
+          const int j = lpos[c];
+          if (j >= 0) atomicOr(&wbits[j >> 5], 1u << (j & 31));
+        }
+    }
+    __syncthreads();
+    for (int w = threadIdx.x; w < W; w += blockDim.x) adj[(int64_t)i * W + w] = wbits[w];
+    __syncthreads();
   }
 }
 
