@@ -107,6 +107,9 @@ typedef struct rb_params {
   int32_t dist_grid;      /* 0 auto; > 0 caps the distance kernel's grid           */
   int32_t host_threads;   /* 0 auto (all cores); > 0 host tree-stage threads       */
   int32_t trace;          /* 1: per-round linkage / host-stage trace on stderr     */
+  int32_t side_buffer;    /* -1 auto: in-place rounds on 16-bit codes append merged
+                             columns to a transposed side buffer; 0: rewrite the
+                             columns in the matrix                                  */
 } rb_params;
 
 /* Per-build statistics (host, filled by rb_build_index). Times are CUDA-event

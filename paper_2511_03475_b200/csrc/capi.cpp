@@ -119,6 +119,7 @@ Tuning Tuning::from(const rb_params *p) {
   t.dist_grid = p->dist_grid;
   t.host_threads = p->host_threads;
   t.trace = p->trace != 0;
+  t.side_buffer = p->side_buffer;
   return t;
 }
 
@@ -161,11 +162,15 @@ ScratchLayout ScratchLayout::make(int64_t N, int32_t K, bool keep_rows, bool lin
     L.zs = take(o, (size_t)N * 4);
     L.amask = take(o, (size_t)(N / 32 + 1) * 4);
     L.mlist = take(o, (size_t)N * 4);
+    L.tcol = take(o, (size_t)kSideCap * 4);
+    L.tslot = take(o, (size_t)N * 4);
+    L.dmask = take(o, (size_t)(N / 32 + 1) * 4);
+    L.tctl = take(o, 64);
     // compacted matrices: at most (N-1) rows with a leading dimension padded to 4
     // (also holds an N x N copy for the intersection linkage with RB_KEEP_ROWS)
     const size_t mat = std::max((size_t)(N - 1) * (size_t)((N + 2) & ~3ll), (size_t)N * N) * 4;
     // code mode: two code matrices of max(N x N, (N-1) x round_up(N, 8)) in the same region
-    const size_t cmat = (std::max((size_t)N * N, (size_t)(N - 1) * (size_t)((N + 7) & ~7ll)) * 2 + 255) & ~(size_t)255;
+    const size_t cmat = code_mat_bytes(N);
     L.matA = take(o, std::max(mat, 2 * cmat));
     L.codes = L.matA;
     L.mat16 = L.matA + cmat;
@@ -206,6 +211,7 @@ rb_status rb_params_init(rb_params *p) {
   p->dist_grid = 0;
   p->host_threads = 0;
   p->trace = 0;
+  p->side_buffer = -1;
   return RB_OK;
 }
 

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstddef>
 #include <cstdint>
 #include <functional>
@@ -33,6 +34,7 @@ inline int64_t padded_cols(int64_t N) { return round_up(N, kChunk); }
 struct ScratchLayout {
   size_t err, idsT, nnkey, stage_ids, stage_lens, lut, lutc, vals, key0, key1, rep0, rep1, sz0, sz1, leader, aux0, aux1, aux2, aux3, aux4,
       alive, za, zb, zh, zs, amask, mlist, counters, matA, matB, total;
+  size_t tcol, tslot, dmask, tctl;  // code mode: in-place side buffer maps (linkage.cu)
   size_t pmap;         // code mode: int2 [N + 128] new column -> (leader, pair member), or the compact map
   size_t codes, mat16;  // code mode (inside matA): [N][N] codes, then the first compacted code matrix
   size_t ptab;          // tile path: packed Eq. 1 table (value, code << 16) [(K+1) * (K*K/2+1)]
@@ -50,6 +52,7 @@ struct Tuning {
   int dist_grid = 0;            // 0 auto, > 0 grid cap of the distance kernel
   int host_threads = 0;         // 0 auto
   bool trace = false;           // per-round trace on stderr
+  int side_buffer = -1;         // -1 auto, 0 in-place column rewrites in the matrix
   static Tuning from(const rb_params *p);
 };
 
@@ -84,6 +87,12 @@ cudaError_t launch_code_table(const float *lut, int32_t K, int stride, int64_t e
 
 // Linkage on 16-bit codes (linkage.cu): codes [N][N] (ld N) from the distance
 // kernel, a second buffer for compacted matrices, the code -> value table.
+// Bytes of one code matrix region (capi.cpp ScratchLayout; two per build).
+inline size_t code_mat_bytes(int64_t N) {
+  return (std::max((size_t)N * N, (size_t)(N - 1) * (size_t)((N + 7) & ~7ll)) * 2 + 255) & ~(size_t)255;
+}
+constexpr int kSideCap = 8192;  // in-place side buffer: slots (dirty columns) between flushes
+
 struct CodeMode {
   uint16_t *codes;
   uint16_t *mat16;

@@ -160,20 +160,45 @@ cudaError_t launch_merge(const T *cur, int64_t ld, int M, int Mn, const PrepArgs
   return cudaGetLastError();
 }
 
-// In-place round for element type T (see k_inplace_*).
+// In-place round for element type T (see k_inplace_*).  With a side buffer
+// (sb.T, code mode) the survivors' columns go to it instead of the matrix.
 template <typename T>
 cudaError_t launch_inplace(T *cur, int64_t ld, int M, int max_groups, const PrepArgs &pa, int sms, uint32_t *amask,
-                           int *mlist, int *nmulti, int *sz, unsigned long long *key, cudaStream_t st) {
+                           int *mlist, int *nmulti, int *sz, unsigned long long *key, const SideBuf &sb,
+                           cudaStream_t st, int *launches) {
   constexpr int VW = Elem<T>::VW;
-  k_inplace_prep<<<sms * 2, 256, 0, st>>>(pa, M, amask, mlist, nmulti, sz, key);
+  k_inplace_prep<<<sms * 2, 256, 0, st>>>(pa, M, amask, mlist, nmulti, sz, key, sb);
   const size_t smem = (size_t)((M + VW - 1) / VW) * 16;
-  occupancy_cached(k_inplace_rows<512, T>, 512, smem);
-  k_inplace_rows<512, T><<<sms * 2, 512, smem, st>>>(pa, cur, ld, M, amask, mlist, nmulti, key);
-  k_inplace_cols<T><<<dim3((unsigned)std::max(max_groups, 1), (unsigned)((M + kColsRows - 1) / kColsRows)), 256, 0,
-                      st>>>(pa, cur, ld, M, amask, mlist, nmulti);
-  k_inplace_check<T><<<(M + 255) / 256, 256, 0, st>>>(pa, cur, ld, M, key, pa.cnt, nmulti + 1);  // cnt: free after the compaction map
-  k_inplace_rescan<256, T><<<sms * 4, 256, 0, st>>>(cur, ld, M, amask, pa.cnt, nmulti + 1, key);
+  if constexpr (sizeof(T) == 2) {
+    if (sb.T) {
+      const size_t smem2 = smem + (size_t)sb.cap * 2;
+      occupancy_cached(k_inplace_rows_sb<512>, 512, smem2);
+      k_inplace_rows_sb<512><<<sms * 2, 512, smem2, st>>>(pa, cur, ld, M, amask, mlist, nmulti, key, sb);
+      k_side_tpose<<<dim3((unsigned)((M + 63) / 64), (unsigned)((std::max(max_groups, 1) + 31) / 32)), 256, 0, st>>>(
+          pa, cur, ld, M, mlist, nmulti, sb);
+      k_side_maps<<<1, 1024, 0, st>>>(pa, mlist, nmulti, sb);
+      *launches += 3;
+    }
+  }
+  if (!sb.T) {
+    occupancy_cached(k_inplace_rows<512, T>, 512, smem);
+    k_inplace_rows<512, T><<<sms * 2, 512, smem, st>>>(pa, cur, ld, M, amask, mlist, nmulti, key);
+    k_inplace_cols<T><<<dim3((unsigned)std::max(max_groups, 1), (unsigned)((M + kColsRows - 1) / kColsRows)), 256,
+                        0, st>>>(pa, cur, ld, M, amask, mlist, nmulti);
+    *launches += 2;
+  }
+  k_inplace_check<T><<<(M + 255) / 256, 256, 0, st>>>(pa, cur, ld, M, key, pa.cnt, nmulti + 1, sb);  // cnt: free after the compaction map
+  k_inplace_rescan<256, T><<<sms * 4, 256, 0, st>>>(cur, ld, M, amask, pa.cnt, nmulti + 1, key, sb);
+  *launches += 3;
   return cudaGetLastError();
+}
+
+// Side buffer state back to clean (after a flush, or at the start).
+cudaError_t side_reset(const SideBuf &sb, int M, cudaStream_t st) {
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(sb.tslot, 0xff, (size_t)M * 4, st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(sb.dmask, 0, (size_t)(M / 32 + 1) * 4, st)) != cudaSuccess) return e;
+  return cudaMemsetAsync(sb.nt, 0, 4, st);
 }
 
 }  // namespace
@@ -258,6 +283,43 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
   int zprev = 0;
   int zdone = 0;
   std::vector<cudaEvent_t> mev;  // [start, end] per compaction launch (merge_ms)
+  // In-place side buffer (code mode): T after the level adjacency in the free
+  // code-matrix region (`next` is untouched by in-place rounds); maps in scratch.
+  SideBuf sb{};
+  sb.tcol = at<int>(scratch, L.tcol);
+  sb.tslot = at<int>(scratch, L.tslot);
+  sb.dmask = at<uint32_t>(scratch, L.dmask);
+  sb.nt = at<int>(scratch, L.tctl);
+  int sb_used = 0;  // host upper bound of the slots in use (merges of the in-place rounds since the last flush)
+  if (codes && (e = side_reset(sb, (int)N, st)) != cudaSuccess) return e;
+  auto side_for = [&](int Mc, void *nx) {  // the side buffer for a matrix of Mc rows with `nx` free
+    SideBuf b = sb;
+    b.T = nullptr;
+    b.cap = 0;
+    if (!codes || tu.side_buffer == 0) return b;
+    // the level adjacency (n x W words, n <= Mc) and the clique sweep's work
+    // area after it (k_level_cliques: I [n][W rounded to 4], 6 arrays of n
+    // ints, the per-block decision logs) come first
+    const size_t W4 = (size_t)(((Mc + 31) / 32 + 3) & ~3);
+    const size_t adj_bytes = ((2 * (size_t)Mc * W4 * 4 + 16 * ((size_t)Mc + 1024) * 4) + 255) & ~(size_t)255;
+    const size_t region = code_mat_bytes(N);
+    if (region <= adj_bytes) return b;
+    const int64_t cap = std::min<int64_t>(kSideCap, (int64_t)((region - adj_bytes) / (2 * (size_t)Mc))) & ~7ll;
+    if (cap < 64) return b;
+    b.T = reinterpret_cast<uint16_t *>(static_cast<unsigned char *>(nx) + adj_bytes);
+    b.cap = (int)cap;
+    return b;
+  };
+  auto side_flush = [&](void *cm_, int64_t ld_, int Mc, void *nx) -> cudaError_t {
+    if (sb_used == 0) return cudaSuccess;
+    const SideBuf b = side_for(Mc, nx);
+    const size_t smem = (size_t)((Mc + 7) / 8) * 16 + (size_t)b.cap * 4;
+    occupancy_cached(k_side_flush, 256, smem);
+    k_side_flush<<<sms * 4, 256, smem, st>>>(static_cast<uint16_t *>(cm_), ld_, Mc, b);
+    ++*launches;
+    sb_used = 0;
+    return side_reset(sb, Mc, st);
+  };
   while (live > 1) {
     if (trace) {
       cudaMemsetAsync(counters + 4, 0, 8 * sizeof(int), st);
@@ -280,13 +342,15 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
       const size_t smem = (size_t)((M + 31) / 32) * 4;
       const int grid = std::min(M, sms * 8);
       if (codes) {
+        // dirty columns (side buffer in use) need the vector path, which in-place rounds guarantee
+        const SideBuf b = sb_used > 0 ? side_for(M, next) : SideBuf{};
         auto kern = vec ? k_level_adj_rows<uint16_t, true> : k_level_adj_rows<uint16_t, false>;
         if (smem > 48 * 1024) occupancy_cached(kern, 256, smem);
-        kern<<<grid, 256, smem, st>>>(pa, adj);
+        kern<<<grid, 256, smem, st>>>(pa, adj, b);
       } else {
         auto kern = vec ? k_level_adj_rows<float, true> : k_level_adj_rows<float, false>;
         if (smem > 48 * 1024) occupancy_cached(kern, 256, smem);
-        kern<<<grid, 256, smem, st>>>(pa, adj);
+        kern<<<grid, 256, smem, st>>>(pa, adj, SideBuf{});
       }
     }
     {
@@ -347,15 +411,21 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
         mask_ok = true;
       }
       if ((e = cudaMemsetAsync(nmulti, 0, 8, st)) != cudaSuccess) return e;  // nmulti, nres
+      SideBuf b = side_for(M, next);
+      if (b.T && sb_used + merges_round > b.cap && (e = side_flush(cur, ld, M, next)) != cudaSuccess) return e;
+      if (b.T && merges_round > b.cap) b.T = nullptr;  // more survivors than slots: columns rewritten in place
+      if (!b.T && sb_used > 0 && (e = side_flush(cur, ld, M, next)) != cudaSuccess) return e;
+      if (b.T) sb_used += merges_round;  // merged groups <= merges of the round
       // merged groups <= merges of the round (the grid of the column kernel)
       e = codes ? launch_inplace<uint16_t>(static_cast<uint16_t *>(cur), ld, M, merges_round, pa, sms, amask, mlist,
-                                           nmulti, sz[p], key[p], st)
+                                           nmulti, sz[p], key[p], b, st, launches)
                 : launch_inplace<float>(static_cast<float *>(cur), ld, M, merges_round, pa, sms, amask, mlist, nmulti,
-                                        sz[p], key[p], st);
-      *launches += 5;
+                                        sz[p], key[p], SideBuf{}, st, launches);
+      ++*launches;
       out->paths |= RB_PATH_INPLACE;
       if (e != cudaSuccess) return e;
     } else if (Mn > 1) {
+      if ((e = side_flush(cur, ld, M, next)) != cudaSuccess) return e;  // dirty columns back into the matrix
       cudaEvent_t me[2];
       cudaEventCreateWithFlags(&me[0], cudaEventDefault);
       cudaEventCreateWithFlags(&me[1], cudaEventDefault);
@@ -383,6 +453,9 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
       float a = 0, b = 0;
       cudaEventElapsedTime(&a, tev[0], tev[1]);
       cudaEventElapsedTime(&b, tev[1], tev[2]);
+      int ires[2] = {0, 0};  // in-place rounds: merged groups, rescanned rows
+      if (inplace) cudaMemcpy(ires, counters + 12, 8, cudaMemcpyDeviceToHost);
+      if (inplace) std::fprintf(stderr, "[ragb linkage]   inplace groups=%d rescans=%d\n", ires[0], ires[1]);
       std::fprintf(stderr,
                    "[ragb linkage] round %d M=%d live=%d Mn=%d merges=%d %s prep=%.3fms merge=%.3fms | level n=%d "
                    "starts=%d batches=%d picks=%d cands=%d kclk w0=%d pass=%d collect=%d\n",

@@ -84,7 +84,7 @@ struct PrepArgs {
   int2 *pmap;  // [Mn + 8] new column -> (leader, other member of a pair | -1 singleton | -2 larger), or nullptr
                // (when pm32_fits: the same buffer holds the compact map pm32 and the clique list, see k_compact_maps)
   int *nclq;   // groups of 3+ members listed after pm32 (compact map only)
-  int *lpos;   // [M] level position of each column (-1: not in the level), or nullptr (k_prep_list)
+  int *lpos;   // [M] level position of each level column (where alive is set), or nullptr (k_prep_list)
   int *level;  // [0] level list length, [1] h bits
   int *cstat;  // clique diagnostics: starts, batches, picks, candidates, level n, clk/1k (warp0, pass)
   int *sweep_ctl;  // level-clique sweep with helper CTAs: published block count (0 between launches), or nullptr
@@ -206,9 +206,10 @@ __global__ void __launch_bounds__(PT, 1) k_prep_list(PrepArgs a) {
   const int nlist = block_scan_all(
       a.M, [&](int i) { return alive[i] != 0 ? 1 : 0; },
       [&](int i, int pre) {
-        const bool in = alive[i] != 0;
-        if (in) a.list[pre] = i;
-        if (lpos) lpos[i] = in ? pre : -1;
+        if (alive[i] != 0) {
+          a.list[pre] = i;
+          if (lpos) lpos[i] = pre;  // valid where alive (the level flag) is set
+        }
       },
       S);
   if (threadIdx.x == 0) a.level[0] = nlist;
@@ -238,13 +239,33 @@ __global__ void k_level_adj(PrepArgs a, uint32_t *__restrict__ adj) {
   }
 }
 
+// Side buffer of the in-place rounds (code mode).  Rewriting the merged
+// survivors' columns in place costs one scattered 2-byte store per row and
+// merge (most of an in-place round).  Instead a survivor's column becomes
+// "dirty": its values are appended, transposed, to a row-major buffer
+// T[r][slot] (one coalesced segment per row for the round's survivors), and
+// the readers of the matrix take a dirty column's value from T:
+//   val(r, c) = dirty(c) ? T[r][tslot[c]] : D[r][c].
+// Merged rows are still rewritten in place (D part), together with their T
+// row.  Before the next compaction the buffer is flushed into the matrix
+// row by row (k_side_flush).
+struct SideBuf {
+  uint16_t *T;      // [M][cap] dirty-column values, or nullptr (no side buffer)
+  int cap;          // slots per row (multiple of 8)
+  int *tcol;        // [cap] column of slot k, -1 retired
+  int *tslot;       // [M] slot of column c, -1 clean
+  uint32_t *dmask;  // [M/32 + 1] dirty-column bits
+  int *nt;          // slots in use
+};
+__device__ __forceinline__ bool sb_dirty(const SideBuf &sb, int c) { return (sb.dmask[c >> 5] >> (c & 31)) & 1u; }
+
 // Round step 2, row form (single GPU): one CTA per level row i streams the
 // whole matrix row list[i] (16-byte loads) and sets bit lpos[c] of its
 // adjacency row for every column c holding h.  Every such column is a level
 // vertex (its row minimum is <= h, the global minimum); columns outside the
-// level (lpos -1: other rows, rows merged away by in-place rounds) are skipped.
+// level (rows merged away by in-place rounds hold stale values) are skipped.
 template <typename T, bool VEC>
-__global__ void __launch_bounds__(256) k_level_adj_rows(PrepArgs a, uint32_t *__restrict__ adj) {
+__global__ void __launch_bounds__(256) k_level_adj_rows(PrepArgs a, uint32_t *__restrict__ adj, SideBuf sb) {
   extern __shared__ uint32_t wbits[];  // [W]
   const int n = a.level[0];
   if (n < 2) return;
@@ -254,6 +275,7 @@ __global__ void __launch_bounds__(256) k_level_adj_rows(PrepArgs a, uint32_t *__
   const T *D = static_cast<const T *>(a.D);
   const int W = (n + 31) >> 5, M = a.M;
   const int *__restrict__ lpos = a.lpos;
+  const uint8_t *__restrict__ lev = a.alive;  // level flags (k_prep_rnn)
   for (int i = blockIdx.x; i < n; i += gridDim.x) {
     for (int w = threadIdx.x; w < W; w += blockDim.x) wbits[w] = 0u;
     __syncthreads();
@@ -267,17 +289,26 @@ __global__ void __launch_bounds__(256) k_level_adj_rows(PrepArgs a, uint32_t *__
 #pragma unroll
         for (int k = 0; k < VW; ++k) {
           const int c = q * VW + k;
-          if (v[k] == hb && c < M && c != r) {
+          if (v[k] == hb && c < M && c != r && !(sb.T && sb_dirty(sb, c)) && lev[c]) {
             const int j = lpos[c];
-            if (j >= 0) atomicOr(&wbits[j >> 5], 1u << (j & 31));
+            atomicOr(&wbits[j >> 5], 1u << (j & 31));
           }
+        }
+      }
+      if (sb.T) {  // dirty columns from the side buffer
+        const int nt = *sb.nt;
+        for (int k = threadIdx.x; k < nt; k += blockDim.x) {
+          const int c = sb.tcol[k];
+          if (c < 0 || c == r || (unsigned)sb.T[(int64_t)r * sb.cap + k] != hb || !lev[c]) continue;
+          const int j = lpos[c];
+          atomicOr(&wbits[j >> 5], 1u << (j & 31));
         }
       }
     } else {
       for (int c = threadIdx.x; c < M; c += blockDim.x)
-        if (E::bits(__ldg(row + c)) == hb && c != r) {
+        if (E::bits(__ldg(row + c)) == hb && c != r && lev[c]) {
           const int j = lpos[c];
-          if (j >= 0) atomicOr(&wbits[j >> 5], 1u << (j & 31));
+          atomicOr(&wbits[j >> 5], 1u << (j & 31));
         }
     }
     __syncthreads();
@@ -1675,10 +1706,11 @@ __global__ void __launch_bounds__(NTH) k_merge_gather2(const uint16_t *__restric
 // complete-linkage values only grow, X7, and the group keeps the smallest
 // index, X8).  Column order is unchanged, so column order == rep order still.
 
+
 // S0: per-row flags; multi-member groups -> mlist; members other than the
 // survivor -> dead; the survivor's size.
 __global__ void k_inplace_prep(PrepArgs a, int M, uint32_t *__restrict__ amask, int *__restrict__ mlist,
-                               int *__restrict__ nmulti, int *__restrict__ sz, u64 *__restrict__ key) {
+                               int *__restrict__ nmulti, int *__restrict__ sz, u64 *__restrict__ key, SideBuf sb) {
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < M; x += gridDim.x * blockDim.x) {
     const int l = a.leader[x];
     uint8_t chg = 0;
@@ -1689,6 +1721,7 @@ __global__ void k_inplace_prep(PrepArgs a, int M, uint32_t *__restrict__ amask, 
         if (x != l) {
           key[x] = kDead;
           atomicAnd(&amask[x >> 5], ~(1u << (x & 31)));
+          if (sb.T && sb.tslot[x] >= 0) sb.tcol[sb.tslot[x]] = -1;  // a dirty column merged away
         } else {
           mlist[atomicAdd(nmulti, 1)] = g;
           sz[x] = a.sz_n[g];
@@ -1769,6 +1802,179 @@ __global__ void __launch_bounds__(NTH, 2) k_inplace_rows(PrepArgs a, T *__restri
   }
 }
 
+// S1 with the side buffer (code mode): as k_inplace_rows, and the survivor's
+// T row is the max of its members' T rows; a member's value at a dirty column
+// comes from T; the row minimum takes clean live columns (and the round's
+// survivors, whose values are in the new row) from the row and the other
+// live dirty columns from T.
+template <int NTH>
+__global__ void __launch_bounds__(NTH, 2) k_inplace_rows_sb(PrepArgs a, uint16_t *__restrict__ D, int64_t ld,
+                                                         int M, const uint32_t *__restrict__ amask,
+                                                         const int *__restrict__ mlist,
+                                                         const int *__restrict__ nmulti_p, u64 *__restrict__ key,
+                                                         SideBuf sb) {
+  typedef Elem<uint16_t> E;
+  constexpr int VW = 8;
+  extern __shared__ __align__(16) uint4 rowv[];  // [MV] row, then [cap / 8] T row
+  uint16_t *row = reinterpret_cast<uint16_t *>(rowv);
+  __shared__ u64 wmin[NTH / 32];
+  const int nmulti = *nmulti_p, nt = *sb.nt;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int MV = (M + VW - 1) / VW, TV = (nt + 7) / 8;
+  uint4 *trow4 = rowv + MV;
+  const uint16_t *trow = reinterpret_cast<const uint16_t *>(trow4);
+  for (int gi = blockIdx.x; gi < nmulti; gi += gridDim.x) {
+    const int g = mlist[gi];
+    const int rb = a.goff[g], re = a.goff[g + 1];
+    const int L = a.cursor[g];  // first_old: the survivor
+    for (int q = tid; q < MV; q += NTH) {
+      uint4 v = make_uint4(0, 0, 0, 0);
+      for (int r = rb; r < re; ++r)
+        v = vmax4<uint16_t>(v, __ldcs(reinterpret_cast<const uint4 *>(D + (int64_t)a.gmem[r] * ld) + q));
+      rowv[q] = v;
+    }
+    for (int q = tid; q < TV; q += NTH) {
+      uint4 v = make_uint4(0, 0, 0, 0);
+      for (int r = rb; r < re; ++r)
+        v = vmax4<uint16_t>(v, *(reinterpret_cast<const uint4 *>(sb.T + (int64_t)a.gmem[r] * sb.cap) + q));
+      trow4[q] = v;
+    }
+    __syncthreads();
+    for (int hi = tid; hi < nmulti; hi += NTH) {
+      const int h = mlist[hi];
+      if (h == g) continue;
+      unsigned v = 0u;
+      for (int r = a.goff[h]; r < a.goff[h + 1]; ++r) {
+        const int x = a.gmem[r];
+        v = max(v, sb_dirty(sb, x) ? (unsigned)trow[sb.tslot[x]] : (unsigned)row[x]);
+      }
+      row[a.cursor[h]] = (uint16_t)v;
+    }
+    __syncthreads();
+    if (tid == 0) row[L] = 0;
+    __syncthreads();
+    u64 best = ~0ull;
+    uint4 *out = reinterpret_cast<uint4 *>(D + (int64_t)L * ld);
+    for (int q = tid; q < MV; q += NTH) {
+      const uint4 v = rowv[q];
+      __stcs(out + q, v);
+      unsigned vv[VW];
+      E::unpack(v, vv);
+      const int c0 = VW * q;
+      const unsigned mb = (amask[c0 >> 5] >> (c0 & 31)) & 0xffu, db = (sb.dmask[c0 >> 5] >> (c0 & 31)) & 0xffu;
+#pragma unroll
+      for (int k = 0; k < VW; ++k) {
+        const int c = c0 + k;
+        // live, and clean or merged this round (its value is in the new row)
+        const bool live = ((mb >> k) & 1u) && c < M && c != L && (!((db >> k) & 1u) || a.alive[c]);
+        const u64 kk = ((u64)vv[k] << 32) | (unsigned)c;
+        best = (live && kk < best) ? kk : best;
+      }
+    }
+    uint4 *tout = reinterpret_cast<uint4 *>(sb.T + (int64_t)L * sb.cap);
+    for (int q = tid; q < TV; q += NTH) tout[q] = trow4[q];
+    for (int k = tid; k < nt; k += NTH) {
+      const int c = sb.tcol[k];  // retired slots (incl. dead columns): -1
+      if (c < 0 || c == L || a.alive[c]) continue;
+      const u64 kk = ((u64)trow[k] << 32) | (unsigned)c;
+      best = kk < best ? kk : best;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const u64 y = __shfl_xor_sync(0xffffffffu, best, o);
+      best = y < best ? y : best;
+    }
+    if (lane == 0) wmin[w] = best;
+    __syncthreads();
+    if (tid == 0) {
+      u64 b = wmin[0];
+#pragma unroll
+      for (int i = 1; i < NTH / 32; ++i) b = wmin[i] < b ? wmin[i] : b;
+      key[L] = b;
+    }
+    __syncthreads();
+  }
+}
+
+// S2 with the side buffer: the round's survivors' new rows, transposed, into
+// slots nt .. nt + nmulti - 1 of every row's T segment.  CTA = 64 rows x 32
+// survivors through a shared-memory tile (row segments read coalesced, each
+// T row gets 32 consecutive slots).
+__global__ void __launch_bounds__(256) k_side_tpose(PrepArgs a, const uint16_t *__restrict__ D, int64_t ld, int M,
+                                                    const int *__restrict__ mlist, const int *__restrict__ nmulti_p,
+                                                    SideBuf sb) {
+  __shared__ uint16_t tile[32][64 + 2];
+  const int m = *nmulti_p, nt = *sb.nt;
+  const int k0 = blockIdx.y * 32;
+  if (k0 >= m) return;
+  const int r0 = blockIdx.x * 64;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < 32 * 64; e += 256) {
+    const int kk = e >> 6, rr = e & 63;
+    uint16_t v = 0;
+    const int r = r0 + rr;
+    if (k0 + kk < m && r < M) {
+      // val(L, r): a dirty column r (not merged this round) holds its value in
+      // L's T row; the round's survivors' values are in the new row itself
+      const int L = a.cursor[mlist[k0 + kk]];
+      v = (sb_dirty(sb, r) && !a.alive[r]) ? sb.T[(int64_t)L * sb.cap + sb.tslot[r]] : D[(int64_t)L * ld + r];
+    }
+    tile[kk][rr] = v;
+  }
+  __syncthreads();
+  for (int e = tid; e < 32 * 64; e += 256) {
+    const int rr = e >> 5, kk = e & 31;
+    if (k0 + kk < m && r0 + rr < M) sb.T[(int64_t)(r0 + rr) * sb.cap + nt + k0 + kk] = tile[kk][rr];
+  }
+}
+
+// S2b (one CTA): slot maps of the round's survivors (a re-merged dirty column
+// retires its old slot), dirty bits, then the new slot count.
+__global__ void __launch_bounds__(1024) k_side_maps(PrepArgs a, const int *__restrict__ mlist,
+                                                    const int *__restrict__ nmulti_p, SideBuf sb) {
+  const int m = *nmulti_p, nt = *sb.nt;
+  for (int k = threadIdx.x; k < m; k += blockDim.x) {
+    const int L = a.cursor[mlist[k]];
+    const int old = sb.tslot[L];
+    if (old >= 0) sb.tcol[old] = -1;
+    sb.tslot[L] = nt + k;
+    sb.tcol[nt + k] = L;
+    atomicOr(&sb.dmask[L >> 5], 1u << (L & 31));
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *sb.nt = nt + m;
+}
+
+// Flush (before a compaction): every row < M staged in shared memory, its
+// dirty columns patched from T, written back whole.
+__global__ void __launch_bounds__(256) k_side_flush(uint16_t *__restrict__ D, int64_t ld, int M, SideBuf sb) {
+  extern __shared__ __align__(16) uint4 rowv[];  // [MV] row, then [cap] slot columns
+  uint16_t *row = reinterpret_cast<uint16_t *>(rowv);
+  const int nt = *sb.nt;
+  const int MV = (M + 7) / 8;
+  int *scol = reinterpret_cast<int *>(rowv + MV);
+  for (int k = threadIdx.x; k < nt; k += blockDim.x) scol[k] = sb.tcol[k];
+  for (int r = blockIdx.x; r < M; r += gridDim.x) {
+    uint4 *src = reinterpret_cast<uint4 *>(D + (int64_t)r * ld);
+    for (int q = threadIdx.x; q < MV; q += blockDim.x) rowv[q] = __ldcs(src + q);
+    __syncthreads();
+    const uint16_t *trow = sb.T + (int64_t)r * sb.cap;
+    for (int k0 = threadIdx.x; k0 < nt; k0 += blockDim.x * 4) {
+      uint16_t v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = k0 + u * (int)blockDim.x < nt ? trow[k0 + u * blockDim.x] : (uint16_t)0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = k0 + u * blockDim.x;
+        if (k < nt && scol[k] >= 0) row[scol[k]] = v[u];
+      }
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < MV; q += blockDim.x) __stcs(src + q, rowv[q]);
+    __syncthreads();
+  }
+}
+
 // S2: columns from rows (symmetry): D[r][L] = D[L][r] for every live row r.
 // CTA (x = merged group, y = chunk of CR rows): the group's survivor L is
 // looked up once, then every thread moves CR / 256 rows (independent
@@ -1806,14 +2012,14 @@ __global__ void __launch_bounds__(256) k_inplace_cols(PrepArgs a, T *__restrict_
 // larger); otherwise r goes to the rescan list.
 template <typename T>
 __global__ void k_inplace_check(PrepArgs a, const T *__restrict__ D, int64_t ld, int M,
-                                u64 *__restrict__ key, int *__restrict__ rlist, int *__restrict__ nres) {
+                                u64 *__restrict__ key, int *__restrict__ rlist, int *__restrict__ nres, SideBuf sb) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < M; r += gridDim.x * blockDim.x) {
     const u64 kr = key[r];
     if (kr == kDead || a.alive[r]) continue;  // dead, or a survivor (done in S1)
     const int t = (int)(kr & 0xffffffffu);
     if (!a.alive[t]) continue;  // neighbour not merged: unchanged
     const int Lg = a.leader[t];
-    const unsigned v = Elem<T>::bits(D[(int64_t)r * ld + Lg]);
+    const unsigned v = sb.T ? (unsigned)sb.T[(int64_t)r * sb.cap + sb.tslot[Lg]] : Elem<T>::bits(D[(int64_t)r * ld + Lg]);
     if (v == (unsigned)(kr >> 32))
       key[r] = ((u64)v << 32) | (unsigned)Lg;
     else
@@ -1826,7 +2032,8 @@ template <int NTH, typename T>
 __global__ void __launch_bounds__(NTH) k_inplace_rescan(const T *__restrict__ D, int64_t ld, int M,
                                                         const uint32_t *__restrict__ amask,
                                                         const int *__restrict__ rlist,
-                                                        const int *__restrict__ nres_p, u64 *__restrict__ key) {
+                                                        const int *__restrict__ nres_p, u64 *__restrict__ key,
+                                                        SideBuf sb) {
   typedef Elem<T> E;
   constexpr int VW = E::VW;
   __shared__ u64 wmin[NTH / 32];
@@ -1837,15 +2044,48 @@ __global__ void __launch_bounds__(NTH) k_inplace_rescan(const T *__restrict__ D,
     const int r = rlist[i];
     u64 best = ~0ull;
     const uint4 *src = reinterpret_cast<const uint4 *>(D + (int64_t)r * ld);
-    for (int q = tid; q < MV; q += NTH) {
-      unsigned vv[VW];
-      E::unpack(__ldcs(src + q), vv);
+    constexpr int UR = 4;  // vectors in flight per thread
+    for (int q0 = tid; q0 < MV; q0 += NTH * UR) {
+      uint4 x[UR];
 #pragma unroll
-      for (int k = 0; k < VW; ++k) {
-        const int c = VW * q + k;
-        const bool live = c < M && c != r && ((amask[c >> 5] >> (c & 31)) & 1u);
-        const u64 kk = ((u64)vv[k] << 32) | (unsigned)c;
-        best = (live && kk < best) ? kk : best;
+      for (int u = 0; u < UR; ++u) x[u] = q0 + u * NTH < MV ? __ldcs(src + q0 + u * NTH) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int u = 0; u < UR; ++u) {
+        const int q = q0 + u * NTH;
+        if (q >= MV) continue;
+        unsigned vv[VW];
+        E::unpack(x[u], vv);
+        // the vector's VW columns lie in one mask word: live and (with a side
+        // buffer) clean
+        const int c0 = VW * q;
+        const unsigned mw = amask[c0 >> 5] & ~(sb.T ? sb.dmask[c0 >> 5] : 0u);
+        const unsigned mb = (mw >> (c0 & 31)) & ((1u << VW) - 1u);
+#pragma unroll
+        for (int k = 0; k < VW; ++k) {
+          const int c = c0 + k;
+          const bool live = ((mb >> k) & 1u) && c < M && c != r;
+          const u64 kk = ((u64)vv[k] << 32) | (unsigned)c;
+          best = (live && kk < best) ? kk : best;
+        }
+      }
+    }
+    if (sb.T) {  // dirty columns from the side buffer (retired slots: tcol -1, incl. dead columns)
+      const int nt = *sb.nt;
+      const uint16_t *trow = sb.T + (int64_t)r * sb.cap;
+      for (int k0 = tid; k0 < nt; k0 += NTH * 4) {
+        int cs[4];
+        unsigned vs[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int k = k0 + u * NTH;
+          cs[u] = k < nt ? __ldg(sb.tcol + k) : -1;
+          vs[u] = k < nt ? trow[k] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const u64 kk = ((u64)vs[u] << 32) | (unsigned)cs[u];
+          best = (cs[u] >= 0 && cs[u] != r && kk < best) ? kk : best;
+        }
       }
     }
 #pragma unroll

@@ -55,10 +55,11 @@ class Params(ctypes.Structure):
                 ("value_codes", ctypes.c_int32), ("inplace", ctypes.c_int32),
                 ("inplace_weight", ctypes.c_float), ("gather", ctypes.c_int32),
                 ("long_lists", ctypes.c_int32), ("dist_grid", ctypes.c_int32),
-                ("host_threads", ctypes.c_int32), ("trace", ctypes.c_int32)]
+                ("host_threads", ctypes.c_int32), ("trace", ctypes.c_int32),
+                ("side_buffer", ctypes.c_int32)]
 
 TUNING_FIELDS = ("value_codes", "inplace", "inplace_weight", "gather", "long_lists", "dist_grid",
-                 "host_threads", "trace")
+                 "host_threads", "trace", "side_buffer")
 
 
 class Stats(ctypes.Structure):
