@@ -377,9 +377,10 @@ def run_ours(args, ws, rank, local):
                  "share_of_step": mean["distance_ms"] / ms}
     mb = mean["merge_bytes"] / max(mean["merge_launches"], 1)
     merge_gbs = mean["merge_bytes"] / (mean["merge_ms"] * 1e-3) / 1e9 if mean["merge_ms"] > 0 else 0.0
-    # the single-GPU code-mode rounds compact with the gather kernel; the
+    # the single-GPU code-mode rounds compact with the gather kernel (compact
+    # 32-bit map: k_merge_gather2); the
     # sharded build and the fp32 rounds with the window kernel
-    mkern = "k_merge_gather" if codes and not sharded else "k_merge_rows"
+    mkern = "k_merge_gather2" if codes and not sharded else "k_merge_rows"
     roof_merge = {"kernel": f"{mkern} (a5, linkage compaction rounds)", "bound": "hbm",
                   "achieved": merge_gbs, "peak": hbm, "unit": "GB/s", "frac": merge_gbs / hbm,
                   "traffic": traffic.get(mkern) if traffic and not sharded else None, "peak_source": peak_src,

@@ -24,7 +24,7 @@ def main():
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     per = {}
     for r in rows[2:]:
-        name = next((k for k in ("k_dist_tile", "k_merge_rows", "k_merge_gather") if k in r[ki]), None)
+        name = next((k for k in ("k_dist_tile", "k_merge_rows", "k_merge_gather2", "k_merge_gather") if k in r[ki]), None)
         if name is None:
             continue
         b = float(r[rd].replace(",", "")) * scale[units[rd]] + float(r[wr].replace(",", "")) * scale[units[wr]]

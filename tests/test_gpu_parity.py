@@ -302,16 +302,19 @@ def test_C3_full_vs_oracle():
         assert np.array_equal(x, y)
 
 
-@pytest.mark.parametrize("codes", [0, -1])
+@pytest.mark.parametrize("codes,side", [(0, -1), (-1, -1), (-1, 0)])
 @pytest.mark.parametrize("mode", [0, 1])
 @pytest.mark.parametrize("case", ["C2", "var", "ties"])
-def test_round_strategy(mode, case, codes):
+def test_round_strategy(mode, case, codes, side):
     """Linkage rounds in place (inplace=1, forced wherever allowed) or always
     compacting (0), on fp32 matrices (value_codes=0) or on 16-bit value codes
-    (default where the Eq. 1 table exists), give the oracle's merge order (the
-    strategy and the stored form are implementation choices, X7-X9 fix the
-    result)."""
-    tu = dict(inplace=mode, value_codes=codes)
+    (default where the Eq. 1 table exists), with the in-place side buffer
+    (default in code mode) or in-place column rewrites (side_buffer=0), give
+    the oracle's merge order (the strategy and the stored form are
+    implementation choices, X7-X9 fix the result)."""
+    if mode == 0 and side == 0:
+        pytest.skip("no in-place rounds: the side buffer is not used")
+    tu = dict(inplace=mode, value_codes=codes, side_buffer=side)
     if case == "C2":
         idx = check_full(config("C2").ids, counts=False, tuning=tu)
     elif case == "var":
@@ -358,13 +361,14 @@ def test_code_window_compaction(case):
 
 def test_round_strategy_full_size():
     """At C4 size (level cliques above 4096 vertices, block path) the merge
-    order and the document order do not depend on the round strategy nor on
-    the stored form of the matrices (fp32 values or 16-bit value codes)."""
+    order and the document order do not depend on the round strategy, on the
+    stored form of the matrices (fp32 values or 16-bit value codes) nor on
+    the in-place side buffer."""
     ids = config("C4").ids
     t = torch.from_numpy(ids.view(np.int32)).cuda()
     res = []
-    for mode, codes in ((0, -1), (-1, -1), (-1, 0)):
-        idx, ws = F.build_index(t, tuning=dict(inplace=mode, value_codes=codes))
+    for mode, codes, side in ((0, -1, -1), (-1, -1, -1), (-1, 0, -1), (-1, -1, 0)):
+        idx, ws = F.build_index(t, tuning=dict(inplace=mode, value_codes=codes, side_buffer=side))
         res.append((idx.linkage(), idx.order_contexts()))
         del idx, ws
         torch.cuda.empty_cache()
