@@ -109,13 +109,17 @@ cudaError_t launch_merge(const T *cur, int64_t ld, int M, int Mn, const PrepArgs
   const bool compact = sizeof(T) == 2 && pa.pmap && pa.nclq && pm32_fits(M, Mn);  // k_compact_maps wrote pm32
   if (compact && tu.gather != 0) {
     // code mode with the compact map: k_merge_gather2 when the old row fits
-    auto kern = wide16 ? (vec16 ? k_merge_gather2<true, 1024> : k_merge_gather2<false, 1024>)
-                       : (vec16 ? k_merge_gather2<true, 256> : k_merge_gather2<false, 256>);
+    // rows that fit twice in half the shared memory (M <= ~28K): two
+    // 512-thread CTAs per SM, each double-buffered
+    const bool mid = wide16 && vec16 && 4 * row_bytes + 4096 <= 227 * 1024 && tu.gather != 2;
+    auto kern = mid ? k_merge_gather2<true, 512>
+                    : wide16 ? (vec16 ? k_merge_gather2<true, 1024> : k_merge_gather2<false, 1024>)
+                             : (vec16 ? k_merge_gather2<true, 256> : k_merge_gather2<false, 256>);
     const size_t lim = dyn_smem_limit(kern);
     if (row_bytes <= lim) {
       const int db = vec16 && 2 * row_bytes <= lim ? 1 : 0;  // double-buffered rows
       const size_t smem = row_bytes * (1 + db);
-      const int nth = wide16 ? 1024 : 256;
+      const int nth = mid ? 512 : wide16 ? 1024 : 256;
       const int per_sm = occupancy_cached(kern, nth, smem);
       if (per_sm < 1) return cudaErrorInvalidConfiguration;
       *paths |= wide16 ? RB_PATH_GATHER_WIDE : RB_PATH_GATHER;
