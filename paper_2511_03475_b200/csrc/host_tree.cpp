@@ -370,16 +370,77 @@ rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg) {
   const int64_t V = (int64_t)vraw.size();
   lap("collapse");
 
+  // Two independent branches from here on, each on its own OpenMP team:
+  //   A (side thread): ordered prefixes of the virtual nodes (X10), then the
+  //     leaves' ordered contexts (a7) and prefix lengths;
+  //   B (this thread): children lists by rep (X12), search paths, schedule.
+  const int thA = std::max(1, nth / 2), thB = std::max(1, nth - thA);
+  H.V = V;
+  H.vparent.assign(vpar.begin(), vpar.end());
+  std::thread branchA([&] {
+    // ---- virtual nodes: ordered prefixes (X10) ------------------------------
+    // prefix(k) = prefix(parent) ++ sorted(set(k) \ set(parent)) has |set(k)|
+    // entries; each node writes its own by walking up its ancestors (depth <=
+    // K + 1 after the collapse), so the nodes are filled in parallel.
+    H.vpre_off.assign(V + 2, 0);  // by node id 0..V (root: empty)
+    for (int64_t k = 1; k <= V; ++k) {
+      int nk;
+      set_ptr(vraw[k - 1], &nk);
+      H.vpre_off[k + 1] = H.vpre_off[k] + nk;
+    }
+    H.vpre.resize(H.vpre_off[V + 1]);
+#pragma omp parallel for num_threads(thA) schedule(dynamic, 512)
+    for (int64_t k = 1; k <= V; ++k) {
+      int32_t chain[260];
+      int nc = 0;
+      for (int32_t x = (int32_t)k; x > 0; x = vpar[x - 1]) chain[nc++] = x;
+      uint32_t *o = H.vpre.data() + H.vpre_off[k];
+      for (int c = nc - 1; c >= 0; --c) {  // top-down
+        const int32_t x = chain[c], px = vpar[x - 1];
+        int nx, np = 0;
+        const uint32_t *sx = set_ptr(vraw[x - 1], &nx);
+        const uint32_t *sp = px > 0 ? set_ptr(vraw[px - 1], &np) : nullptr;
+        int q = 0;
+        for (int z = 0; z < nx; ++z) {  // both sorted: merge-difference
+          while (q < np && sp[q] < sx[z]) ++q;
+          if (q < np && sp[q] == sx[z]) continue;
+          *o++ = sx[z];
+        }
+      }
+    }
+    // ---- leaves: ordered contexts (a7) and prefix lengths -------------------
+    H.ordered.resize((size_t)N * K);  // every entry written below (no fill)
+    H.prefix_len.assign(N, 0);
+#pragma omp parallel for num_threads(thA) schedule(static)
+    for (int64_t i = 0; i < N; ++i) {
+      const int32_t p = H.lparent[i];
+      const int64_t p0 = H.vpre_off[p], p1 = H.vpre_off[p + 1];
+      uint32_t *out = H.ordered.data() + i * K;
+      int o = 0;
+      for (int64_t z = p0; z < p1; ++z) out[o++] = H.vpre[z];
+      int np = 0;
+      const uint32_t *sp = p > 0 ? set_ptr(vraw[p - 1], &np) : nullptr;
+      const uint32_t *row = H.ids.data() + i * K;
+      const int L = len_of(i);
+      for (int k = 0; k < L; ++k)
+        if (!in_sorted(sp, np, row[k])) out[o++] = row[k];
+      for (int k = L; k < K; ++k) out[k] = row[k];  // padding slots of a shorter context
+      H.prefix_len[i] = (uint8_t)(p1 - p0);
+    }
+  });
+
   // ---- children CSR over nodes 0..V, ordered by rep (X12) -----------------
   std::vector<int32_t> rep_of(1 + V + N);
   rep_of[0] = -1;
+#pragma omp parallel for num_threads(thB) schedule(static)
   for (int64_t k = 1; k <= V; ++k) rep_of[k] = H.za[vraw[k - 1] - N];  // rep = a (< b)
+#pragma omp parallel for num_threads(thB) schedule(static)
   for (int64_t i = 0; i < N; ++i) rep_of[V + 1 + i] = (int32_t)i;
   H.kids_off.assign(V + 2, 0);
   for (int64_t k = 1; k <= V; ++k) ++H.kids_off[vpar[k - 1] + 1];
   for (int64_t i = 0; i < N; ++i) ++H.kids_off[H.lparent[i] + 1];
   for (int64_t k = 0; k <= V; ++k) H.kids_off[k + 1] += H.kids_off[k];
-  H.kids.assign(V + N, 0);
+  H.kids.resize(V + N);  // every entry placed below
   std::vector<int32_t> child_idx(1 + V + N, 0);
   {
     // Nodes in ascending rep order, appended to their parents' lists, give
@@ -389,9 +450,8 @@ rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg) {
     // leftmost descendants share a rep but are never siblings).  The walk runs
     // in leaf chunks: per-chunk counts per parent, their prefix over the
     // chunks, then every chunk places its nodes.
-    const int nc = std::max(1, std::min<int>(nth, (int)(N / 4096) + 1));
+    const int nc = std::max(1, std::min<int>(thB, (int)(N / 4096) + 1));
     const int64_t P = V + 1;
-    lap("ch:csr");
     std::vector<int32_t> off((size_t)nc * P);
     auto walk = [&](int c, auto &&visit) {
       for (int64_t i = N * c / nc; i < N * (c + 1) / nc; ++i) {
@@ -410,7 +470,6 @@ rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg) {
       std::fill(o, o + P, 0);
       walk(c, [&](int32_t, int32_t par) { ++o[par]; });
     }
-    lap("ch:count");
 #pragma omp parallel for num_threads(nc) schedule(static)
     for (int64_t p = 0; p < P; ++p) {
       int32_t run = 0;
@@ -420,7 +479,6 @@ rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg) {
         run += k;
       }
     }
-    lap("ch:prefix");
 #pragma omp parallel for num_threads(nc) schedule(static, 1)
     for (int c = 0; c < nc; ++c) {
       int32_t *o = off.data() + (size_t)c * P;
@@ -433,71 +491,28 @@ rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg) {
   }
   lap("children");
 
-  // ---- virtual nodes: ordered prefixes (X10) and paths ---------------------
-  // prefix(k) = prefix(parent) ++ sorted(set(k) \ set(parent)) has |set(k)|
-  // entries; each node writes its own by walking up its ancestors (depth <=
-  // K + 1 after the collapse), so the nodes are filled in parallel.
-  H.V = V;
-  H.vparent.assign(vpar.begin(), vpar.end());
+  // ---- search paths: virtual nodes, then leaves -----------------------------
   H.vrep.resize(V);
-  H.vpre_off.assign(V + 2, 0);  // by node id 0..V (root: empty)
   std::vector<int64_t> vpath_off(V + 2, 0);
   std::vector<int32_t> depth(V + 1, 0);
   for (int64_t k = 1; k <= V; ++k) {
-    int nk;
-    set_ptr(vraw[k - 1], &nk);
     H.vrep[k - 1] = rep_of[k];
     depth[k] = depth[vpar[k - 1]] + 1;
-    H.vpre_off[k + 1] = H.vpre_off[k] + nk;
     vpath_off[k + 1] = vpath_off[k] + depth[k];
   }
-  H.vpre.resize(H.vpre_off[V + 1]);
   std::vector<int32_t> vpath(vpath_off[V + 1]);
-#pragma omp parallel for num_threads(nth) schedule(dynamic, 512)
+#pragma omp parallel for num_threads(thB) schedule(static)
   for (int64_t k = 1; k <= V; ++k) {
-    int32_t chain[260];
-    int nc = 0;
-    for (int32_t x = (int32_t)k; x > 0; x = vpar[x - 1]) chain[nc++] = x;
-    uint32_t *o = H.vpre.data() + H.vpre_off[k];
-    int32_t *pp = vpath.data() + vpath_off[k];
-    for (int c = nc - 1; c >= 0; --c) {  // top-down
-      const int32_t x = chain[c], px = vpar[x - 1];
-      int nx, np = 0;
-      const uint32_t *sx = set_ptr(vraw[x - 1], &nx);
-      const uint32_t *sp = px > 0 ? set_ptr(vraw[px - 1], &np) : nullptr;
-      int q = 0;
-      for (int z = 0; z < nx; ++z) {  // both sorted: merge-difference
-        while (q < np && sp[q] < sx[z]) ++q;
-        if (q < np && sp[q] == sx[z]) continue;
-        *o++ = sx[z];
-      }
-      *pp++ = child_idx[x];
-    }
+    int32_t *pp = vpath.data() + vpath_off[k + 1];  // filled backwards: the node, then its ancestors
+    for (int32_t x = (int32_t)k; x > 0; x = vpar[x - 1]) *--pp = child_idx[x];
   }
-  lap("virtual");
-
-  // ---- leaves (parallel): ordered contexts (a7), prefix lengths, paths -----
-  H.ordered.resize((size_t)N * K);  // every entry written below (no fill)
-  H.prefix_len.assign(N, 0);
   H.path_off.assign(N + 1, 0);
   for (int64_t i = 0; i < N; ++i) H.path_off[i + 1] = H.path_off[i] + depth[H.lparent[i]] + 1;
-  H.path.assign(H.path_off[N], 0);
+  H.path.resize(H.path_off[N]);  // every entry written below
   int64_t max_depth = 0;
-#pragma omp parallel for num_threads(nth) schedule(static) reduction(max : max_depth)
+#pragma omp parallel for num_threads(thB) schedule(static) reduction(max : max_depth)
   for (int64_t i = 0; i < N; ++i) {
     const int32_t p = H.lparent[i];
-    const int64_t p0 = H.vpre_off[p], p1 = H.vpre_off[p + 1];
-    uint32_t *out = H.ordered.data() + i * K;
-    int o = 0;
-    for (int64_t z = p0; z < p1; ++z) out[o++] = H.vpre[z];
-    int np = 0;
-    const uint32_t *sp = p > 0 ? set_ptr(vraw[p - 1], &np) : nullptr;
-    const uint32_t *row = H.ids.data() + i * K;
-    const int L = len_of(i);
-    for (int k = 0; k < L; ++k)
-      if (!in_sorted(sp, np, row[k])) out[o++] = row[k];
-    for (int k = L; k < K; ++k) out[k] = row[k];  // padding slots of a shorter context
-    H.prefix_len[i] = (uint8_t)(p1 - p0);
     int32_t *pp = H.path.data() + H.path_off[i];
     for (int64_t z = vpath_off[p]; z < vpath_off[p + 1]; ++z) *pp++ = vpath[z];
     *pp = child_idx[V + 1 + i];
@@ -505,36 +520,47 @@ rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg) {
   }
   H.stats.n_virtual = V;
   H.stats.max_depth = max_depth;
-  lap("leaves");
+  lap("paths");
 
-  // ---- schedule: counting sort by (group of first appearance, -len, index) -
+  // ---- schedule: groups of first appearance, length descending, index -----
   // The group of leaf i is the root child on its path; the first leaf of a
   // group (in index order) is the group's rep, and root children are ordered
-  // by rep (X12), so groups rank by child index.  Buckets (group, length):
-  // atomic counts and placement, then each bucket sorted by index.
+  // by rep (X12), so groups rank by child index.  A group holds the leaves of
+  // its root child's subtree (the cluster size of that child's merge): offsets
+  // by a prefix over the root children, atomic placement, then each group
+  // sorted by (length descending, index).
   {
     const int64_t G = H.kids_off[1] - H.kids_off[0];  // root children
-    const int64_t LMAX = max_depth + 1;
-    const int64_t nb = G * LMAX;
-    std::vector<int64_t> key(N);
-    std::vector<int32_t> cnt(nb + 1, 0);
-#pragma omp parallel for num_threads(nth) schedule(static)
-    for (int64_t i = 0; i < N; ++i) {
-      const int32_t g = H.path[H.path_off[i]];
-      const int64_t len = H.path_off[i + 1] - H.path_off[i];
-      key[i] = g * LMAX + (LMAX - len);  // length descending within a group
-      __atomic_fetch_add(&cnt[key[i] + 1], 1, __ATOMIC_RELAXED);
+    std::vector<int64_t> goff(G + 1, 0);
+    for (int64_t g = 0; g < G; ++g) {
+      const int32_t x = H.kids[H.kids_off[0] + g];
+      goff[g + 1] = goff[g] + (x > V ? 1 : H.zs[vraw[x - 1] - N]);
     }
-    for (int64_t z = 1; z <= nb; ++z) cnt[z] += cnt[z - 1];
-    std::vector<int32_t> cur(cnt.begin(), cnt.end() - 1);
+    if (goff[G] != N) {
+      *msg = "schedule: root subtrees do not cover the contexts";
+      branchA.join();
+      sorter.join();
+      return RB_EINVAL;
+    }
+    std::vector<int64_t> gcur(goff.begin(), goff.end() - 1);
+    // sort key within a group: (max_depth - length) << 32 | index
+    std::vector<uint64_t> sk(N);
+#pragma omp parallel for num_threads(thB) schedule(static)
+    for (int64_t i = 0; i < N; ++i) {
+      const int64_t p0 = H.path_off[i], len = H.path_off[i + 1] - p0;
+      const int32_t g = H.path[p0];
+      sk[__atomic_fetch_add(&gcur[g], 1, __ATOMIC_RELAXED)] = ((uint64_t)(max_depth - len) << 32) | (uint64_t)i;
+    }
     H.schedule.resize(N);
-#pragma omp parallel for num_threads(nth) schedule(static)
-    for (int64_t i = 0; i < N; ++i) H.schedule[__atomic_fetch_add(&cur[key[i]], 1, __ATOMIC_RELAXED)] = i;
-#pragma omp parallel for num_threads(nth) schedule(dynamic, 1024)
-    for (int64_t z = 0; z < nb; ++z)
-      if (cnt[z + 1] - cnt[z] > 1) std::sort(H.schedule.begin() + cnt[z], H.schedule.begin() + cnt[z + 1]);  // index ties
+#pragma omp parallel for num_threads(thB) schedule(dynamic, 256)
+    for (int64_t g = 0; g < G; ++g) {
+      if (goff[g + 1] - goff[g] > 1) std::sort(sk.begin() + goff[g], sk.begin() + goff[g + 1]);
+      for (int64_t z = goff[g]; z < goff[g + 1]; ++z) H.schedule[z] = (int64_t)(sk[z] & 0xffffffffull);
+    }
   }
   lap("schedule");
+  branchA.join();
+  lap("prefixes+leaves (A)");
 
   sorter.join();
   for (int64_t t = 0; t < (int64_t)zk.size(); ++t) {
