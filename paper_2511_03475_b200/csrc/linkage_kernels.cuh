@@ -441,9 +441,16 @@ __device__ int cliques_warp(const PrepArgs &a, const uint32_t *adj, int n, int W
   }
   return nseq;
 }
-// Above 4096 vertices the per-batch fold (picks x WPL loads per lane) makes
-// the single warp slower than the block-wide passes (measured at n = 16082).
-constexpr int kWarpCliqueMaxN = 32 * 32 * 4;
+// Levels above 128 vertices go to the block sweep with helper CTAs: measured
+// faster than the single warp's 32-candidate batches from n = 128 up (C4's
+// top levels of 500-2000 vertices: 0.30-0.48 -> 0.16-0.22 ms per level; a
+// tie-heavy N = 20k, K = 4 build 11.4 -> 7.4 ms of linkage).  The warp path
+// for 1024 < n <= 4096 (cliques_warp<4>) stays selectable with
+// -DRAGB_WARP_CLIQUE_MAX=4096 (the round-1 threshold).
+#ifndef RAGB_WARP_CLIQUE_MAX
+#define RAGB_WARP_CLIQUE_MAX 128
+#endif
+constexpr int kWarpCliqueMaxN = RAGB_WARP_CLIQUE_MAX;
 
 constexpr int CT = 512;  // threads of k_level_cliques (128 registers for the pick chain)
 
