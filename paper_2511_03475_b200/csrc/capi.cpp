@@ -257,6 +257,9 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
   H.alpha_den = p->alpha_den;
   const ragb::Tuning tu = ragb::Tuning::from(p);
   H.trace = tu.trace;
+#ifdef RAGB_HOST_TRACE
+  H.trace = true;  // host-stage laps on stderr (variant build for host profiling)
+#endif
   ragb::set_host_threads(tu.host_threads);
   int launches = 0;
   cudaError_t e;
