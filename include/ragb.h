@@ -110,6 +110,8 @@ typedef struct rb_params {
   int32_t side_buffer;    /* -1 auto: in-place rounds on 16-bit codes append merged
                              columns to a transposed side buffer; 0: rewrite the
                              columns in the matrix                                  */
+  int32_t nn_cache;       /* -1 auto: in-place rounds keep each rescanned row's
+                             second-nearest key; 0: every affected row rescans    */
 } rb_params;
 
 /* Per-build statistics (host, filled by rb_build_index). Times are CUDA-event

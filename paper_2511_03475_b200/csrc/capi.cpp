@@ -120,6 +120,7 @@ Tuning Tuning::from(const rb_params *p) {
   t.host_threads = p->host_threads;
   t.trace = p->trace != 0;
   t.side_buffer = p->side_buffer;
+  t.nn_cache = p->nn_cache;
   return t;
 }
 
@@ -166,6 +167,9 @@ ScratchLayout ScratchLayout::make(int64_t N, int32_t K, bool keep_rows, bool lin
     L.tslot = take(o, (size_t)N * 4);
     L.dmask = take(o, (size_t)(N / 32 + 1) * 4);
     L.tctl = take(o, 64);
+    L.nnkey2 = take(o, (size_t)N * 8);
+    L.nnround = take(o, (size_t)N * 4);
+    L.colver = take(o, (size_t)N * 4);
     // compacted matrices: at most (N-1) rows with a leading dimension padded to 4
     // (also holds an N x N copy for the intersection linkage with RB_KEEP_ROWS)
     const size_t mat = std::max((size_t)(N - 1) * (size_t)((N + 2) & ~3ll), (size_t)N * N) * 4;
@@ -212,6 +216,7 @@ rb_status rb_params_init(rb_params *p) {
   p->host_threads = 0;
   p->trace = 0;
   p->side_buffer = -1;
+  p->nn_cache = -1;
   return RB_OK;
 }
 

@@ -35,6 +35,7 @@ struct ScratchLayout {
   size_t err, idsT, nnkey, stage_ids, stage_lens, lut, lutc, vals, key0, key1, rep0, rep1, sz0, sz1, leader, aux0, aux1, aux2, aux3, aux4,
       alive, za, zb, zh, zs, amask, mlist, counters, matA, matB, total;
   size_t tcol, tslot, dmask, tctl;  // code mode: in-place side buffer maps (linkage.cu)
+  size_t nnkey2, nnround, colver;   // in-place second-nearest cache (linkage.cu)
   size_t pmap;         // code mode: int2 [N + 128] new column -> (leader, pair member), or the compact map
   size_t codes, mat16;  // code mode (inside matA): [N][N] codes, then the first compacted code matrix
   size_t ptab;          // tile path: packed Eq. 1 table (value, code << 16) [(K+1) * (K*K/2+1)]
@@ -53,6 +54,7 @@ struct Tuning {
   int host_threads = 0;         // 0 auto
   bool trace = false;           // per-round trace on stderr
   int side_buffer = -1;         // -1 auto, 0 in-place column rewrites in the matrix
+  int nn_cache = -1;            // -1 auto, 0 no second-nearest cache (every affected row rescans)
   static Tuning from(const rb_params *p);
 };
 

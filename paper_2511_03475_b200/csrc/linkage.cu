@@ -169,9 +169,9 @@ cudaError_t launch_merge(const T *cur, int64_t ld, int M, int Mn, const PrepArgs
 template <typename T>
 cudaError_t launch_inplace(T *cur, int64_t ld, int M, int max_groups, const PrepArgs &pa, int sms, uint32_t *amask,
                            int *mlist, int *nmulti, int *sz, unsigned long long *key, const SideBuf &sb,
-                           cudaStream_t st, int *launches) {
+                           const NNCache &nc, cudaStream_t st, int *launches) {
   constexpr int VW = Elem<T>::VW;
-  k_inplace_prep<<<sms * 2, 256, 0, st>>>(pa, M, amask, mlist, nmulti, sz, key, sb);
+  k_inplace_prep<<<sms * 2, 256, 0, st>>>(pa, M, amask, mlist, nmulti, sz, key, sb, nc);
   const size_t smem = (size_t)((M + VW - 1) / VW) * 16;
   if constexpr (sizeof(T) == 2) {
     if (sb.T) {
@@ -191,8 +191,8 @@ cudaError_t launch_inplace(T *cur, int64_t ld, int M, int max_groups, const Prep
                         0, st>>>(pa, cur, ld, M, amask, mlist, nmulti);
     *launches += 2;
   }
-  k_inplace_check<T><<<(M + 255) / 256, 256, 0, st>>>(pa, cur, ld, M, key, pa.cnt, nmulti + 1, sb);  // cnt: free after the compaction map
-  k_inplace_rescan<256, T><<<sms * 4, 256, 0, st>>>(cur, ld, M, amask, pa.cnt, nmulti + 1, key, sb);
+  k_inplace_check<T><<<(M + 255) / 256, 256, 0, st>>>(pa, cur, ld, M, key, pa.cnt, nmulti + 1, sb, nc);  // cnt: free after the compaction map
+  k_inplace_rescan<256, T><<<sms * 4, 256, 0, st>>>(cur, ld, M, amask, pa.cnt, nmulti + 1, key, sb, nc);
   *launches += 3;
   return cudaGetLastError();
 }
@@ -295,6 +295,20 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
   sb.dmask = at<uint32_t>(scratch, L.dmask);
   sb.nt = at<int>(scratch, L.tctl);
   int sb_used = 0;  // host upper bound of the slots in use (merges of the in-place rounds since the last flush)
+  // second-nearest cache of the in-place rounds (valid for the current matrix
+  // numbering: cleared after every compaction)
+  NNCache nc{};
+  if (tu.nn_cache != 0) {
+    nc.key2 = at<u64>(scratch, L.nnkey2);
+    nc.kround = at<int>(scratch, L.nnround);
+    nc.ver = at<int>(scratch, L.colver);
+  }
+  auto nc_reset = [&](int Mc) -> cudaError_t {
+    if (!nc.key2) return cudaSuccess;
+    cudaError_t e2 = cudaMemsetAsync(nc.kround, 0, (size_t)Mc * 4, st);
+    return e2 != cudaSuccess ? e2 : cudaMemsetAsync(nc.ver, 0, (size_t)Mc * 4, st);
+  };
+  if ((e = nc_reset((int)N)) != cudaSuccess) return e;
   if (codes && (e = side_reset(sb, (int)N, st)) != cudaSuccess) return e;
   auto side_for = [&](int Mc, void *nx) {  // the side buffer for a matrix of Mc rows with `nx` free
     SideBuf b = sb;
@@ -421,10 +435,11 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
       if (!b.T && sb_used > 0 && (e = side_flush(cur, ld, M, next)) != cudaSuccess) return e;
       if (b.T) sb_used += merges_round;  // merged groups <= merges of the round
       // merged groups <= merges of the round (the grid of the column kernel)
+      nc.round = out->rounds;
       e = codes ? launch_inplace<uint16_t>(static_cast<uint16_t *>(cur), ld, M, merges_round, pa, sms, amask, mlist,
-                                           nmulti, sz[p], key[p], b, st, launches)
+                                           nmulti, sz[p], key[p], b, nc, st, launches)
                 : launch_inplace<float>(static_cast<float *>(cur), ld, M, merges_round, pa, sms, amask, mlist, nmulti,
-                                        sz[p], key[p], SideBuf{}, st, launches);
+                                        sz[p], key[p], SideBuf{}, nc, st, launches);
       ++*launches;
       out->paths |= RB_PATH_INPLACE;
       if (e != cudaSuccess) return e;
@@ -450,6 +465,7 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
       next = (next == matA) ? matB : matA;
       ld = codes ? mat_ld<uint16_t>(Mn) : mat_ld<float>(Mn);  // padded leading dimension of the new matrix
       mask_ok = false;
+      if ((e = nc_reset(Mn)) != cudaSuccess) return e;  // new column numbering
     }
     if (trace) {
       cudaEventRecord(tev[2], st);

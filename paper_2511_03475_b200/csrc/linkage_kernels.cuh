@@ -259,6 +259,24 @@ struct SideBuf {
 };
 __device__ __forceinline__ bool sb_dirty(const SideBuf &sb, int c) { return (sb.dmask[c >> 5] >> (c & 31)) & 1u; }
 
+// Second-nearest cache of the in-place rounds.  A full rescan of row r in
+// round R also records its second-smallest key k2 = (value, column).  Every
+// other column's key exceeded k2 at the scan.  Values only grow (complete
+// linkage), and a cluster merged since from such columns (not k2's) keeps a
+// key above k2: its value is the max of its members' (>= k2's value), and if
+// equal to k2's, every member had k2's value and a larger column, so does
+// the cluster's smallest member, its index.  So as long as k2's column has
+// not merged since (ver[c] <= R), when the nearest neighbour merges into L
+// with a larger value the new key is min((d(r, L), L), k2) without a rescan
+// (hub clusters, the nearest neighbour of thousands of rows, merge
+// repeatedly in C4's late in-place rounds).  One use per scan.
+struct NNCache {
+  u64 *key2;   // [M] second-smallest key of the last full scan, or nullptr (disabled)
+  int *kround; // [M] round of that scan (0: no usable entry)
+  int *ver;    // [M] round in which column c last merged (as survivor or member)
+  int round;   // this round (>= 1)
+};
+
 // Round step 2, row form (single GPU): one CTA per level row i streams the
 // whole matrix row list[i] (16-byte loads) and sets bit lpos[c] of its
 // adjacency row for every column c holding h.  Every such column is a level
@@ -1717,7 +1735,8 @@ __global__ void __launch_bounds__(NTH) k_merge_gather2(const uint16_t *__restric
 // S0: per-row flags; multi-member groups -> mlist; members other than the
 // survivor -> dead; the survivor's size.
 __global__ void k_inplace_prep(PrepArgs a, int M, uint32_t *__restrict__ amask, int *__restrict__ mlist,
-                               int *__restrict__ nmulti, int *__restrict__ sz, u64 *__restrict__ key, SideBuf sb) {
+                               int *__restrict__ nmulti, int *__restrict__ sz, u64 *__restrict__ key, SideBuf sb,
+                               NNCache nc) {
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < M; x += gridDim.x * blockDim.x) {
     const int l = a.leader[x];
     uint8_t chg = 0;
@@ -1725,6 +1744,10 @@ __global__ void k_inplace_prep(PrepArgs a, int M, uint32_t *__restrict__ amask, 
       const int g = a.newidx[l];
       if (a.goff[g + 1] - a.goff[g] >= 2) {
         chg = 1;
+        if (nc.key2) {
+          nc.ver[x] = nc.round;
+          nc.kround[x] = 0;  // the survivor's row is recomputed; members die
+        }
         if (x != l) {
           key[x] = kDead;
           atomicAnd(&amask[x >> 5], ~(1u << (x & 31)));
@@ -2019,7 +2042,8 @@ __global__ void __launch_bounds__(256) k_inplace_cols(PrepArgs a, T *__restrict_
 // larger); otherwise r goes to the rescan list.
 template <typename T>
 __global__ void k_inplace_check(PrepArgs a, const T *__restrict__ D, int64_t ld, int M,
-                                u64 *__restrict__ key, int *__restrict__ rlist, int *__restrict__ nres, SideBuf sb) {
+                                u64 *__restrict__ key, int *__restrict__ rlist, int *__restrict__ nres, SideBuf sb,
+                                NNCache nc) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < M; r += gridDim.x * blockDim.x) {
     const u64 kr = key[r];
     if (kr == kDead || a.alive[r]) continue;  // dead, or a survivor (done in S1)
@@ -2027,29 +2051,47 @@ __global__ void k_inplace_check(PrepArgs a, const T *__restrict__ D, int64_t ld,
     if (!a.alive[t]) continue;  // neighbour not merged: unchanged
     const int Lg = a.leader[t];
     const unsigned v = sb.T ? (unsigned)sb.T[(int64_t)r * sb.cap + sb.tslot[Lg]] : Elem<T>::bits(D[(int64_t)r * ld + Lg]);
-    if (v == (unsigned)(kr >> 32))
+    if (v == (unsigned)(kr >> 32)) {
       key[r] = ((u64)v << 32) | (unsigned)Lg;
-    else
-      rlist[atomicAdd(nres, 1)] = r;
+    } else {
+      const int kround = nc.key2 ? nc.kround[r] : 0;
+      const u64 k2 = kround > 0 ? nc.key2[r] : ~0ull;
+      if (kround > 0 && nc.ver[(int)(k2 & 0xffffffffu)] <= kround) {
+        const u64 kL = ((u64)v << 32) | (unsigned)Lg;  // (the second-nearest cache, one use)
+        key[r] = kL < k2 ? kL : k2;
+        nc.kround[r] = 0;
+      } else {
+        rlist[atomicAdd(nres, 1)] = r;
+      }
+    }
   }
 }
 
 // S3b: full rescans of the listed rows over the live columns.
+// Keeps the two smallest keys b[0] < b[1] (a cheap reject first).
+__device__ __forceinline__ void top2_insert(u64 (&b)[2], u64 kk) {
+  if (kk < b[1]) {
+    const bool l1 = kk < b[0];
+    b[1] = l1 ? b[0] : kk;
+    b[0] = l1 ? kk : b[0];
+  }
+}
+
 template <int NTH, typename T>
 __global__ void __launch_bounds__(NTH) k_inplace_rescan(const T *__restrict__ D, int64_t ld, int M,
                                                         const uint32_t *__restrict__ amask,
                                                         const int *__restrict__ rlist,
                                                         const int *__restrict__ nres_p, u64 *__restrict__ key,
-                                                        SideBuf sb) {
+                                                        SideBuf sb, NNCache nc) {
   typedef Elem<T> E;
   constexpr int VW = E::VW;
-  __shared__ u64 wmin[NTH / 32];
+  __shared__ u64 wmin[NTH / 32][2];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int MV = (M + VW - 1) / VW;
   const int nres = *nres_p;
   for (int i = blockIdx.x; i < nres; i += gridDim.x) {
     const int r = rlist[i];
-    u64 best = ~0ull;
+    u64 bt[2] = {~0ull, ~0ull};  // the row's two smallest keys (this thread)
     const uint4 *src = reinterpret_cast<const uint4 *>(D + (int64_t)r * ld);
     constexpr int UR = 4;  // vectors in flight per thread
     for (int q0 = tid; q0 < MV; q0 += NTH * UR) {
@@ -2071,8 +2113,7 @@ __global__ void __launch_bounds__(NTH) k_inplace_rescan(const T *__restrict__ D,
         for (int k = 0; k < VW; ++k) {
           const int c = c0 + k;
           const bool live = ((mb >> k) & 1u) && c < M && c != r;
-          const u64 kk = ((u64)vv[k] << 32) | (unsigned)c;
-          best = (live && kk < best) ? kk : best;
+          top2_insert(bt, live ? (((u64)vv[k] << 32) | (unsigned)c) : ~0ull);
         }
       }
     }
@@ -2089,24 +2130,33 @@ __global__ void __launch_bounds__(NTH) k_inplace_rescan(const T *__restrict__ D,
           vs[u] = k < nt ? trow[k] : 0u;
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const u64 kk = ((u64)vs[u] << 32) | (unsigned)cs[u];
-          best = (cs[u] >= 0 && cs[u] != r && kk < best) ? kk : best;
-        }
+        for (int u = 0; u < 4; ++u)
+          top2_insert(bt, (cs[u] >= 0 && cs[u] != r) ? (((u64)vs[u] << 32) | (unsigned)cs[u]) : ~0ull);
       }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      const u64 y = __shfl_xor_sync(0xffffffffu, best, o);
-      best = y < best ? y : best;
+      u64 y[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) y[q] = __shfl_xor_sync(0xffffffffu, bt[q], o);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) top2_insert(bt, y[q]);
     }
-    if (lane == 0) wmin[w] = best;
+    if (lane == 0) {
+      wmin[w][0] = bt[0];
+      wmin[w][1] = bt[1];
+    }
     __syncthreads();
     if (tid == 0) {
-      u64 b = wmin[0];
+      u64 b[2] = {wmin[0][0], wmin[0][1]};
+      for (int i2 = 1; i2 < NTH / 32; ++i2)
 #pragma unroll
-      for (int i2 = 1; i2 < NTH / 32; ++i2) b = wmin[i2] < b ? wmin[i2] : b;
-      key[r] = b;
+        for (int q = 0; q < 2; ++q) top2_insert(b, wmin[i2][q]);
+      key[r] = b[0];
+      if (nc.key2) {  // the second-nearest cache
+        nc.key2[r] = b[1];
+        nc.kround[r] = b[1] != ~0ull ? nc.round : 0;
+      }
     }
     __syncthreads();
   }

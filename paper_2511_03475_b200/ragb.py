@@ -56,10 +56,10 @@ class Params(ctypes.Structure):
                 ("inplace_weight", ctypes.c_float), ("gather", ctypes.c_int32),
                 ("long_lists", ctypes.c_int32), ("dist_grid", ctypes.c_int32),
                 ("host_threads", ctypes.c_int32), ("trace", ctypes.c_int32),
-                ("side_buffer", ctypes.c_int32)]
+                ("side_buffer", ctypes.c_int32), ("nn_cache", ctypes.c_int32)]
 
 TUNING_FIELDS = ("value_codes", "inplace", "inplace_weight", "gather", "long_lists", "dist_grid",
-                 "host_threads", "trace", "side_buffer")
+                 "host_threads", "trace", "side_buffer", "nn_cache")
 
 
 class Stats(ctypes.Structure):

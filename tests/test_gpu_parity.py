@@ -314,7 +314,7 @@ def test_round_strategy(mode, case, codes, side):
     implementation choices, X7-X9 fix the result)."""
     if mode == 0 and side == 0:
         pytest.skip("no in-place rounds: the side buffer is not used")
-    tu = dict(inplace=mode, value_codes=codes, side_buffer=side)
+    tu = dict(inplace=mode, value_codes=codes, side_buffer=side, nn_cache=-1 if side else 0)
     if case == "C2":
         idx = check_full(config("C2").ids, counts=False, tuning=tu)
     elif case == "var":
@@ -362,13 +362,14 @@ def test_code_window_compaction(case):
 def test_round_strategy_full_size():
     """At C4 size (level cliques above 4096 vertices, block path) the merge
     order and the document order do not depend on the round strategy, on the
-    stored form of the matrices (fp32 values or 16-bit value codes) nor on
-    the in-place side buffer."""
+    stored form of the matrices (fp32 values or 16-bit value codes), on the
+    in-place side buffer nor on the second-nearest cache."""
     ids = config("C4").ids
     t = torch.from_numpy(ids.view(np.int32)).cuda()
     res = []
-    for mode, codes, side in ((0, -1, -1), (-1, -1, -1), (-1, 0, -1), (-1, -1, 0)):
-        idx, ws = F.build_index(t, tuning=dict(inplace=mode, value_codes=codes, side_buffer=side))
+    for mode, codes, side, nnc in ((0, -1, -1, -1), (-1, -1, -1, -1), (-1, 0, -1, -1), (-1, -1, 0, -1),
+                                   (-1, -1, -1, 0)):
+        idx, ws = F.build_index(t, tuning=dict(inplace=mode, value_codes=codes, side_buffer=side, nn_cache=nnc))
         res.append((idx.linkage(), idx.order_contexts()))
         del idx, ws
         torch.cuda.empty_cache()
