@@ -260,9 +260,12 @@ def run_ours(args, ws, rank, local):
         def build(ids):
             return ragb.build_index(ids, workspace=wsp, stream=stream)[0]
 
+    # the caller's output arrays, reused across builds (page-faulted once)
+    ord_out = (np.empty((N, K), dtype=np.uint32), np.empty(N, dtype=np.uint8), np.empty(N, dtype=np.int64))
+
     def step():
         idx = build(ids_dev)
-        idx.order_contexts()
+        idx.order_contexts(out=ord_out)
         return idx
 
     for _ in range(args.warmup):
@@ -304,7 +307,7 @@ def run_ours(args, ws, rank, local):
             idx = db.build(ids_d, stream=stream)
         else:
             idx, _ = ragb.build_index_host(ids_pin.numpy().view(np.uint32), workspace=wsp, stream=stream)
-        out, plen, sched = idx.order_contexts()
+        out, plen, sched = idx.order_contexts(out=ord_out)
         nn_i, nn_d = idx.nn()
         za = idx.linkage()
         return idx

@@ -278,12 +278,20 @@ class Index:
                                        _np_ptr(plen), _np_ptr(sched)))
         return out, plen, sched
 
-    def order_contexts(self):
-        """Offline prefix-first ordering + schedule of the indexed set."""
+    def order_contexts(self, out=None):
+        """Offline prefix-first ordering + schedule of the indexed set.
+        ``out``: optional (ordered [n][K] uint32, prefix_len [n] uint8,
+        schedule [n] int64) arrays to fill (reused across calls)."""
         n = self.size()
-        out = np.empty((n, self.K), dtype=np.uint32)
-        plen = np.empty(n, dtype=np.uint8)
-        sched = np.empty(n, dtype=np.int64)
+        if out is None:
+            out, plen, sched = (np.empty((n, self.K), dtype=np.uint32), np.empty(n, dtype=np.uint8),
+                                np.empty(n, dtype=np.int64))
+        else:
+            out, plen, sched = out
+            if (out.shape != (n, self.K) or out.dtype != np.uint32 or plen.shape != (n,) or plen.dtype != np.uint8
+                    or sched.shape != (n,) or sched.dtype != np.int64
+                    or not all(a.flags.c_contiguous for a in (out, plen, sched))):
+                raise ValueError("order_contexts: out arrays must be C-contiguous uint32 [n][K], uint8 [n], int64 [n]")
         _check(lib().rb_order_contexts(self._h, None, None, n, self.K, _np_ptr(out), _np_ptr(plen),
                                        _np_ptr(sched)))
         return out, plen, sched

@@ -180,3 +180,20 @@ def test_session_from_index_path():
     with pytest.raises(ragb.RagbError) as e:
         idx.session(7)
     assert e.value.code == ragb.RB_EPATH
+
+
+def test_order_contexts_into_caller_arrays():
+    """order_contexts(out=...) fills the caller's arrays (reused across calls)
+    with exactly what the allocating form returns, and rejects mismatched
+    arrays."""
+    w = generate(300, 6, 900, 77)
+    ids = w.ids
+    idx = ragb.index_from_linkage(ids, *oc.linkage(oc.pairwise_rows(ids, None, 1, 200)))
+    ref = idx.order_contexts()
+    bufs = (np.zeros((300, 6), dtype=np.uint32), np.zeros(300, dtype=np.uint8), np.zeros(300, dtype=np.int64))
+    for _ in range(2):
+        got = idx.order_contexts(out=bufs)
+        assert all(g is b for g, b in zip(got, bufs))
+        assert all(np.array_equal(g, r) for g, r in zip(got, ref))
+    with pytest.raises(ValueError):
+        idx.order_contexts(out=(bufs[0], bufs[1], np.zeros(300, dtype=np.int32)))
