@@ -305,13 +305,6 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
   RB_CUDA(ragb::launch_validate(ids_d, lens_d, N, K, Npad, idsT, err_d, st, &launches), "validate");
   uint32_t err_h = 0;
   RB_CUDA(cudaMemcpyAsync(&err_h, err_d, 4, cudaMemcpyDeviceToHost, st), "D2H err");
-  // host copy of the contexts for the tree stage (overlaps the distance kernel)
-  H.ids.resize((size_t)N * K);
-  if (lens_d) H.lens.resize((size_t)N);
-  if (ids_host) {
-    std::memcpy(H.ids.data(), ids_host, (size_t)N * K * 4);
-    if (lens_host) std::memcpy(H.lens.data(), lens_host, (size_t)N);
-  }
   RB_CUDA(cudaStreamSynchronize(st), "validate sync");
   if (err_h & ragb::kErrLen) return cleanup(fail(RB_EINVAL, "context length not in [1, K]"));
   if (err_h & ragb::kErrReserved) return cleanup(fail(RB_EINVAL, "reserved DocId 0xFFFFFFFF"));
@@ -374,7 +367,13 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
   }
   RB_CUDA(ragb::launch_distance(da, st, &launches), "distance kernel");
   RB_CUDA(cudaEventRecord(ev[2], st), "event");
-  if (!ids_host) {
+  // host copy of the contexts for the tree stage, while the distance kernel runs
+  H.ids.resize((size_t)N * K);
+  if (lens_d) H.lens.resize((size_t)N);
+  if (ids_host) {
+    std::memcpy(H.ids.data(), ids_host, (size_t)N * K * 4);
+    if (lens_host) std::memcpy(H.lens.data(), lens_host, (size_t)N);
+  } else {
     // the host copy of the contexts (tree stage) comes from the caller's
     // buffer on a side stream while the distance kernel runs (the input is
     // complete: the stream was synchronised after validation)
