@@ -97,9 +97,32 @@ size_t dyn_smem_limit(F kern) {
 // Compaction launch for element type T (see k_merge_rows): wide rows get
 // 1024-thread CTAs, one per SM, with a window of up to 56K columns; narrow
 // rows 256-thread CTAs so that several rows are in flight per SM.
+// The code-mode compaction kernel with the compact map (k_merge_gather2) for
+// this round, or nullptr when another form runs (launch_merge).
+typedef void (*Gather2Fn)(const uint16_t *, int64_t, int, const int *, const int *, const int *, const uint32_t *,
+                          const int *, uint16_t *, u64 *, int, SideBuf);
+template <typename T>
+Gather2Fn gather2_kernel(const void *cur, int64_t ld, int M, int Mn, const PrepArgs &pa, const Tuning &tu, bool *mid_out) {
+  const size_t row_bytes = (size_t)((M + 7) / 8) * 16;
+  const bool vec16 = ld % 8 == 0 && (reinterpret_cast<uintptr_t>(cur) & 15) == 0;
+  const bool wide16 = M > 16 * 1024;
+  const bool compact = sizeof(T) == 2 && pa.pmap && pa.nclq && pm32_fits(M, Mn);  // k_compact_maps wrote pm32
+  if (!compact || tu.gather == 0) return nullptr;
+  // rows that fit twice in half the shared memory (M <= ~28K): two 512-thread
+  // CTAs per SM, each double-buffered
+  const bool mid = wide16 && vec16 && 4 * row_bytes + 4096 <= 227 * 1024 && tu.gather != 2;
+  Gather2Fn kern = mid ? k_merge_gather2<true, 512>
+                       : wide16 ? (vec16 ? k_merge_gather2<true, 1024> : k_merge_gather2<false, 1024>)
+                                : (vec16 ? k_merge_gather2<true, 256> : k_merge_gather2<false, 256>);
+  if (row_bytes > dyn_smem_limit(kern)) return nullptr;
+  if (mid_out) *mid_out = mid;
+  return kern;
+}
+
 template <typename T>
 cudaError_t launch_merge(const T *cur, int64_t ld, int M, int Mn, const PrepArgs &pa, int sms, T *next,
-                         unsigned long long *keyn, cudaStream_t st, const Tuning &tu, unsigned *paths) {
+                         unsigned long long *keyn, cudaStream_t st, const Tuning &tu, unsigned *paths,
+                         const SideBuf &patch) {
   constexpr int VW = Elem<T>::VW;
   const size_t row_bytes = (size_t)((M + 7) / 8) * 16;
   const bool vec16 = ld % 8 == 0 && (reinterpret_cast<uintptr_t>(cur) & 15) == 0;
@@ -107,16 +130,11 @@ cudaError_t launch_merge(const T *cur, int64_t ld, int M, int Mn, const PrepArgs
   auto gkern = wide16 ? (vec16 ? k_merge_gather<true, 1024> : k_merge_gather<false, 1024>)
                       : (vec16 ? k_merge_gather<true, 256> : k_merge_gather<false, 256>);
   const bool compact = sizeof(T) == 2 && pa.pmap && pa.nclq && pm32_fits(M, Mn);  // k_compact_maps wrote pm32
-  if (compact && tu.gather != 0) {
-    // code mode with the compact map: k_merge_gather2 when the old row fits
-    // rows that fit twice in half the shared memory (M <= ~28K): two
-    // 512-thread CTAs per SM, each double-buffered
-    const bool mid = wide16 && vec16 && 4 * row_bytes + 4096 <= 227 * 1024 && tu.gather != 2;
-    auto kern = mid ? k_merge_gather2<true, 512>
-                    : wide16 ? (vec16 ? k_merge_gather2<true, 1024> : k_merge_gather2<false, 1024>)
-                             : (vec16 ? k_merge_gather2<true, 256> : k_merge_gather2<false, 256>);
+  bool mid = false;
+  if (Gather2Fn kern = gather2_kernel<T>(cur, ld, M, Mn, pa, tu, &mid)) {
+    // code mode with the compact map: k_merge_gather2 (the old row fits)
     const size_t lim = dyn_smem_limit(kern);
-    if (row_bytes <= lim) {
+    {
       const int db = vec16 && 2 * row_bytes <= lim ? 1 : 0;  // double-buffered rows
       const size_t smem = row_bytes * (1 + db);
       const int nth = mid ? 512 : wide16 ? 1024 : 256;
@@ -126,11 +144,12 @@ cudaError_t launch_merge(const T *cur, int64_t ld, int M, int Mn, const PrepArgs
       const int grid = std::min<int>(Mn, sms * per_sm);
       kern<<<grid, nth, smem, st>>>(reinterpret_cast<const uint16_t *>(cur), ld, M, pa.Mn, pa.goff, pa.gmem,
                                     reinterpret_cast<const uint32_t *>(pa.pmap), pa.nclq,
-                                    reinterpret_cast<uint16_t *>(next), keyn, db);
+                                    reinterpret_cast<uint16_t *>(next), keyn, db, patch);
       return cudaGetLastError();
     }
   }
   const size_t glim = sizeof(T) == 2 && pa.pmap && !compact ? dyn_smem_limit(gkern) : 0;
+  if (patch.T) return cudaErrorInvalidValue;  // dirty columns only through k_merge_gather2 (the caller flushes)
   if (sizeof(T) == 2 && pa.pmap && !compact && row_bytes <= glim && tu.gather != 0) {
     // code mode, old row fits in shared memory: gather form (k_merge_gather)
     const uint16_t *c16 = reinterpret_cast<const uint16_t *>(cur);
@@ -357,7 +376,7 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
       // level rows streamed whole (k_level_adj_rows); W words of bits per row
       // in shared memory (the level has at most M vertices)
       const bool vec = ld % (codes ? 8 : 4) == 0 && (reinterpret_cast<uintptr_t>(cur) & 15) == 0;
-      const size_t smem = (size_t)((M + 31) / 32) * 4;
+      const size_t smem = (size_t)((M + 31) / 32) * 12;  // row bits, level mask, mask prefix
       const int grid = std::min(M, sms * 8);
       if (codes) {
         // dirty columns (side buffer in use) need the vector path, which in-place rounds guarantee
@@ -444,15 +463,31 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
       out->paths |= RB_PATH_INPLACE;
       if (e != cudaSuccess) return e;
     } else if (Mn > 1) {
-      if ((e = side_flush(cur, ld, M, next)) != cudaSuccess) return e;  // dirty columns back into the matrix
+      // dirty columns of the side buffer: patched into the staged old rows by
+      // k_merge_gather2 when it runs and its output stays clear of the buffer
+      // (it is written into the same free region), else flushed first
+      SideBuf patch{};
+      if (sb_used > 0) {
+        const SideBuf b = side_for(M, next);
+        const size_t new_bytes = (size_t)Mn * (size_t)mat_ld<uint16_t>(Mn) * 2;
+        if (codes && b.T && gather2_kernel<uint16_t>(cur, ld, M, Mn, pa, tu, nullptr) &&
+            new_bytes <= (size_t)(reinterpret_cast<unsigned char *>(b.T) - static_cast<unsigned char *>(next)))
+          patch = b;
+        else if ((e = side_flush(cur, ld, M, next)) != cudaSuccess)
+          return e;
+      }
       cudaEvent_t me[2];
       cudaEventCreateWithFlags(&me[0], cudaEventDefault);
       cudaEventCreateWithFlags(&me[1], cudaEventDefault);
       cudaEventRecord(me[0], st);
       e = codes ? launch_merge<uint16_t>(static_cast<const uint16_t *>(cur), ld, M, Mn, pa, sms,
-                                         static_cast<uint16_t *>(next), key[p ^ 1], st, tu, &out->paths)
+                                         static_cast<uint16_t *>(next), key[p ^ 1], st, tu, &out->paths, patch)
                 : launch_merge<float>(static_cast<const float *>(cur), ld, M, Mn, pa, sms, static_cast<float *>(next),
-                                      key[p ^ 1], st, tu, &out->paths);
+                                      key[p ^ 1], st, tu, &out->paths, patch);
+      if (e == cudaSuccess && patch.T) {  // the side buffer was consumed by the compaction
+        sb_used = 0;
+        e = side_reset(sb, M, st);
+      }
       cudaEventRecord(me[1], st);
       mev.push_back(me[0]);
       mev.push_back(me[1]);

@@ -284,16 +284,47 @@ struct NNCache {
 // level (rows merged away by in-place rounds hold stale values) are skipped.
 template <typename T, bool VEC>
 __global__ void __launch_bounds__(256) k_level_adj_rows(PrepArgs a, uint32_t *__restrict__ adj, SideBuf sb) {
-  extern __shared__ uint32_t wbits[];  // [W]
+  // [W] this row's adjacency bits, then the level's column mask [MW] and its
+  // per-word exclusive popcount prefix [MW]: a column's level position is
+  // lpre[c / 32] + popc(lmask[c / 32] below c) — no global lookups per match
+  extern __shared__ uint32_t wbits[];
+  __shared__ int wsum[8];
   const int n = a.level[0];
-  if (n < 2) return;
+  if (n < 2 || (int)blockIdx.x >= n) return;
   typedef Elem<T> E;
   constexpr int VW = E::VW;
   const unsigned hb = (unsigned)a.level[1];
   const T *D = static_cast<const T *>(a.D);
-  const int W = (n + 31) >> 5, M = a.M;
-  const int *__restrict__ lpos = a.lpos;
+  const int W = (n + 31) >> 5, M = a.M, MW = (M + 31) >> 5;
+  uint32_t *lmask = wbits + MW;  // (wbits is sized for any level of this matrix: MW words)
+  uint32_t *lpre = lmask + MW;
   const uint8_t *__restrict__ lev = a.alive;  // level flags (k_prep_rnn)
+  for (int w = threadIdx.x; w < MW; w += blockDim.x) {
+    const uint32_t *l4 = reinterpret_cast<const uint32_t *>(lev + 32 * w);
+    uint32_t m = 0u;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint32_t x = 32 * w + 4 * q < M ? __ldg(l4 + q) : 0u;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) m |= (((x >> (8 * b)) & 0xffu) != 0u ? 1u : 0u) << (4 * q + b);
+    }
+    if (32 * w + 32 > M) m &= (1u << (M - 32 * w)) - 1u;
+    lmask[w] = m;
+  }
+  __syncthreads();
+  {
+    const int per = (MW + (int)blockDim.x - 1) / (int)blockDim.x;
+    const int w0 = min(MW, (int)threadIdx.x * per), w1 = min(MW, w0 + per);
+    int cnt = 0;
+    for (int w = w0; w < w1; ++w) cnt += __popc(lmask[w]);
+    int pre = block_excl_scan<256>(cnt, wsum);
+    for (int w = w0; w < w1; ++w) {
+      lpre[w] = (uint32_t)pre;
+      pre += __popc(lmask[w]);
+    }
+  }
+  __syncthreads();
+  const int *__restrict__ lpos = a.lpos;  // (dirty columns and the scalar path)
   for (int i = blockIdx.x; i < n; i += gridDim.x) {
     for (int w = threadIdx.x; w < W; w += blockDim.x) wbits[w] = 0u;
     __syncthreads();
@@ -304,11 +335,19 @@ __global__ void __launch_bounds__(256) k_level_adj_rows(PrepArgs a, uint32_t *__
       for (int q = threadIdx.x; q * VW < M; q += blockDim.x) {
         unsigned v[VW];
         E::unpack(__ldg(row4 + q), v);
+        const int c0 = q * VW;  // VW columns in one mask word
+        const uint32_t mw = lmask[c0 >> 5];
+        const uint32_t below = mw & ((1u << (c0 & 31)) - 1u);
+        const uint32_t mb = (mw >> (c0 & 31)) & ((1u << VW) - 1u);
+        if (mb == 0u) continue;
+        // dirty columns (side buffer) hold stale values here: taken from T below
+        const uint32_t clean = sb.T ? ~(sb.dmask[c0 >> 5] >> (c0 & 31)) : ~0u;
+        const int base = (int)lpre[c0 >> 5] + __popc(below);
 #pragma unroll
         for (int k = 0; k < VW; ++k) {
-          const int c = q * VW + k;
-          if (v[k] == hb && c < M && c != r && !(sb.T && sb_dirty(sb, c)) && lev[c]) {
-            const int j = lpos[c];
+          const int c = c0 + k;
+          if (((mb & clean) >> k & 1u) && v[k] == hb && c != r) {
+            const int j = base + __popc(mb & ((1u << k) - 1u));
             atomicOr(&wbits[j >> 5], 1u << (j & 31));
           }
         }
@@ -1509,7 +1548,7 @@ __global__ void __launch_bounds__(NTH) k_merge_gather2(const uint16_t *__restric
                                                        const int *__restrict__ Mn_p, const int *__restrict__ goff,
                                                        const int *__restrict__ gmem, const uint32_t *__restrict__ pm,
                                                        const int *__restrict__ nclq_p, uint16_t *__restrict__ Dn,
-                                                       u64 *__restrict__ keyn, int db) {
+                                                       u64 *__restrict__ keyn, int db, SideBuf sb) {
   constexpr int NWARP = NTH / 32;
   constexpr int kMaxChunks = 32;  // chunks per row (progressive refill needs Mn / (4 * CQ) <= kMaxChunks)
   extern __shared__ __align__(16) uint4 smem4[];  // [1 + db][ceil(M / 8)]
@@ -1609,6 +1648,19 @@ __global__ void __launch_bounds__(NTH) k_merge_gather2(const uint16_t *__restric
         }
       }
     }
+    if (sb.T) {
+      // dirty columns of the in-place side buffer (see SideBuf): the row's
+      // value at a dirty column is the max of its members' T entries
+      const int nt = *sb.nt;
+      __syncthreads();
+      for (int k = tid; k < nt; k += NTH) {
+        const int col = sb.tcol[k];
+        if (col < 0) continue;
+        unsigned v = 0u;
+        for (int rr = rb; rr < re; ++rr) v = max(v, (unsigned)sb.T[(int64_t)gmem[rr] * sb.cap + k]);
+        srow[col] = (uint16_t)v;
+      }
+    }
     if (nclq > 0) {
       __syncthreads();
       for (int i = tid; i < nclq; i += NTH) {  // 3+-member groups: members folded into the leader's slot
@@ -1618,7 +1670,7 @@ __global__ void __launch_bounds__(NTH) k_merge_gather2(const uint16_t *__restric
         srow[g + (int)(pm[pm32_index(g)] & 0x7fffu)] = (uint16_t)v;
       }
     }
-    if (!VEC || re - rb > 1 || nclq > 0) __syncthreads();
+    if (!VEC || re - rb > 1 || nclq > 0 || sb.T) __syncthreads();
     // ---- phase 2: gather -------------------------------------------------------
     uint2 *__restrict__ out4 = reinterpret_cast<uint2 *>(Dn + (int64_t)c * ldn);
     const int qc = c >> 2;  // the quad holding the diagonal
