@@ -211,7 +211,11 @@ cudaError_t launch_inplace(T *cur, int64_t ld, int M, int max_groups, const Prep
     *launches += 2;
   }
   k_inplace_check<T><<<(M + 255) / 256, 256, 0, st>>>(pa, cur, ld, M, key, pa.cnt, nmulti + 1, sb, nc);  // cnt: free after the compaction map
-  k_inplace_rescan<256, T><<<sms * 4, 256, 0, st>>>(cur, ld, M, amask, pa.cnt, nmulti + 1, key, sb, nc);
+  {
+    const size_t rs = (size_t)(((M / 32 + 1) + 3) & ~3) * 4 + (size_t)(sb.T ? sb.cap : 0) * 4;  // scan mask + slot columns
+    occupancy_cached(k_inplace_rescan<256, T>, 256, rs);
+    k_inplace_rescan<256, T><<<sms * 4, 256, rs, st>>>(cur, ld, M, amask, pa.cnt, nmulti + 1, key, sb, nc);
+  }
   *launches += 3;
   return cudaGetLastError();
 }

@@ -2138,9 +2138,20 @@ __global__ void __launch_bounds__(NTH) k_inplace_rescan(const T *__restrict__ D,
   typedef Elem<T> E;
   constexpr int VW = E::VW;
   __shared__ u64 wmin[NTH / 32][2];
+  // the scan mask (live and clean columns) and the side buffer's slot
+  // columns, the same for every row: staged once per CTA
+  extern __shared__ __align__(16) unsigned char rsmem[];
+  unsigned *smask = reinterpret_cast<unsigned *>(rsmem);  // [M/32 + 1]
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int MV = (M + VW - 1) / VW;
   const int nres = *nres_p;
+  if ((int)blockIdx.x >= nres) return;
+  const int MW = M / 32 + 1;
+  int *scol = reinterpret_cast<int *>(smask + ((MW + 3) & ~3));  // [nt]
+  const int nt = sb.T ? *sb.nt : 0;
+  for (int k = tid; k < MW; k += NTH) smask[k] = amask[k] & ~(sb.T ? sb.dmask[k] : 0u);
+  for (int k = tid; k < nt; k += NTH) scol[k] = sb.tcol[k];
+  __syncthreads();
   for (int i = blockIdx.x; i < nres; i += gridDim.x) {
     const int r = rlist[i];
     u64 bt[2] = {~0ull, ~0ull};  // the row's two smallest keys (this thread)
@@ -2159,7 +2170,7 @@ __global__ void __launch_bounds__(NTH) k_inplace_rescan(const T *__restrict__ D,
         // the vector's VW columns lie in one mask word: live and (with a side
         // buffer) clean
         const int c0 = VW * q;
-        const unsigned mw = amask[c0 >> 5] & ~(sb.T ? sb.dmask[c0 >> 5] : 0u);
+        const unsigned mw = smask[c0 >> 5];
         const unsigned mb = (mw >> (c0 & 31)) & ((1u << VW) - 1u);
 #pragma unroll
         for (int k = 0; k < VW; ++k) {
@@ -2169,21 +2180,17 @@ __global__ void __launch_bounds__(NTH) k_inplace_rescan(const T *__restrict__ D,
         }
       }
     }
-    if (sb.T) {  // dirty columns from the side buffer (retired slots: tcol -1, incl. dead columns)
-      const int nt = *sb.nt;
-      const uint16_t *trow = sb.T + (int64_t)r * sb.cap;
-      for (int k0 = tid; k0 < nt; k0 += NTH * 4) {
-        int cs[4];
-        unsigned vs[4];
+    if (nt > 0) {  // dirty columns from the side buffer (retired slots: tcol -1, incl. dead columns)
+      const uint4 *trow4 = reinterpret_cast<const uint4 *>(sb.T + (int64_t)r * sb.cap);  // 8 slots per vector
+      for (int k8 = tid; 8 * k8 < nt; k8 += NTH) {
+        unsigned vs[8];
+        Elem<uint16_t>::unpack(trow4[k8], vs);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int k = k0 + u * NTH;
-          cs[u] = k < nt ? __ldg(sb.tcol + k) : -1;
-          vs[u] = k < nt ? trow[k] : 0u;
+        for (int u = 0; u < 8; ++u) {
+          const int k = 8 * k8 + u;
+          const int c = k < nt ? scol[k] : -1;
+          top2_insert(bt, (c >= 0 && c != r) ? (((u64)vs[u] << 32) | (unsigned)c) : ~0ull);
         }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          top2_insert(bt, (cs[u] >= 0 && cs[u] != r) ? (((u64)vs[u] << 32) | (unsigned)cs[u]) : ~0ull);
       }
     }
 #pragma unroll
