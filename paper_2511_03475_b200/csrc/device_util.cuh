@@ -94,6 +94,13 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned pari
       "r"(parity)
       : "memory");
 }
+// 16-bit shared-memory load into a 32-bit register (zero-extended), by
+// shared-window byte address
+__device__ __forceinline__ unsigned lds_u16(unsigned addr) {
+  unsigned v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
 // L2 prefetch of [src, src + bytes) by the TMA engine (16-byte aligned, multiple of 16)
 __device__ __forceinline__ void bulk_prefetch_l2(const void *src, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");

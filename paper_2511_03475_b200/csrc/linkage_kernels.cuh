@@ -1673,6 +1673,7 @@ __global__ void __launch_bounds__(NTH) k_merge_gather2(const uint16_t *__restric
     if (!VEC || re - rb > 1 || nclq > 0 || sb.T) __syncthreads();
     // ---- phase 2: gather -------------------------------------------------------
     uint2 *__restrict__ out4 = reinterpret_cast<uint2 *>(Dn + (int64_t)c * ldn);
+    const unsigned sbase = smem_u32(srow);
     const int qc = c >> 2;  // the quad holding the diagonal
     // row minimum per thread: value << 16 | step << 2 | k (steps in increasing
     // column order: the strict minimum keeps the smallest column, X8)
@@ -1697,17 +1698,22 @@ __global__ void __launch_bounds__(NTH) k_merge_gather2(const uint16_t *__restric
         if (4 * q + 3 < Mn) {
           const int t = 4 * q;
           const unsigned ev[4] = {ec.x, ec.y, ec.z, ec.w};
+          // shared-window byte addresses: s[t + k + off] at sbase + 2 (t + k) + 2 off
+          const unsigned a0 = sbase + 8u * (unsigned)q;
           unsigned v[4];
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            v[k] = max((unsigned)srow[t + k + (int)(ev[k] & 0x7fffu)], (unsigned)srow[t + k + (int)(ev[k] >> 15)]);
+          for (int k = 0; k < 4; ++k) {
+            const unsigned ax = a0 + 2u * k + ((ev[k] << 1) & 0xfffeu), ay = a0 + 2u * k + ((ev[k] >> 14) & ~1u);
+            v[k] = max(lds_u16(ax), lds_u16(ay));
+          }
           if (q == qc) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) v[k] = t + k == c ? 0xffffu : v[k];
           }
-          __stcs(out4 + q, make_uint2(v[0] | (v[1] << 16), v[2] | (v[3] << 16)));
+          __stcs(out4 + q, make_uint2(__byte_perm(v[0], v[1], 0x5410), __byte_perm(v[2], v[3], 0x5410)));
           const unsigned sb = step << 2;
-          kmin = min(kmin, min(min((v[0] << 16) | sb, (v[1] << 16) | sb | 1u), min((v[2] << 16) | sb | 2u, (v[3] << 16) | sb | 3u)));
+          kmin = min(kmin, min(min(v[0] * 65536u + sb, v[1] * 65536u + (sb | 1u)),
+                               min(v[2] * 65536u + (sb | 2u), v[3] * 65536u + (sb | 3u))));
         } else if (4 * q < Mn) {  // the last, partial quad
           const int t = 4 * q;
           const unsigned ev[4] = {ec.x, ec.y, ec.z, ec.w};
