@@ -442,6 +442,13 @@ rb_status build_index_dist(rb_dist *d, const uint32_t *ids_d, const uint8_t *len
   // writes the 16-bit value codes of its rows (into its B buffer, the first
   // round's input) and the rounds run on codes
   const Tuning tu = Tuning::from(p);
+  // host tree stage threads: every rank of the node runs it (replicated),
+  // so one process per GPU shares the cores (15 threads each on 8 ranks would
+  // oversubscribe the host ~8x)
+  if (tu.host_threads > 0)
+    set_host_threads(tu.host_threads);
+  else if (nloc < world)  // one process per rank
+    set_host_threads(std::max(1, (int)(std::thread::hardware_concurrency() / (unsigned)world) - 1));
   const bool codes = N > 1 && tile_path_ok(K, lens_d == nullptr) && tu.value_codes != 0;
   for (int l = 0; l < nloc; ++l) {
     const int r = g0 + l;
