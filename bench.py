@@ -256,9 +256,12 @@ def run_ours(args, ws, rank, local):
             return db.build(ids, stream=stream)
     else:
         wsp = ragb.Workspace(N, K, p, device=dev)
+        # independent builds on every GPU of the node: the host stage's
+        # threads share the cores
+        tu = {"host_threads": max(1, (os.cpu_count() or 2) // ws - 1)} if ws > 1 else None
 
         def build(ids):
-            return ragb.build_index(ids, workspace=wsp, stream=stream)[0]
+            return ragb.build_index(ids, workspace=wsp, stream=stream, tuning=tu)[0]
 
     # the caller's output arrays, reused across builds (page-faulted once)
     ord_out = (np.empty((N, K), dtype=np.uint32), np.empty(N, dtype=np.uint8), np.empty(N, dtype=np.int64))
@@ -306,7 +309,7 @@ def run_ours(args, ws, rank, local):
             ids_d = ids_pin.to(dev, non_blocking=True)
             idx = db.build(ids_d, stream=stream)
         else:
-            idx, _ = ragb.build_index_host(ids_pin.numpy().view(np.uint32), workspace=wsp, stream=stream)
+            idx, _ = ragb.build_index_host(ids_pin.numpy().view(np.uint32), workspace=wsp, stream=stream, tuning=tu)
         out, plen, sched = idx.order_contexts(out=ord_out)
         nn_i, nn_d = idx.nn()
         za = idx.linkage()
