@@ -496,3 +496,21 @@ def test_row_sharded_full_size_C4():
     """C4 with 8 ranks' shards on one device (~130 GB): identical to the
     single-GPU build."""
     _dist_vs_single(config("C4").ids, None, 8)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_inplace_side_buffer_and_cache_random(seed):
+    """Random tie-heavy and clustered inputs with in-place rounds forced
+    wherever allowed: the side buffer (dirty columns, slot retirement,
+    capacity flushes, the patch into the next compaction) and the
+    second-nearest cache give the oracle's merge order, tree and orders, and
+    the same result as the column-rewrite form without the cache."""
+    rng = np.random.default_rng(1000 + seed)
+    N = int(rng.integers(1500, 5000))
+    K = int(rng.integers(3, 12))
+    V = int(rng.integers(K * 20, K * 400))
+    w = generate(N, K, V, 2000 + seed)
+    idx = check_full(w.ids, counts=False, tuning=dict(inplace=1))
+    ref, _ = dev_build(w.ids, flags=0, tuning=dict(inplace=1, side_buffer=0, nn_cache=0))
+    for x, y in zip(idx.linkage() + idx.order_contexts(), ref.linkage() + ref.order_contexts()):
+        assert np.array_equal(x, y)
