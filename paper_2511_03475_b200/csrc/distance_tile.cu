@@ -67,7 +67,7 @@ __global__ void k_pack_table(const float *__restrict__ lut, const uint32_t *__re
   ptab[i] = make_uint2(__float_as_uint(lut[e]), lutc[e] << 16);
 }
 
-template <int R, bool SCALE8, bool TAB_SMEM>
+template <int R, bool SCALE8, bool TAB_SMEM, bool CODES>
 __global__ void __launch_bounds__(NT, 1) k_dist_tile(DistArgs a, Plan P) {
   extern __shared__ __align__(128) unsigned char smem[];
   // the table first: its entries are addressed by the packed accumulator alone
@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(NT, 1) k_dist_tile(DistArgs a, Plan P) {
   uint2 *cinfo = cinfo_all + w * 32;
   const int cg = lane & 7, rr = lane >> 3;  // finalize: column group, first row
   const bool counts = a.s_out != nullptr;
-  const bool codes_out = a.codes != nullptr;
+  constexpr bool codes_out = CODES;  // (a.codes != nullptr, a template parameter: no per-store branch)
   const bool vec_n = (N & 3) == 0;
   const uint32_t lanes_le = 0xffffffffu >> (31 - lane);
   int64_t g = 0;  // position in this CTA's chunk sequence
@@ -441,7 +441,7 @@ bool make_plan(int K, int R, bool tab_smem, size_t limit, Plan *out) {
 
 template <int R, bool S8, bool TS>
 cudaError_t launch(const DistArgs &a, const Plan &P, cudaStream_t st) {
-  auto kern = k_dist_tile<R, S8, TS>;
+  auto kern = a.codes ? k_dist_tile<R, S8, TS, true> : k_dist_tile<R, S8, TS, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.total);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0;
