@@ -540,6 +540,24 @@ __device__ __forceinline__ uint4 above4(int p) {  // bits > p of a 128-bit mask
                          p < 96 ? ~0u : (p < 127 ? ~0u << (p - 95) : 0u)};
   return make_uint4(m[0], m[1], m[2], m[3]);
 }
+// x - 1 over 128 bits (carry chain): x & (x - 1) drops the lowest set bit.
+// In a pick chain the candidate set has no bits below its lowest pick p, so
+// "the candidates above p" is the set minus its lowest bit, and the picked
+// bit itself is x ^ (x & (x - 1)).
+__device__ __forceinline__ uint4 dec128(uint4 x) {
+  uint4 r;
+  asm("sub.cc.u32 %0, %4, 1;\n\tsubc.cc.u32 %1, %5, 0;\n\tsubc.cc.u32 %2, %6, 0;\n\tsubc.u32 %3, %7, 0;"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "r"(x.x), "r"(x.y), "r"(x.z), "r"(x.w));
+  return r;
+}
+// the chain step after picking p = ffs4(c): u loses p, c becomes the
+// candidates above p adjacent to p
+__device__ __forceinline__ void chain_step(uint4 &c, uint4 &u, const uint4 &adjp) {
+  const uint4 cl = and4(c, dec128(c));
+  u = make_uint4(u.x & ~(c.x ^ cl.x), u.y & ~(c.y ^ cl.y), u.z & ~(c.z ^ cl.z), u.w & ~(c.w ^ cl.w));
+  c = and4(cl, adjp);
+}
 __device__ __forceinline__ uint4 clear4(uint4 x, int p) {
   const uint32_t b = ~(1u << (p & 31));
   const int q = p >> 5;
@@ -733,8 +751,7 @@ __device__ int cliques_sweep(const PrepArgs &a, const uint32_t *__restrict__ adj
                 s_bj[nb] = j;
                 s_bv[nb] = p;
                 ++nb;
-                u = clear4(u, p);
-                cm = and4(and4(cm, s_adjB[p]), above4(p));
+                chain_step(cm, u, s_adjB[p]);
               }
             }
             u.x = __shfl_sync(0xffffffffu, u.x, L);
@@ -767,14 +784,13 @@ __device__ int cliques_sweep(const PrepArgs &a, const uint32_t *__restrict__ adj
         s_bj[nb] = J;
         s_bv[nb] = p | 0x10000;  // start of clique J (not a merge)
         ++nb;
-        uint4 cm = and4(and4(u, s_adjB[p]), above4(p));
+        uint4 cm = and4(u, s_adjB[p]);  // (u has no bits at or below p)
         while (any4(cm)) {
           const int q = ffs4(cm);
           s_bj[nb] = J;
           s_bv[nb] = q;
           ++nb;
-          u = clear4(u, q);
-          cm = and4(and4(cm, s_adjB[q]), above4(q));
+          chain_step(cm, u, s_adjB[q]);
         }
         ++J;
       }
