@@ -223,6 +223,20 @@ RB_API rb_status rb_index_size(const rb_index *idx, int64_t *N, int32_t *K);
 /* Build statistics. */
 RB_API rb_status rb_index_stats(const rb_index *idx, rb_stats *st);
 
+/* The distance rows this index was built for: [row0, row0 + nrows) (all N
+ * for a single-GPU build or an index from a merge list). */
+RB_API rb_status rb_index_shard(const rb_index *idx, int64_t *row0, int64_t *nrows);
+
+/* Parity output: s_ij (uint8) and the
+ * positional sum D_ij (uint16) of Eq. 1 for rows [row0, row0 + nrows) of the
+ * indexed contexts, into caller-owned device buffers [nrows][N] — computed
+ * again by the distance kernel from the index's copy of the contexts
+ * (temporary device buffers, the default stream, synchronised on return).
+ * Errors: RB_EINVAL (NULL buffers, bad range), RB_ESTATE (index updated
+ * online), RB_ECUDA, RB_ENOMEM. */
+RB_API rb_status rb_index_counts(const rb_index *idx, int64_t row0, int64_t nrows, uint8_t *s_dev,
+                                 uint16_t *D_dev);
+
 /* Row NN (host, [nrows]): nn_idx = -1 and nn_d = +inf when N == 1. */
 RB_API rb_status rb_index_nn(const rb_index *idx, int32_t *nn_idx, float *nn_d);
 

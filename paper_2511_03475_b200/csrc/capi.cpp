@@ -258,6 +258,8 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
   HostIndex &H = idx->H;
   H.N = N;
   H.K = K;
+  H.row0 = row0;
+  H.nrows = nrows;
   H.alpha_num = p->alpha_num;
   H.alpha_den = p->alpha_den;
   const ragb::Tuning tu = ragb::Tuning::from(p);
@@ -563,6 +565,8 @@ rb_status rb_index_from_linkage(const uint32_t *ids_host, const uint8_t *lens_ho
   HostIndex &H = idx->H;
   H.N = N;
   H.K = K;
+  H.row0 = 0;
+  H.nrows = N;
   H.ids.assign(ids_host, ids_host + (size_t)N * K);
   if (lens_host) H.lens.assign(lens_host, lens_host + N);
   // validate contexts (same rules as the device a1)
@@ -616,6 +620,53 @@ rb_status rb_index_stats(const rb_index *idx, rb_stats *st) {
   if (!idx || !st) return fail(RB_EINVAL, "NULL argument");
   *st = idx->H.stats;
   return RB_OK;
+}
+
+rb_status rb_index_shard(const rb_index *idx, int64_t *row0, int64_t *nrows) {
+  if (!idx || !row0 || !nrows) return fail(RB_EINVAL, "NULL argument");
+  *row0 = idx->H.row0;
+  *nrows = idx->H.nrows;
+  return RB_OK;
+}
+
+rb_status rb_index_counts(const rb_index *idx, int64_t row0, int64_t nrows, uint8_t *s_dev, uint16_t *D_dev) {
+  if (!idx || !s_dev || !D_dev) return fail(RB_EINVAL, "NULL argument");
+  const HostIndex &H = idx->H;
+  if (H.dyn) return fail(RB_ESTATE, "index was updated online (the counts cover the built set only)");
+  if (row0 < 0 || nrows < 0 || row0 + nrows > H.N) return fail(RB_EINVAL, "bad row range");
+  if (nrows == 0) return RB_OK;
+  if (rb_status ps = check_poisoned()) return ps;
+  // a2 again for the requested rows, in counts mode, from the index's own
+  // copy of the contexts: a rows-only build (no linkage) on temporary buffers
+  rb_params p;
+  rb_params_init(&p);
+  p.alpha_num = H.alpha_num;
+  p.alpha_den = H.alpha_den;
+  p.flags = RB_EMIT_COUNTS | RB_SKIP_LINKAGE | RB_ALPHA_ANY;  // (alpha was checked when the index was built)
+  p.row0 = row0;
+  p.nrows = nrows;
+  size_t rows_bytes = 0, scratch_bytes = 0;
+  if (rb_status s = rb_workspace_size(H.N, H.K, &p, &rows_bytes, &scratch_bytes)) return s;
+  void *rows = nullptr, *scratch = nullptr;
+  cudaError_t e = cudaMalloc(&rows, rows_bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&scratch, std::max<size_t>(scratch_bytes, 1));
+  if (e != cudaSuccess) {
+    cudaFree(rows);
+    return cuda_fail(e, "counts buffers");
+  }
+  rb_index *tmp = nullptr;
+  const rb_status s = build_common(nullptr, nullptr, H.N, H.K, &p, static_cast<float *>(rows), scratch,
+                                   scratch_bytes, s_dev, D_dev, H.ids.data(),
+                                   H.lens.empty() ? nullptr : H.lens.data(), &tmp);
+  if (s == RB_OK) {
+    // the build ran on the default stream: the caller's buffers are complete
+    e = cudaStreamSynchronize(nullptr);
+  }
+  rb_index_free(tmp);
+  cudaFree(rows);
+  cudaFree(scratch);
+  if (s != RB_OK) return s;
+  return e == cudaSuccess ? RB_OK : cuda_fail(e, "counts");
 }
 
 rb_status rb_index_nn(const rb_index *idx, int32_t *nn_idx, float *nn_d) {

@@ -190,6 +190,7 @@ struct NoInitAlloc : std::allocator<T> {
 struct HostIndex {
   int64_t N = 0;
   int32_t K = 0;
+  int64_t row0 = 0, nrows = 0;  // distance rows this index was built for (rb_index_shard)
   std::vector<uint32_t, NoInitAlloc<uint32_t>> ids;  // [N][K] (filled by copies: no zero fill)
   std::vector<uint8_t> lens;  // [N]
   bool has_linkage = false;

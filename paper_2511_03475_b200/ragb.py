@@ -30,7 +30,8 @@ STATUS_NAMES = {0: "RB_OK", -1: "RB_EINVAL", -2: "RB_EDUPDOC", -3: "RB_EALPHA", 
 
 EXPORTED = [
     "rb_version", "rb_last_error", "rb_params_init", "rb_workspace_size", "rb_build_index",
-    "rb_build_index_host", "rb_index_from_linkage", "rb_index_size", "rb_index_stats", "rb_index_nn",
+    "rb_build_index_host", "rb_index_from_linkage", "rb_index_size", "rb_index_stats", "rb_index_shard",
+    "rb_index_counts", "rb_index_nn",
     "rb_index_linkage", "rb_index_tree_info", "rb_index_tree", "rb_order_contexts", "rb_session_open",
     "rb_session_open_docs", "rb_dedup_turn", "rb_session_turn", "rb_session_free", "rb_index_free",
     "rb_index_set_alpha", "rb_index_set_online", "rb_session_context", "rb_dedup_batch",
@@ -99,6 +100,8 @@ def lib():
         "rb_index_from_linkage": ([P, P, i64, i32, P, P, P, P, PP], i32),
         "rb_index_size": ([P, ctypes.POINTER(i64), ctypes.POINTER(i32)], i32),
         "rb_index_stats": ([P, ctypes.POINTER(Stats)], i32),
+        "rb_index_shard": ([P, ctypes.POINTER(i64), ctypes.POINTER(i64)], i32),
+        "rb_index_counts": ([P, i64, i64, P, P], i32),
         "rb_index_nn": ([P, P, P], i32),
         "rb_index_linkage": ([P, P, P, P, P], i32),
         "rb_index_tree_info": ([P, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64)], i32),
@@ -202,6 +205,22 @@ class Index:
         s = Stats()
         _check(lib().rb_index_stats(self._h, ctypes.byref(s)))
         return s.as_dict()
+
+    def shard(self):
+        """(row0, nrows): the distance rows this index was built for."""
+        r0, nr = ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().rb_index_shard(self._h, ctypes.byref(r0), ctypes.byref(nr)))
+        return r0.value, nr.value
+
+    def counts(self, row0=0, nrows=None, device="cuda"):
+        """Parity output: (s uint8, D int16 viewed as uint16) [nrows][N] device
+        tensors of Eq. 1's overlap and positional sum for rows row0.."""
+        import torch
+        n = self.N - row0 if nrows is None else nrows
+        s = torch.empty((n, self.N), dtype=torch.uint8, device=device)
+        D = torch.empty((n, self.N), dtype=torch.int16, device=device)
+        _check(lib().rb_index_counts(self._h, row0, n, ctypes.c_void_p(s.data_ptr()), ctypes.c_void_p(D.data_ptr())))
+        return s, D
 
     def nn(self, nrows=None):
         n = self.N if nrows is None else nrows

@@ -197,3 +197,13 @@ def test_order_contexts_into_caller_arrays():
         assert all(np.array_equal(g, r) for g, r in zip(got, ref))
     with pytest.raises(ValueError):
         idx.order_contexts(out=(bufs[0], bufs[1], np.zeros(300, dtype=np.int32)))
+
+
+def test_index_shard_of_host_index():
+    """rb_index_shard: an index from a merge list covers all N rows."""
+    w = generate(40, 5, 120, 5)
+    idx = ragb.index_from_linkage(w.ids, *oc.linkage(oc.pairwise_rows(w.ids, None, 1, 200)))
+    assert idx.shard() == (0, 40)
+    with pytest.raises(ragb.RagbError):
+        lib_counts_bad = ragb.lib().rb_index_counts(idx._h, 0, 41, None, None)  # NULL buffers
+        ragb._check(lib_counts_bad)

@@ -514,3 +514,21 @@ def test_inplace_side_buffer_and_cache_random(seed):
     ref, _ = dev_build(w.ids, flags=0, tuning=dict(inplace=1, side_buffer=0, nn_cache=0))
     for x, y in zip(idx.linkage() + idx.order_contexts(), ref.linkage() + ref.order_contexts()):
         assert np.array_equal(x, y)
+
+
+def test_index_counts_and_shard():
+    """rb_index_counts recomputes (s, D) rows of the indexed set equal to the
+    RB_EMIT_COUNTS output of the build (and to the oracle's); rb_index_shard
+    reports the built row range."""
+    w = config("C2")
+    N = w.ids.shape[0]
+    idx, ws = dev_build(w.ids, flags=F.RB_KEEP_ROWS | F.RB_EMIT_COUNTS)
+    assert idx.shard() == (0, N)
+    s, D = idx.counts(0, N)
+    assert torch.equal(s, ws.s) and torch.equal(D, ws.D)
+    s2, D2 = idx.counts(1000, 77)
+    _, sref, Dref = oc.pairwise_rows(w.ids, None, 1, 200, counts=True, row0=1000, nrows=77)
+    assert np.array_equal(s2.cpu().numpy(), sref) and np.array_equal(D2.cpu().numpy().view(np.uint16), Dref)
+    t = torch.from_numpy(w.ids.view(np.int32)).cuda()
+    part, _ = F.build_index(t, row0=512, nrows=256)
+    assert part.shard() == (512, 256)
