@@ -1594,7 +1594,7 @@ __global__ void __launch_bounds__(NTH) k_merge_gather2(const uint16_t *__restric
     const unsigned char *src = reinterpret_cast<const unsigned char *>(D + (int64_t)gmem[goff[row]] * ld) + (size_t)v0 * 16;
     unsigned char *dst = reinterpret_cast<unsigned char *>(smem4 + (size_t)slot * MV + v0);
     const unsigned bytes = (unsigned)(v1 - v0) * 16u;
-    for (unsigned o = 0; o < bytes; o += 32768u) bulk_g2s(dst + o, src + o, min(32768u, bytes - o), &bar[slot]);
+    for (unsigned o = 0; o < bytes; o += 32768u) bulk_g2s_stream(dst + o, src + o, min(32768u, bytes - o), &bar[slot]);
   };
   if (VEC && tid == 0) {
     for (int k = 0; k <= db; ++k)
