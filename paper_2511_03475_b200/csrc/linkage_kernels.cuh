@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(256) k_level_adj_rows(PrepArgs a, uint32_t *__
       const uint4 *row4 = reinterpret_cast<const uint4 *>(row);
       for (int q = threadIdx.x; q * VW < M; q += blockDim.x) {
         unsigned v[VW];
-        E::unpack(__ldg(row4 + q), v);
+        E::unpack(__ldcs(row4 + q), v);  // (rows read once: evict-first, the adjacency stays in L2)
         const int c0 = q * VW;  // VW columns in one mask word
         const uint32_t mw = lmask[c0 >> 5];
         const uint32_t below = mw & ((1u << (c0 & 31)) - 1u);
