@@ -780,7 +780,15 @@ rb_status rb_order_contexts(rb_index *idx, const uint32_t *ids, const uint8_t *l
     return RB_OK;
   }
   if (M != H.N) return fail(RB_EINVAL, "M must match the indexed contexts");
-  if (out_ids) std::memcpy(out_ids, H.ordered.data(), H.ordered.size() * 4);
+  if (out_ids) {  // N x K words: copied by the host-stage threads in 1 MB pieces
+    const size_t n = H.ordered.size(), piece = 1 << 18;
+    const int64_t np = (int64_t)((n + piece - 1) / piece);
+#pragma omp parallel for num_threads(ragb::host_threads()) schedule(static)
+    for (int64_t q = 0; q < np; ++q) {
+      const size_t b = (size_t)q * piece;
+      std::memcpy(out_ids + b, H.ordered.data() + b, std::min(piece, n - b) * 4);
+    }
+  }
   if (out_prefix_len) std::memcpy(out_prefix_len, H.prefix_len.data(), H.prefix_len.size());
   if (out_schedule) std::memcpy(out_schedule, H.schedule.data(), H.schedule.size() * 8);
   return RB_OK;
