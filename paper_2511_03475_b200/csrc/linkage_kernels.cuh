@@ -215,30 +215,6 @@ __global__ void __launch_bounds__(PT, 1) k_prep_list(PrepArgs a) {
   if (threadIdx.x == 0) a.level[0] = nlist;
 }
 
-// Round step 2 (grid): adjacency bits of the level graph, adj[i][w] bit j <=>
-// D[list[i]][list[32w + j]] == h (j != i).  One warp per word: 32 lanes read
-// 32 ascending columns of the same row.
-template <typename T>
-__global__ void k_level_adj(PrepArgs a, uint32_t *__restrict__ adj) {
-  const int n = a.level[0];
-  if (n < 2) return;
-  const unsigned hb = (unsigned)a.level[1];
-  const T *D = static_cast<const T *>(a.D);
-  const int W = (n + 31) >> 5;
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t total = (int64_t)n * W;
-  for (int64_t q = gw; q < total; q += nw) {
-    const int i = (int)(q / W), w = (int)(q - (int64_t)i * W);
-    const int j = w * 32 + lane;
-    bool bit = false;
-    if (j < n && j != i) bit = Elem<T>::bits(__ldg(D + (int64_t)a.list[i] * a.ld + a.list[j])) == hb;
-    const unsigned word = __ballot_sync(0xffffffffu, bit);
-    if (lane == 0) adj[q] = word;
-  }
-}
-
 // Side buffer of the in-place rounds (code mode).  Rewriting the merged
 // survivors' columns in place costs one scattered 2-byte store per row and
 // merge (most of an in-place round).  Instead a survivor's column becomes
@@ -772,8 +748,8 @@ __device__ int cliques_sweep(const PrepArgs &a, const uint32_t *__restrict__ adj
       __syncthreads();
       { const long long c1 = clock64(); tk[2] += c1 - c0; c0 = c1; }
     }
-    // -- new cliques among the vertices still undecided --------------------------
-    const int nb_join = s_nb;  // decisions [0, nb_join) join existing cliques
+    // -- new cliques among the vertices still undecided (decisions before s_nb
+    //    join existing cliques) ----------------------------------------------------
     if (tid == 0) {
       uint4 u = s_und;
       int nb = s_nb, J = s_J;
@@ -802,7 +778,6 @@ __device__ int cliques_sweep(const PrepArgs &a, const uint32_t *__restrict__ adj
     const int nb = s_nb;
     // -- record the merges; eager candidate sets for the words after the block ----
     const int wn = wb + 4;  // first word after the block
-    const int nw = W - wn;
     {  // decision t of the block -> global arrays, rank within its clique (a
        // clique's decisions of the block are contiguous: one chain each)
       const int nd0 = s_nd;
