@@ -105,6 +105,12 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned pari
       "r"(parity)
       : "memory");
 }
+// Programmatic dependent launch: a kernel launched with the programmatic
+// stream-serialization attribute (launch_pdl) may be scheduled before its
+// predecessor in the stream has finished; it waits here, first thing, for the
+// predecessor's completion and memory flush (a no-op for a normal launch).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // 16-bit shared-memory load into a 32-bit register (zero-extended), by
 // shared-window byte address
 __device__ __forceinline__ unsigned lds_u16(unsigned addr) {

@@ -190,16 +190,16 @@ cudaError_t launch_inplace(T *cur, int64_t ld, int M, int max_groups, const Prep
                            int *mlist, int *nmulti, int *sz, unsigned long long *key, const SideBuf &sb,
                            const NNCache &nc, cudaStream_t st, int *launches) {
   constexpr int VW = Elem<T>::VW;
-  k_inplace_prep<<<sms * 2, 256, 0, st>>>(pa, M, amask, mlist, nmulti, sz, key, sb, nc);
+  launch_pdl(k_inplace_prep, sms * 2, 256, 0, st, pa, M, amask, mlist, nmulti, sz, key, sb, nc);
   const size_t smem = (size_t)((M + VW - 1) / VW) * 16;
   if constexpr (sizeof(T) == 2) {
     if (sb.T) {
       const size_t smem2 = smem + (size_t)sb.cap * 2;
       occupancy_cached(k_inplace_rows_sb<512>, 512, smem2);
-      k_inplace_rows_sb<512><<<sms * 2, 512, smem2, st>>>(pa, cur, ld, M, amask, mlist, nmulti, key, sb);
-      k_side_tpose<<<dim3((unsigned)((M + 63) / 64), (unsigned)((std::max(max_groups, 1) + 31) / 32)), 256, 0, st>>>(
-          pa, cur, ld, M, mlist, nmulti, sb);
-      k_side_maps<<<1, 1024, 0, st>>>(pa, mlist, nmulti, sb);
+      launch_pdl(k_inplace_rows_sb<512>, sms * 2, 512, smem2, st, pa, cur, ld, M, amask, mlist, nmulti, key, sb);
+      launch_pdl(k_side_tpose, dim3((unsigned)((M + 63) / 64), (unsigned)((std::max(max_groups, 1) + 31) / 32)), 256, 0,
+                 st, pa, static_cast<const uint16_t *>(cur), ld, M, mlist, nmulti, sb);
+      launch_pdl(k_side_maps, 1, 1024, 0, st, pa, mlist, nmulti, sb);
       *launches += 3;
     }
   }
@@ -210,11 +210,12 @@ cudaError_t launch_inplace(T *cur, int64_t ld, int M, int max_groups, const Prep
                         0, st>>>(pa, cur, ld, M, amask, mlist, nmulti);
     *launches += 2;
   }
-  k_inplace_check<T><<<(M + 255) / 256, 256, 0, st>>>(pa, cur, ld, M, key, pa.cnt, nmulti + 1, sb, nc);  // cnt: free after the compaction map
+  launch_pdl(k_inplace_check<T>, (M + 255) / 256, 256, 0, st, pa, cur, ld, M, key, pa.cnt, nmulti + 1, sb,
+             nc);  // cnt: free after the compaction map
   {
     const size_t rs = (size_t)(((M / 32 + 1) + 3) & ~3) * 4 + (size_t)(sb.T ? sb.cap : 0) * 4;  // scan mask + slot columns
     occupancy_cached(k_inplace_rescan<256, T>, 256, rs);
-    k_inplace_rescan<256, T><<<sms * 4, 256, rs, st>>>(cur, ld, M, amask, pa.cnt, nmulti + 1, key, sb, nc);
+    launch_pdl(k_inplace_rescan<256, T>, sms * 4, 256, rs, st, cur, ld, M, amask, pa.cnt, nmulti + 1, key, sb, nc);
   }
   *launches += 3;
   return cudaGetLastError();
@@ -387,7 +388,7 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
         const SideBuf b = sb_used > 0 ? side_for(M, next) : SideBuf{};
         auto kern = vec ? k_level_adj_rows<uint16_t, true> : k_level_adj_rows<uint16_t, false>;
         if (smem > 48 * 1024) occupancy_cached(kern, 256, smem);
-        kern<<<grid, 256, smem, st>>>(pa, adj, b);
+        launch_pdl(kern, grid, 256, smem, st, pa, adj, b);
       } else {
         auto kern = vec ? k_level_adj_rows<float, true> : k_level_adj_rows<float, false>;
         if (smem > 48 * 1024) occupancy_cached(kern, 256, smem);
@@ -401,7 +402,7 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
         occupancy_cached(k_level_cliques, CT, smem);
       // CTA 0 decides; with a level above 4096 vertices the other CTAs
       // (one per SM, all resident) update the clique candidate sets
-      k_level_cliques<<<std::min(sms, 1 + kSweepHelpers), CT, smem, st>>>(pa, adj);
+      launch_pdl(k_level_cliques, std::min(sms, 1 + kSweepHelpers), CT, smem, st, pa, adj);
     }
     launch_prep_compact(pa, sms, st, launches);
     *launches += 2;

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <utility>
 
 #include "device_util.cuh"
 #include "internal.h"
@@ -167,6 +168,7 @@ __device__ int block_compact(int n, Pred pred, Val value, int *out, BlockScratch
 // become the level list (one CTA, ascending).  Only the scans run in one CTA;
 // the per-row work with dependent loads and atomics is spread over the grid.
 __global__ void k_prep_min(PrepArgs a) {
+  pdl_wait();
   unsigned hl = 0xffffffffu;
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < a.M; x += gridDim.x * blockDim.x)
     hl = min(hl, (unsigned)(a.key[x] >> 32));
@@ -176,6 +178,7 @@ __global__ void k_prep_min(PrepArgs a) {
 }
 
 __global__ void k_prep_rnn(PrepArgs a) {
+  pdl_wait();
   const unsigned h = (unsigned)a.level[1];
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < a.M; x += gridDim.x * blockDim.x) {
     const u64 kx = a.key[x];
@@ -200,6 +203,7 @@ __global__ void k_prep_rnn(PrepArgs a) {
 }
 
 __global__ void __launch_bounds__(PT, 1) k_prep_list(PrepArgs a) {
+  pdl_wait();
   __shared__ BlockScratch S;
   const uint8_t *alive = a.alive;
   int *lpos = a.lpos;
@@ -260,6 +264,7 @@ struct NNCache {
 // level (rows merged away by in-place rounds hold stale values) are skipped.
 template <typename T, bool VEC>
 __global__ void __launch_bounds__(256) k_level_adj_rows(PrepArgs a, uint32_t *__restrict__ adj, SideBuf sb) {
+  pdl_wait();
   // [W] this row's adjacency bits, then the level's column mask [MW] and its
   // per-word exclusive popcount prefix [MW]: a column's level position is
   // lpre[c / 32] + popc(lmask[c / 32] below c) — no global lookups per match
@@ -909,6 +914,7 @@ __device__ int cliques_sweep(const PrepArgs &a, const uint32_t *__restrict__ adj
 
 __global__ void __launch_bounds__(CT, 1) k_level_cliques(PrepArgs a,
                                                          const uint32_t *__restrict__ adj) {
+  pdl_wait();
   extern __shared__ __align__(16) uint32_t bits[];  // staged adjacency of levels <= 1024
   __shared__ int s_p[64];     // next candidates (list positions), ascending (warp paths)
   __shared__ int s_nseq;
@@ -996,6 +1002,7 @@ __global__ void __launch_bounds__(CT, 1) k_level_cliques(PrepArgs a,
 // Round step 4: order-preserving compaction map and group CSR.  Scans in one
 // CTA (newidx, goff), the per-row passes over the grid.
 __global__ void __launch_bounds__(PT, 1) k_compact_scan1(PrepArgs a) {
+  pdl_wait();
   __shared__ BlockScratch S;
   const int M = a.M;
   // new index of every survivor (order preserving)
@@ -1013,6 +1020,7 @@ __global__ void __launch_bounds__(PT, 1) k_compact_scan1(PrepArgs a) {
 }
 
 __global__ void k_compact_groups(PrepArgs a) {
+  pdl_wait();
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < a.M; x += gridDim.x * blockDim.x) {
     const int l = a.leader[x];
     if (l < 0) continue;  // dead row
@@ -1024,6 +1032,7 @@ __global__ void k_compact_groups(PrepArgs a) {
 }
 
 __global__ void __launch_bounds__(PT, 1) k_compact_scan2(PrepArgs a) {
+  pdl_wait();
   __shared__ BlockScratch S;
   const int Mn = *a.Mn;
   const int live = block_scan_all(
@@ -1032,6 +1041,7 @@ __global__ void __launch_bounds__(PT, 1) k_compact_scan2(PrepArgs a) {
 }
 
 __global__ void k_compact_members(PrepArgs a) {
+  pdl_wait();
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < a.M; x += gridDim.x * blockDim.x) {
     const int l = a.leader[x];
     if (l < 0) continue;
@@ -1062,6 +1072,7 @@ __device__ __forceinline__ int *clq_of(const PrepArgs &a, int Mn) {
 // 2 a non-leader of a larger group; new column -> its leader (first_old,
 // in cursor, free after the member scatter); pmap (or pm32) for the gather
 __global__ void k_compact_maps(PrepArgs a) {
+  pdl_wait();
   const int M = a.M, Mn = *a.Mn;
   const bool compact = a.pmap && a.nclq && pm32_fits(M, Mn);
   const int i0 = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1102,20 +1113,42 @@ __global__ void k_compact_maps(PrepArgs a) {
   }
 }
 
+// Launch with programmatic stream serialization (PDL): the kernel may be
+// scheduled while its predecessor drains and waits in pdl_wait() — the
+// per-launch gap of the round's ~15 small kernels shrinks.
+template <typename... KP, typename... A>
+inline void launch_pdl(void (*k)(KP...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A &&...args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+#ifdef RAGB_NO_PDL
+  cfg.numAttrs = 0;  // (A/B builds: plain stream-ordered launches)
+#else
+  cfg.numAttrs = 1;
+#endif
+  cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...);
+}
+
 // Launch sequences of the round preparation (single GPU and sharded build).
 inline void launch_prep_mark(const PrepArgs &pa, int sms, cudaStream_t st, int *launches) {
   cudaMemsetAsync(pa.level + 1, 0xff, 4, st);
-  k_prep_min<<<sms, 256, 0, st>>>(pa);
-  k_prep_rnn<<<sms * 2, 256, 0, st>>>(pa);
-  k_prep_list<<<1, PT, 0, st>>>(pa);
+  launch_pdl(k_prep_min, sms, 256, 0, st, pa);
+  launch_pdl(k_prep_rnn, sms * 2, 256, 0, st, pa);
+  launch_pdl(k_prep_list, 1, PT, 0, st, pa);
   *launches += 3;
 }
 inline void launch_prep_compact(const PrepArgs &pa, int sms, cudaStream_t st, int *launches) {
-  k_compact_scan1<<<1, PT, 0, st>>>(pa);
-  k_compact_groups<<<sms * 2, 256, 0, st>>>(pa);
-  k_compact_scan2<<<1, PT, 0, st>>>(pa);
-  k_compact_members<<<sms * 2, 256, 0, st>>>(pa);
-  k_compact_maps<<<sms * 2, 256, 0, st>>>(pa);
+  launch_pdl(k_compact_scan1, 1, PT, 0, st, pa);
+  launch_pdl(k_compact_groups, sms * 2, 256, 0, st, pa);
+  launch_pdl(k_compact_scan2, 1, PT, 0, st, pa);
+  launch_pdl(k_compact_members, sms * 2, 256, 0, st, pa);
+  launch_pdl(k_compact_maps, sms * 2, 256, 0, st, pa);
   *launches += 5;
 }
 
@@ -1786,6 +1819,7 @@ __global__ void __launch_bounds__(NTH) k_merge_gather2(const uint16_t *__restric
 __global__ void k_inplace_prep(PrepArgs a, int M, uint32_t *__restrict__ amask, int *__restrict__ mlist,
                                int *__restrict__ nmulti, int *__restrict__ sz, u64 *__restrict__ key, SideBuf sb,
                                NNCache nc) {
+  pdl_wait();
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < M; x += gridDim.x * blockDim.x) {
     const int l = a.leader[x];
     uint8_t chg = 0;
@@ -1892,6 +1926,7 @@ __global__ void __launch_bounds__(NTH, 2) k_inplace_rows_sb(PrepArgs a, uint16_t
                                                          const int *__restrict__ mlist,
                                                          const int *__restrict__ nmulti_p, u64 *__restrict__ key,
                                                          SideBuf sb) {
+  pdl_wait();
   typedef Elem<uint16_t> E;
   constexpr int VW = 8;
   extern __shared__ __align__(16) uint4 rowv[];  // [MV] row, then [cap / 8] T row
@@ -1982,6 +2017,7 @@ __global__ void __launch_bounds__(NTH, 2) k_inplace_rows_sb(PrepArgs a, uint16_t
 __global__ void __launch_bounds__(256) k_side_tpose(PrepArgs a, const uint16_t *__restrict__ D, int64_t ld, int M,
                                                     const int *__restrict__ mlist, const int *__restrict__ nmulti_p,
                                                     SideBuf sb) {
+  pdl_wait();
   __shared__ uint16_t tile[32][64 + 2];
   const int m = *nmulti_p, nt = *sb.nt;
   const int k0 = blockIdx.y * 32;
@@ -2011,6 +2047,7 @@ __global__ void __launch_bounds__(256) k_side_tpose(PrepArgs a, const uint16_t *
 // retires its old slot), dirty bits, then the new slot count.
 __global__ void __launch_bounds__(1024) k_side_maps(PrepArgs a, const int *__restrict__ mlist,
                                                     const int *__restrict__ nmulti_p, SideBuf sb) {
+  pdl_wait();
   const int m = *nmulti_p, nt = *sb.nt;
   for (int k = threadIdx.x; k < m; k += blockDim.x) {
     const int L = a.cursor[mlist[k]];
@@ -2093,6 +2130,7 @@ template <typename T>
 __global__ void k_inplace_check(PrepArgs a, const T *__restrict__ D, int64_t ld, int M,
                                 u64 *__restrict__ key, int *__restrict__ rlist, int *__restrict__ nres, SideBuf sb,
                                 NNCache nc) {
+  pdl_wait();
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < M; r += gridDim.x * blockDim.x) {
     const u64 kr = key[r];
     if (kr == kDead || a.alive[r]) continue;  // dead, or a survivor (done in S1)
@@ -2132,6 +2170,7 @@ __global__ void __launch_bounds__(NTH) k_inplace_rescan(const T *__restrict__ D,
                                                         const int *__restrict__ rlist,
                                                         const int *__restrict__ nres_p, u64 *__restrict__ key,
                                                         SideBuf sb, NNCache nc) {
+  pdl_wait();
   typedef Elem<T> E;
   constexpr int VW = E::VW;
   __shared__ u64 wmin[NTH / 32][2];
