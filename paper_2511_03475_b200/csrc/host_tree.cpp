@@ -83,7 +83,9 @@ void host_begin(HostIndex &H, TreeBuild &T) {
   // OpenMP team would keep spinning on the cores that thread needs
   T.lset.resize((size_t)N * K);
   {
-    const int nt = std::max(1, std::min<int>(nth, (int)(N / 4096) + 1));
+    // (two cores fewer than the tail stages: the round-launching thread and
+    // this replay worker must not be preempted while the device rounds run)
+    const int nt = std::max(1, std::min<int>(nth - 2, (int)(N / 4096) + 1));
     std::vector<std::thread> pool;
     for (int w = 0; w < nt; ++w)
       pool.emplace_back([&, w] {

@@ -142,9 +142,9 @@ cudaError_t launch_merge(const T *cur, int64_t ld, int M, int Mn, const PrepArgs
       if (per_sm < 1) return cudaErrorInvalidConfiguration;
       *paths |= wide16 ? RB_PATH_GATHER_WIDE : RB_PATH_GATHER;
       const int grid = std::min<int>(Mn, sms * per_sm);
-      kern<<<grid, nth, smem, st>>>(reinterpret_cast<const uint16_t *>(cur), ld, M, pa.Mn, pa.goff, pa.gmem,
-                                    reinterpret_cast<const uint32_t *>(pa.pmap), pa.nclq,
-                                    reinterpret_cast<uint16_t *>(next), keyn, db, patch);
+      launch_pdl(kern, grid, nth, smem, st, reinterpret_cast<const uint16_t *>(cur), ld, M, (const int *)pa.Mn,
+                 (const int *)pa.goff, (const int *)pa.gmem, reinterpret_cast<const uint32_t *>(pa.pmap),
+                 (const int *)pa.nclq, reinterpret_cast<uint16_t *>(next), keyn, db, patch);
       return cudaGetLastError();
     }
   }
@@ -256,7 +256,7 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
   void *matB = codes ? static_cast<void *>(cm->codes) : (keep_rows ? at<void>(scratch, L.matB) : static_cast<void *>(rows));
   int *counters = at<int>(scratch, L.counters);  // [0] zcount, [1] Mn
   cudaError_t e;
-  k_init_state<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(rep[0], sz[0], N);
+  launch_pdl(k_init_state, (unsigned)((N + 255) / 256), 256, 0, st, rep[0], sz[0], N);
   ++*launches;
   if ((e = cudaMemsetAsync(counters, 0, 16 * sizeof(int), st)) != cudaSuccess) return e;
 
@@ -286,7 +286,7 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
   pa.vals = codes ? cm->vals : nullptr;
   pa.pmap = codes ? at<int2>(scratch, L.pmap) : nullptr;
   if (codes) {
-    k_keys_to_codes<<<sms, 256, 0, st>>>(nnkey, N, cm->vals, cm->ncode);
+    launch_pdl(k_keys_to_codes, sms, 256, 0, st, nnkey, N, cm->vals, cm->ncode);
     ++*launches;
   }
 

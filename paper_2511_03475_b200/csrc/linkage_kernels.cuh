@@ -1573,6 +1573,7 @@ __global__ void __launch_bounds__(NTH) k_merge_gather2(const uint16_t *__restric
                                                        const int *__restrict__ gmem, const uint32_t *__restrict__ pm,
                                                        const int *__restrict__ nclq_p, uint16_t *__restrict__ Dn,
                                                        u64 *__restrict__ keyn, int db, SideBuf sb) {
+  pdl_wait();
   constexpr int NWARP = NTH / 32;
   constexpr int kMaxChunks = 32;  // chunks per row (progressive refill needs Mn / (4 * CQ) <= kMaxChunks)
   extern __shared__ __align__(16) uint4 smem4[];  // [1 + db][ceil(M / 8)]
@@ -2261,6 +2262,7 @@ __global__ void __launch_bounds__(NTH) k_inplace_rescan(const T *__restrict__ D,
 // the code of a value is its position in the ascending table vals[0, ncode).
 __global__ void k_keys_to_codes(u64 *__restrict__ key, int64_t N, const float *__restrict__ vals,
                                 const int *__restrict__ ncode_p) {
+  pdl_wait();
   const int ncode = *ncode_p;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
     const u64 k = key[i];
@@ -2279,6 +2281,7 @@ __global__ void k_keys_to_codes(u64 *__restrict__ key, int64_t N, const float *_
 }
 
 __global__ void k_init_state(int *rep, int *sz, int64_t N) {
+  pdl_wait();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < N) {
     rep[i] = (int)i;
