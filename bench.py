@@ -258,7 +258,11 @@ def run_ours(args, ws, rank, local):
         wsp = ragb.Workspace(N, K, p, device=dev)
         # independent builds on every GPU of the node: the host stage's
         # threads share the cores
-        tu = {"host_threads": max(1, (os.cpu_count() or 2) // ws - 1)} if ws > 1 else None
+        tu = {"host_threads": max(1, (os.cpu_count() or 2) // ws - 1)} if ws > 1 else {}
+        if os.environ.get("RAGB_BENCH_HOST_THREADS"):
+            tu["host_threads"] = int(os.environ["RAGB_BENCH_HOST_THREADS"])
+        if os.environ.get("RAGB_BENCH_TRACE"):  # diagnostics: per-round events + worker laps on stderr
+            tu["trace"] = 2
 
         def build(ids):
             return ragb.build_index(ids, workspace=wsp, stream=stream, tuning=tu)[0]

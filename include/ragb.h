@@ -106,7 +106,7 @@ typedef struct rb_params {
   int32_t long_lists;     /* -1 auto; 0 the general distance kernel for 32<K<=128  */
   int32_t dist_grid;      /* 0 auto; > 0 caps the distance kernel's grid           */
   int32_t host_threads;   /* 0 auto (all cores); > 0 host tree-stage threads       */
-  int32_t trace;          /* 1: per-round linkage / host-stage trace on stderr     */
+  int32_t trace;          /* 1: per-round linkage (synced) + host-stage trace on stderr; 2: per-round events only */
   int32_t side_buffer;    /* -1 auto: in-place rounds on 16-bit codes append merged
                              columns to a transposed side buffer; 0: rewrite the
                              columns in the matrix                                  */

@@ -118,7 +118,7 @@ Tuning Tuning::from(const rb_params *p) {
   t.long_lists = p->long_lists;
   t.dist_grid = p->dist_grid;
   t.host_threads = p->host_threads;
-  t.trace = p->trace != 0;
+  t.trace = p->trace;
   t.side_buffer = p->side_buffer;
   t.nn_cache = p->nn_cache;
   return t;
@@ -263,7 +263,7 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
   H.alpha_num = p->alpha_num;
   H.alpha_den = p->alpha_den;
   const ragb::Tuning tu = ragb::Tuning::from(p);
-  H.trace = tu.trace;
+  H.trace = tu.trace != 0;
 #ifdef RAGB_HOST_TRACE
   H.trace = true;  // host-stage laps on stderr (variant build for host profiling)
 #endif
@@ -397,6 +397,7 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
   ragb::LinkageOut lo;
   ragb::TreeBuild T;
   const bool intersection = linkage && p->linkage == RB_LINK_INTERSECTION;
+  auto th_join = clock::now();  // start of the host stage (a6-a7)
   if (intersection) {  // NEXT-3: sequential greedy merges in one cooperative kernel
     H.za.assign(N - 1, 0);
     H.zb.assign(N - 1, 0);
@@ -427,9 +428,16 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
     cudaError_t copy_err = cudaSuccess;
     int cur_dev = 0;
     cudaGetDevice(&cur_dev);
+    std::vector<std::pair<char, float>> wlog;  // trace 2: worker laps (b begin, c copy, r replay)
+    const auto tw0 = clock::now();
+    auto wlap = [&](char c) {
+      if (tu.trace == 2) wlog.emplace_back(c, std::chrono::duration<float, std::milli>(clock::now() - tw0).count());
+    };
     std::thread worker([&] {
       cudaSetDevice(cur_dev);  // a new thread starts on device 0
+      wlap('s');
       ragb::host_begin(H, T);  // sorted leaf sets overlap the device work
+      wlap('b');
       // the round's merges come from the device on this thread's own
       // non-blocking stream: the launching thread never waits for them
       cudaStream_t cs = nullptr;
@@ -464,9 +472,11 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
             break;
           }
           have = upto;
+          wlap('c');
         }
         for (int64_t e : my_ends) ragb::host_replay(H, T, e);  // round by round
         ragb::host_replay(H, T, upto);
+        wlap('r');
         if (!T.ok || (fin && T.done >= upto)) break;
       }
       if (cs) cudaStreamDestroy(cs);
@@ -482,17 +492,38 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
           cv.notify_one();
         },
         tu);
+    // the device stage ends here; waiting for the replay worker counts as host time
+    cudaEventRecord(ev[3], st);  // (an error surfaces at the sync below: the worker must be joined first)
+    th_join = clock::now();
+    cudaEvent_t lev = nullptr;
+    const auto tj = clock::now();
+    if (tu.trace == 2) {
+      cudaEventCreate(&lev);
+      cudaEventRecord(lev, st);
+    }
     {
       std::lock_guard<std::mutex> lk(mu);
       finished = true;
     }
     cv.notify_one();
     worker.join();
+    if (lev) {
+      float a = 0;
+      cudaEventSynchronize(lev);
+      cudaEventElapsedTime(&a, ev[2], lev);
+      std::fprintf(stderr, "[ragb lt] device linkage=%.3f join=%.3f at %.3f |", a,
+                   std::chrono::duration<float, std::milli>(clock::now() - tj).count(),
+                   std::chrono::duration<float, std::milli>(tj - tw0).count());
+      for (auto &w : wlog) std::fprintf(stderr, " %c%.2f", w.first, w.second);
+      std::fprintf(stderr, "\n");
+      cudaEventDestroy(lev);
+    }
     if (le != cudaSuccess) return cleanup(cuda_fail(le, "linkage"));
     if (copy_err != cudaSuccess) return cleanup(cuda_fail(copy_err, "D2H merges"));
   }
-  RB_CUDA(cudaEventRecord(ev[3], st), "event");
+  if (!linkage || intersection) RB_CUDA(cudaEventRecord(ev[3], st), "event");
   RB_CUDA(cudaStreamSynchronize(st), "sync");
+  if (!linkage || intersection) th_join = clock::now();
   for (int64_t r = 0; r < nrows; ++r) {
     const unsigned long long k = keys[r];
     if (k == ~0ull) {
@@ -524,12 +555,17 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
 
   // ---- a6-a7: tree, orders, schedule (host) --------------------------------
   if (linkage) {
-    const auto th = clock::now();
+    const auto th = th_join;
+    const auto tf = clock::now();
     std::string msg;
     s = ragb::host_finish(H, T, &msg);
     if (s != RB_OK) return cleanup(fail(s, "internal: " + msg));
     H.has_linkage = true;
     H.stats.host_ms = std::chrono::duration<float, std::milli>(clock::now() - th).count();
+    if (tu.trace == 2)
+      std::fprintf(stderr, "[ragb lt] host stage: to finish %.3f, finish %.3f ms\n",
+                   std::chrono::duration<float, std::milli>(tf - th).count(),
+                   std::chrono::duration<float, std::milli>(clock::now() - tf).count());
   }
   H.stats.total_ms = std::chrono::duration<float, std::milli>(clock::now() - t_start).count();
   *out = idx;

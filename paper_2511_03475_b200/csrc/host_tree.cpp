@@ -82,6 +82,10 @@ void host_begin(HostIndex &H, TreeBuild &T) {
   // runs while the device rounds are launched from another thread, and an
   // OpenMP team would keep spinning on the cores that thread needs
   T.lset.resize((size_t)N * K);
+  // the ordered contexts (a7, written by host_finish's branch A) are sized
+  // and page-faulted here too, off the critical path: first touches of 8 MB
+  // at C4 cost ~2 ms inside the tail stage otherwise
+  H.ordered.resize((size_t)N * K);
   {
     // (two cores fewer than the tail stages: the round-launching thread and
     // this replay worker must not be preempted while the device rounds run)
@@ -103,6 +107,9 @@ void host_begin(HostIndex &H, TreeBuild &T) {
             d[q] = x;
           }
         }
+        uint32_t *o = H.ordered.data();
+        const int64_t e0 = N * w / nt * K, e1 = N * (w + 1) / nt * K;
+        for (int64_t e = e0; e < e1; e += 1024) o[e] = 0;  // one store per 4 KB page
       });
     for (auto &t : pool) t.join();
   }
@@ -125,6 +132,7 @@ void host_replay(HostIndex &H, TreeBuild &T, int64_t upto) {
   const int32_t K = H.K;
   const bool uniform = H.lens.empty();
   const int64_t t_from = T.done;
+  const auto q0 = std::chrono::steady_clock::now();
   // a round's merges arrive in the device's emission order, which is not
   // deterministic (reciprocal pairs are appended with atomics).  Sorted by key
   // (X9) they are still a valid replay order — the round's reciprocal pairs
@@ -143,7 +151,26 @@ void host_replay(HostIndex &H, TreeBuild &T, int64_t upto) {
       H.zs[t] = m.size;
     }
   }
+  const auto q1 = std::chrono::steady_clock::now();
+  // the loop is bound by the latency of its scattered reads (cur, the two
+  // children's sets): prefetch cur two strides ahead and the sets one stride
+  // ahead (a later merge of this batch may still renumber a cluster: only a
+  // wasted hint then)
+  constexpr int64_t kPf = 8;
+  auto set_addr = [&](int32_t X) -> const void * {
+    return X < N ? static_cast<const void *>(T.lset.data() + (int64_t)X * K)
+                 : static_cast<const void *>(T.vpool.data() + T.voff[X - N]);
+  };
   for (int64_t t = T.done; t < upto && T.ok; ++t) {
+    if (t + 2 * kPf < upto) {
+      __builtin_prefetch(&T.cur[H.za[t + 2 * kPf]]);
+      __builtin_prefetch(&T.cur[H.zb[t + 2 * kPf]]);
+    }
+    if (t + kPf < upto) {
+      const int32_t pa2 = T.cur[H.za[t + kPf]], pb2 = T.cur[H.zb[t + kPf]];
+      if (pa2 >= 0 && pa2 < N + t) __builtin_prefetch(set_addr(pa2));
+      if (pb2 >= 0 && pb2 < N + t) __builtin_prefetch(set_addr(pb2));
+    }
     const int32_t a = H.za[t], b = H.zb[t];
     if (a < 0 || b >= N || a >= b || T.cur[a] < 0 || T.cur[b] < 0 ||
         T.csize[a] + T.csize[b] != H.zs[t]) {
@@ -172,16 +199,12 @@ void host_replay(HostIndex &H, TreeBuild &T, int64_t upto) {
     }
     uint32_t tmp[256];
     int n = 0, ia = 0, ib = 0;
-    while (ia < la && ib < lb) {  // sorted intersection
-      if (pa[ia] < pb[ib]) {
-        ++ia;
-      } else if (pb[ib] < pa[ia]) {
-        ++ib;
-      } else {
-        tmp[n++] = pa[ia];
-        ++ia;
-        ++ib;
-      }
+    while (ia < la && ib < lb) {  // sorted intersection, branch-free steps
+      const uint32_t x = pa[ia], y = pb[ib];
+      tmp[n] = x;
+      n += (x == y);
+      ia += (x <= y);
+      ib += (y <= x);
     }
     T.vpool.insert(T.vpool.end(), tmp, tmp + n);
     T.voff[t + 1] = (int64_t)T.vpool.size();
@@ -198,6 +221,9 @@ void host_replay(HostIndex &H, TreeBuild &T, int64_t upto) {
     T.csize[a] += T.csize[b];
     T.done = t + 1;
   }
+  const auto q2 = std::chrono::steady_clock::now();
+  if (H.trace) std::fprintf(stderr, "[replay] n=%ld sort %.3f loop %.3f\n", (long)(upto - t_from),
+    std::chrono::duration<double, std::milli>(q1 - q0).count(), std::chrono::duration<double, std::milli>(q2 - q1).count());
   // the exported order (X9) is built here too, batch by batch: each replayed
   // batch is sorted while the device runs the next rounds, and host_finish
   // only merges the sorted runs
@@ -214,8 +240,14 @@ rb_status host_build(HostIndex &H, std::string *msg) {
     return RB_EINVAL;
   }
   TreeBuild T;
+  const auto t0 = std::chrono::steady_clock::now();
   host_begin(H, T);
+  const auto t1 = std::chrono::steady_clock::now();
   host_replay(H, T, (int64_t)H.za.size());
+  if (H.trace)
+    std::fprintf(stderr, "[ragb host] begin %.3f ms replay %.3f ms\n",
+                 std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count());
   return host_finish(H, T, msg);
 }
 
@@ -294,6 +326,16 @@ rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg) {
   // set as its raw parent, by induction.  Flags in parallel, then one
   // top-down pass (parents have larger merge index) numbers the kept nodes
   // 1..V in decreasing merge index, so every parent precedes its children.
+  // The tail runs two branches on two OpenMP teams (below) plus the merge
+  // sorter; the collapse uses branch B's team size so that the pool threads
+  // it leaves idle (libgomp spins them for milliseconds) do not compete with
+  // branch A's team for the cores.
+  const int thA = std::max(1, nth / 2), thB = std::max(1, nth - thA);
+#ifdef RAGB_COLLAPSE_NTH
+  const int thC = nth;
+#else
+  const int thC = thB;
+#endif
   std::vector<int64_t> vraw;
   std::vector<int32_t> vpar;
   H.lparent.assign(N, 0);
@@ -313,7 +355,7 @@ rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg) {
     // kept node ids in decreasing merge index (a suffix count of the flags,
     // chunked over the threads)
     std::vector<int32_t> eff(nz);  // kept node id standing for raw merge t
-    const int nc = std::max(1, std::min<int>(nth, (int)(nz / 8192) + 1));
+    const int nc = std::max(1, std::min<int>(thC, (int)(nz / 8192) + 1));
     std::vector<int64_t> ccount(nc + 1, 0);
 #pragma omp parallel for num_threads(nc) schedule(static, 1)
     for (int c = 0; c < nc; ++c) {  // chunk c covers t in [hi - ..., hi) from the top
@@ -344,7 +386,7 @@ rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg) {
     }
     for (bool more = true; more;) {
       more = false;
-#pragma omp parallel for num_threads(nth) schedule(static) reduction(|| : more)
+#pragma omp parallel for num_threads(thC) schedule(static) reduction(|| : more)
       for (int64_t t = 0; t < nz; ++t) {
         const int64_t u = up[t], uu = up[u];
         if (uu != u) {
@@ -354,15 +396,15 @@ rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg) {
       }
     }
     // eff of a collapsed merge: its nearest kept ancestor (0: the root)
-#pragma omp parallel for num_threads(nth) schedule(static)
+#pragma omp parallel for num_threads(thC) schedule(static)
     for (int64_t t = 0; t < nz; ++t)
       if (!keep[t]) eff[t] = keep[up[t]] ? eff[up[t]] : 0;
-#pragma omp parallel for num_threads(nth) schedule(static)
+#pragma omp parallel for num_threads(thC) schedule(static)
     for (int64_t k = 0; k < V0; ++k) {
       const int64_t p = rpar[vraw[k]];
       vpar[k] = p < 0 ? 0 : eff[p - N];
     }
-#pragma omp parallel for num_threads(nth) schedule(static)
+#pragma omp parallel for num_threads(thC) schedule(static)
     for (int64_t i = 0; i < N; ++i) {
       const int64_t p = rpar[i];
       H.lparent[i] = p < 0 ? 0 : eff[p - N];
@@ -376,10 +418,10 @@ rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg) {
   //   A (side thread): ordered prefixes of the virtual nodes (X10), then the
   //     leaves' ordered contexts (a7) and prefix lengths;
   //   B (this thread): children lists by rep (X12), search paths, schedule.
-  const int thA = std::max(1, nth / 2), thB = std::max(1, nth - thA);
   H.V = V;
   H.vparent.assign(vpar.begin(), vpar.end());
   std::thread branchA([&] {
+    const auto ta0 = std::chrono::steady_clock::now();
     // ---- virtual nodes: ordered prefixes (X10) ------------------------------
     // prefix(k) = prefix(parent) ++ sorted(set(k) \ set(parent)) has |set(k)|
     // entries; each node writes its own by walking up its ancestors (depth <=
@@ -410,9 +452,11 @@ rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg) {
         }
       }
     }
+    const auto ta1 = std::chrono::steady_clock::now();
     // ---- leaves: ordered contexts (a7) and prefix lengths -------------------
     H.ordered.resize((size_t)N * K);  // every entry written below (no fill)
     H.prefix_len.assign(N, 0);
+    const auto ta2 = std::chrono::steady_clock::now();
 #pragma omp parallel for num_threads(thA) schedule(static)
     for (int64_t i = 0; i < N; ++i) {
       const int32_t p = H.lparent[i];
@@ -429,6 +473,11 @@ rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg) {
       for (int k = L; k < K; ++k) out[k] = row[k];  // padding slots of a shorter context
       H.prefix_len[i] = (uint8_t)(p1 - p0);
     }
+    if (trace)
+      std::fprintf(stderr, "[ragb host] A: prefixes %.3f alloc %.3f leaves %.3f ms\n",
+                   std::chrono::duration<double, std::milli>(ta1 - ta0).count(),
+                   std::chrono::duration<double, std::milli>(ta2 - ta1).count(),
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ta2).count());
   });
 
   // ---- children CSR over nodes 0..V, ordered by rep (X12) -----------------

@@ -52,7 +52,7 @@ struct Tuning {
   int long_lists = -1;          // -1 auto, 0 general kernel for 32 < K <= 128
   int dist_grid = 0;            // 0 auto, > 0 grid cap of the distance kernel
   int host_threads = 0;         // 0 auto
-  bool trace = false;           // per-round trace on stderr
+  int trace = 0;                // per-round trace on stderr (1: synced per round, 2: events only)
   int side_buffer = -1;         // -1 auto, 0 in-place column rewrites in the matrix
   int nn_cache = -1;            // -1 auto, 0 no second-nearest cache (every affected row rescans)
   static Tuning from(const rb_params *p);

@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -301,7 +302,22 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
   int p = 0;
   void *next = matA;
   // per-round timing on stderr (diagnostics only)
-  const bool trace = tu.trace;
+  const bool trace = tu.trace == 1;
+  // trace 2: per-round events and host timestamps only (no extra syncs),
+  // printed once at the end (jitter diagnostics)
+  const bool ltrace = tu.trace == 2;
+  struct LRound {
+    cudaEvent_t e[3];
+    double h0, h1, h2;  // host: round top, sync returned, round bottom (ms)
+  };
+  std::vector<LRound> lr;
+  const auto lt0 = std::chrono::steady_clock::now();
+  cudaEvent_t lte[2];  // entry, after the last round
+  if (ltrace) {
+    for (auto &x : lte) cudaEventCreate(&x);
+    cudaEventRecord(lte[0], st);
+  }
+  auto lnow = [&] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - lt0).count(); };
   // in-place rounds: 0 never, 1 wherever allowed (testing), -1 cost model
   const int inplace_mode = tu.inplace < 0 ? 2 : tu.inplace;
   const double inplace_w = tu.inplace_weight;  // cost-model weight of a merge (row equivalents)
@@ -363,6 +379,12 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
     return side_reset(sb, Mc, st);
   };
   while (live > 1) {
+    if (ltrace) {
+      lr.emplace_back();
+      for (auto &x : lr.back().e) cudaEventCreate(&x);
+      lr.back().h0 = lnow();
+      cudaEventRecord(lr.back().e[0], st);
+    }
     if (trace) {
       cudaMemsetAsync(counters + 4, 0, 8 * sizeof(int), st);
       cudaEventRecord(tev[0], st);
@@ -408,11 +430,13 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
     *launches += 2;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (trace) cudaEventRecord(tev[1], st);
+    if (ltrace) cudaEventRecord(lr.back().e[1], st);
     int host_c[12] = {0};
     if ((e = cudaMemcpyAsync(host_c, counters, (trace ? 12 : 3) * sizeof(int), cudaMemcpyDeviceToHost, st)) !=
         cudaSuccess)
       return e;
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+    if (ltrace) lr.back().h1 = lnow();
     ++out->rounds;
     {  // this round's merges to the host, then let the host tree catch up
       const int z0 = zdone, z1 = host_c[0];
@@ -507,6 +531,10 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
       mask_ok = false;
       if ((e = nc_reset(Mn)) != cudaSuccess) return e;  // new column numbering
     }
+    if (ltrace) {
+      cudaEventRecord(lr.back().e[2], st);
+      lr.back().h2 = lnow();
+    }
     if (trace) {
       cudaEventRecord(tev[2], st);
       cudaEventSynchronize(tev[2]);
@@ -530,7 +558,27 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
   }
   if (trace)
     for (auto &x : tev) cudaEventDestroy(x);
+  if (ltrace) cudaEventRecord(lte[1], st);
   cudaStreamSynchronize(st);
+  if (ltrace) {
+    float a = 0, b = 0;
+    if (!lr.empty()) {
+      cudaEventElapsedTime(&a, lte[0], lr[0].e[0]);
+      cudaEventElapsedTime(&b, lr.back().e[2], lte[1]);
+    }
+    std::fprintf(stderr, "[ragb lt] setup=%.3f tail=%.3f host_end=%.3f\n", a, b, lnow());
+    for (auto &x : lte) cudaEventDestroy(x);
+    for (size_t i = 0; i < lr.size(); ++i) {
+      float a = 0, b = 0, g = 0;
+      cudaEventElapsedTime(&a, lr[i].e[0], lr[i].e[1]);
+      cudaEventElapsedTime(&b, lr[i].e[1], lr[i].e[2]);
+      if (i + 1 < lr.size()) cudaEventElapsedTime(&g, lr[i].e[2], lr[i + 1].e[0]);
+      std::fprintf(stderr, "[ragb lt] %zu prep=%.3f merge=%.3f gap=%.3f | host top=%.3f sync=%.3f bottom=%.3f\n", i, a,
+                   b, g, lr[i].h0, lr[i].h1, lr[i].h2);
+    }
+    for (auto &r : lr)
+      for (auto &x : r.e) cudaEventDestroy(x);
+  }
   for (size_t i = 0; i + 1 < mev.size(); i += 2) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, mev[i], mev[i + 1]);

@@ -11,7 +11,7 @@ from synth.workload import config
 
 z = np.load(sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/c4_merges.npz")
 w = config("C4")
-for rep in range(3):
+for rep in range(int(os.environ.get("REPS", "3"))):
     t = time.perf_counter()
     idx = ragb.index_from_linkage(w.ids, z["a"], z["b"], z["h"], z["size"])
     print(f"host build {1e3 * (time.perf_counter() - t):.2f} ms", flush=True)
