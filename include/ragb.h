@@ -83,7 +83,11 @@ enum rb_flags {
                                  D_ij (uint16) rows — parity/debug output     */
   RB_ALPHA_ANY = 1u << 1,     /* accept alpha outside the paper's band         */
   RB_KEEP_ROWS = 1u << 2,     /* linkage must not overwrite rows_dev           */
-  RB_SKIP_LINKAGE = 1u << 3   /* stop after distance rows + row NN (a1-a4)     */
+  RB_SKIP_LINKAGE = 1u << 3,  /* stop after distance rows + row NN (a1-a4)     */
+  RB_ASYNC_HOST = 1u << 4     /* return once the device stages (a1-a5) are done;
+                                 the host stage (a6-a7: tree, orders, schedule)
+                                 finishes on a library thread — see
+                                 rb_index_wait                                 */
 };
 
 typedef struct rb_params {
@@ -222,6 +226,17 @@ RB_API rb_status rb_index_size(const rb_index *idx, int64_t *N, int32_t *K);
 
 /* Build statistics. */
 RB_API rb_status rb_index_stats(const rb_index *idx, rb_stats *st);
+
+/* RB_ASYNC_HOST builds: wait for the handle's host stage (a6-a7, PAPER:335-339
+ * tree + §4.1 ordering) and return its status.  The build call returns once
+ * the device work is complete and the caller's device buffers (ids, rows,
+ * scratch) are free for the next build; the host stage uses only host memory
+ * owned by the handle, so a pipelined caller overlaps it with the next build's
+ * device stages.  Every other call on the handle (except rb_index_size /
+ * rb_index_shard) waits for it first; rb_index_free joins it.  Without the
+ * flag this returns RB_OK at once.  Errors: the host stage's (RB_EINVAL for an
+ * inconsistent merge list — an internal error). */
+RB_API rb_status rb_index_wait(rb_index *idx);
 
 /* The distance rows this index was built for: [row0, row0 + nrows) (all N
  * for a single-GPU build or an index from a merge list). */

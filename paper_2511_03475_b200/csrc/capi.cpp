@@ -75,6 +75,18 @@ rb_status check_poisoned() {
                             cudaGetErrorString((cudaError_t)e) + "); restart the process");
 }
 
+// RB_ASYNC_HOST: wait for the handle's host stage (once) and report its status
+rb_status settle(const rb_index *idx) {
+  std::lock_guard<std::mutex> lk(idx->host_mu);
+  if (idx->host.joinable()) idx->host.join();
+  if (idx->host_status != RB_OK) return fail(idx->host_status, idx->host_msg);
+  return RB_OK;
+}
+#define RB_SETTLE(idx)                                 \
+  do {                                                 \
+    if (rb_status s_ = settle(idx); s_ != RB_OK) return s_; \
+  } while (0)
+
 constexpr size_t kAlign = 256;
 
 size_t take(size_t &o, size_t bytes) {
@@ -554,20 +566,37 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
   H.stats.kernel_launches = launches;
 
   // ---- a6-a7: tree, orders, schedule (host) --------------------------------
-  if (linkage) {
-    const auto th = th_join;
+  // (RB_ASYNC_HOST: on a library thread after this call returns; the device
+  // and the caller's buffers are no longer used by then)
+  auto host_stage = [idx, th = th_join, t_start, trace2 = tu.trace == 2](ragb::TreeBuild &TB) -> rb_status {
+    HostIndex &HH = idx->H;
     const auto tf = clock::now();
     std::string msg;
-    s = ragb::host_finish(H, T, &msg);
-    if (s != RB_OK) return cleanup(fail(s, "internal: " + msg));
-    H.has_linkage = true;
-    H.stats.host_ms = std::chrono::duration<float, std::milli>(clock::now() - th).count();
-    if (tu.trace == 2)
+    const rb_status hs = ragb::host_finish(HH, TB, &msg);
+    if (hs != RB_OK) {
+      idx->host_msg = "internal: " + msg;
+      return hs;
+    }
+    HH.has_linkage = true;
+    HH.stats.host_ms = std::chrono::duration<float, std::milli>(clock::now() - th).count();
+    if (trace2)
       std::fprintf(stderr, "[ragb lt] host stage: to finish %.3f, finish %.3f ms\n",
                    std::chrono::duration<float, std::milli>(tf - th).count(),
                    std::chrono::duration<float, std::milli>(clock::now() - tf).count());
+    HH.stats.total_ms = std::chrono::duration<float, std::milli>(clock::now() - t_start).count();
+    return RB_OK;
+  };
+  if (linkage && (p->flags & RB_ASYNC_HOST)) {
+    auto tb = std::make_shared<ragb::TreeBuild>(std::move(T));
+    try {
+      idx->host = std::thread([idx, tb, host_stage]() mutable { idx->host_status = host_stage(*tb); });
+    } catch (...) {
+      return cleanup(fail(RB_ENOMEM, "host stage thread"));
+    }
+  } else {
+    if (linkage && (s = host_stage(T)) != RB_OK) return cleanup(fail(s, idx->host_msg));
+    H.stats.total_ms = std::chrono::duration<float, std::milli>(clock::now() - t_start).count();
   }
-  H.stats.total_ms = std::chrono::duration<float, std::milli>(clock::now() - t_start).count();
   *out = idx;
   g_err.clear();
   return cleanup(RB_OK);
@@ -654,6 +683,7 @@ rb_status rb_index_size(const rb_index *idx, int64_t *N, int32_t *K) {
 
 rb_status rb_index_stats(const rb_index *idx, rb_stats *st) {
   if (!idx || !st) return fail(RB_EINVAL, "NULL argument");
+  RB_SETTLE(idx);
   *st = idx->H.stats;
   return RB_OK;
 }
@@ -667,6 +697,7 @@ rb_status rb_index_shard(const rb_index *idx, int64_t *row0, int64_t *nrows) {
 
 rb_status rb_index_counts(const rb_index *idx, int64_t row0, int64_t nrows, uint8_t *s_dev, uint16_t *D_dev) {
   if (!idx || !s_dev || !D_dev) return fail(RB_EINVAL, "NULL argument");
+  RB_SETTLE(idx);
   const HostIndex &H = idx->H;
   if (H.dyn) return fail(RB_ESTATE, "index was updated online (the counts cover the built set only)");
   if (row0 < 0 || nrows < 0 || row0 + nrows > H.N) return fail(RB_EINVAL, "bad row range");
@@ -707,6 +738,7 @@ rb_status rb_index_counts(const rb_index *idx, int64_t row0, int64_t nrows, uint
 
 rb_status rb_index_nn(const rb_index *idx, int32_t *nn_idx, float *nn_d) {
   if (!idx) return fail(RB_EINVAL, "NULL index");
+  RB_SETTLE(idx);
   const HostIndex &H = idx->H;
   if (H.nn_idx.empty()) return fail(RB_ESTATE, "no NN (index built from a linkage)");
   if (nn_idx) std::memcpy(nn_idx, H.nn_idx.data(), H.nn_idx.size() * 4);
@@ -716,6 +748,7 @@ rb_status rb_index_nn(const rb_index *idx, int32_t *nn_idx, float *nn_d) {
 
 rb_status rb_index_linkage(const rb_index *idx, int32_t *a, int32_t *b, float *h, int32_t *size) {
   if (!idx) return fail(RB_EINVAL, "NULL index");
+  RB_SETTLE(idx);
   const HostIndex &H = idx->H;
   if (!H.has_linkage) return fail(RB_ESTATE, "linkage was skipped");
   const size_t n = H.za.size();
@@ -731,6 +764,7 @@ static int64_t node_count(const HostIndex &H) { return 1 + H.V + H.N; }
 rb_status rb_index_tree_info(const rb_index *idx, int64_t *n_nodes, int64_t *prefix_total,
                              int64_t *path_total) {
   if (!idx) return fail(RB_EINVAL, "NULL index");
+  RB_SETTLE(idx);
   const HostIndex &H = idx->H;
   if (!H.has_linkage) return fail(RB_ESTATE, "linkage was skipped");
   if (H.dyn) {
@@ -753,6 +787,7 @@ rb_status rb_index_tree(const rb_index *idx, int32_t *parent, int32_t *leaf, int
                         int64_t *prefix_off, uint32_t *prefix_ids, int64_t *path_off,
                         int32_t *path) {
   if (!idx) return fail(RB_EINVAL, "NULL index");
+  RB_SETTLE(idx);
   const HostIndex &H = idx->H;
   if (!H.has_linkage) return fail(RB_ESTATE, "linkage was skipped");
   if (H.dyn) {
@@ -799,6 +834,7 @@ rb_status rb_order_contexts(rb_index *idx, const uint32_t *ids, const uint8_t *l
                             int32_t K, uint32_t *out_ids, uint8_t *out_prefix_len,
                             int64_t *out_schedule) {
   if (!idx) return fail(RB_EINVAL, "NULL index");
+  RB_SETTLE(idx);
   HostIndex &H = idx->H;
   if (!H.has_linkage) return fail(RB_ESTATE, "linkage was skipped");
   if (K != H.K) return fail(RB_EINVAL, "K must match the index");
@@ -832,6 +868,7 @@ rb_status rb_order_contexts(rb_index *idx, const uint32_t *ids, const uint8_t *l
 
 rb_status rb_index_set_online(rb_index *idx, int32_t device) {
   if (!idx) return fail(RB_EINVAL, "NULL index");
+  RB_SETTLE(idx);
   if (device < -1 || device > 1) return fail(RB_EINVAL, "device must be -1, 0 or 1");
   if (device == 1 && check_poisoned() != RB_OK) return RB_ECUDA;
   idx->H.online_device = device;
@@ -840,6 +877,7 @@ rb_status rb_index_set_online(rb_index *idx, int32_t device) {
 
 rb_status rb_index_set_alpha(rb_index *idx, uint32_t alpha_num, uint32_t alpha_den) {
   if (!idx) return fail(RB_EINVAL, "NULL index");
+  RB_SETTLE(idx);
   if (alpha_den == 0 || alpha_den > 1000 || alpha_num > alpha_den)
     return fail(RB_EALPHA, "alpha must be num/den with 1 <= den <= 1000, num <= den");
   idx->H.alpha_num = alpha_num;
@@ -864,6 +902,7 @@ static rb_status session_from_docs(const uint32_t *docs, int32_t n, rb_session *
 
 rb_status rb_session_open(const rb_index *idx, int64_t row, rb_session **out) {
   if (!idx || !out) return fail(RB_EINVAL, "NULL argument");
+  RB_SETTLE(idx);
   const HostIndex &H = idx->H;
   if (!H.has_linkage) return fail(RB_ESTATE, "linkage was skipped");
   if (H.dyn) {
@@ -978,6 +1017,7 @@ rb_status rb_session_turn(const rb_session *s, int32_t *turn) {
 rb_status rb_index_cache_event(rb_index *idx, int32_t kind, const int32_t *path, int32_t path_len,
                                int64_t n_tokens, int64_t *taken) {
   if (!idx) return fail(RB_EINVAL, "NULL index");
+  RB_SETTLE(idx);
   if (!idx->H.has_linkage) return fail(RB_ESTATE, "linkage was skipped");
   if (path_len < 0) return fail(RB_EINVAL, "negative path length");
   std::string msg;
@@ -987,12 +1027,18 @@ rb_status rb_index_cache_event(rb_index *idx, int32_t kind, const int32_t *path,
 
 rb_status rb_index_cache_state(const rb_index *idx, int64_t *seq_len, int64_t *last_access) {
   if (!idx) return fail(RB_EINVAL, "NULL index");
+  RB_SETTLE(idx);
   if (!idx->H.dyn) return fail(RB_ESTATE, "no cache events applied yet");
   ragb::dyn_cache_state(idx->H, seq_len, last_access);
   return RB_OK;
 }
 
 void rb_session_free(rb_session *s) { delete s; }
-void rb_index_free(rb_index *idx) { delete idx; }
+void rb_index_free(rb_index *idx) { delete idx; }  // (joins a pending host stage)
+
+rb_status rb_index_wait(rb_index *idx) {
+  if (!idx) return fail(RB_EINVAL, "NULL index");
+  return settle(idx);
+}
 
 }  // extern "C"

@@ -11,6 +11,8 @@
 #include <string>
 #include <utility>
 #include <vector>
+#include <thread>
+#include <mutex>
 
 #include "ragb.h"
 
@@ -277,4 +279,13 @@ rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg);
 // the C-ABI handle (capi.cpp, dist.cu)
 struct rb_index {
   ragb::HostIndex H;
+  // RB_ASYNC_HOST: the host stage (a6-a7) runs on `host` after the build call
+  // returned; every call on the handle settles it first (capi.cpp settle())
+  mutable std::mutex host_mu;
+  mutable std::thread host;
+  mutable rb_status host_status = RB_OK;
+  mutable std::string host_msg;
+  ~rb_index() {
+    if (host.joinable()) host.join();
+  }
 };

@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_PKG, "lib", f"libragb_{os.environ['RAGB_LIB']}.so" if o
 
 RB_OK, RB_EINVAL, RB_EDUPDOC, RB_EALPHA, RB_ENOMEM, RB_ECUDA, RB_ENCCL, RB_EPATH, RB_ESESSION, \
     RB_ESTATE = 0, -1, -2, -3, -4, -5, -6, -7, -8, -9
-RB_EMIT_COUNTS, RB_ALPHA_ANY, RB_KEEP_ROWS, RB_SKIP_LINKAGE = 1, 2, 4, 8
+RB_EMIT_COUNTS, RB_ALPHA_ANY, RB_KEEP_ROWS, RB_SKIP_LINKAGE, RB_ASYNC_HOST = 1, 2, 4, 8, 16
 RB_LINK_COMPLETE, RB_LINK_INTERSECTION = 0, 1
 RB_CACHE_APPENDED, RB_CACHE_ACCESSED, RB_CACHE_EVICTED = 0, 1, 2
 RB_PATH_GATHER, RB_PATH_GATHER_WIDE, RB_PATH_WINDOW, RB_PATH_WINDOW_WIDE, RB_PATH_INPLACE, \
@@ -31,6 +31,7 @@ STATUS_NAMES = {0: "RB_OK", -1: "RB_EINVAL", -2: "RB_EDUPDOC", -3: "RB_EALPHA", 
 EXPORTED = [
     "rb_version", "rb_last_error", "rb_params_init", "rb_workspace_size", "rb_build_index",
     "rb_build_index_host", "rb_index_from_linkage", "rb_index_size", "rb_index_stats", "rb_index_shard",
+    "rb_index_wait",
     "rb_index_counts", "rb_index_nn",
     "rb_index_linkage", "rb_index_tree_info", "rb_index_tree", "rb_order_contexts", "rb_session_open",
     "rb_session_open_docs", "rb_dedup_turn", "rb_session_turn", "rb_session_free", "rb_index_free",
@@ -100,6 +101,7 @@ def lib():
         "rb_index_from_linkage": ([P, P, i64, i32, P, P, P, P, PP], i32),
         "rb_index_size": ([P, ctypes.POINTER(i64), ctypes.POINTER(i32)], i32),
         "rb_index_stats": ([P, ctypes.POINTER(Stats)], i32),
+        "rb_index_wait": ([P], i32),
         "rb_index_shard": ([P, ctypes.POINTER(i64), ctypes.POINTER(i64)], i32),
         "rb_index_counts": ([P, i64, i64, P, P], i32),
         "rb_index_nn": ([P, P, P], i32),
@@ -200,6 +202,12 @@ class Index:
         if h and _lib is not None:
             _lib.rb_index_free(h)
             self._h = None
+
+    def wait(self):
+        """RB_ASYNC_HOST builds: wait for the host stage (a6-a7); every other
+        method waits by itself."""
+        _check(lib().rb_index_wait(self._h))
+        return self
 
     def stats(self) -> dict:
         s = Stats()

@@ -122,6 +122,11 @@ def test_fig4_fig5_host(golden):
     out, plen, _ = idx.order_contexts()
     g = golden["fig5_ordering"]
     assert out[0].tolist() == g["printed"]["C1"] and out[1].tolist() == g["printed"]["C2"]
+    assert idx.wait() is idx  # rb_index_wait: nothing pending on a synchronous handle
+
+
+def test_index_wait_null():
+    assert ragb.lib().rb_index_wait(None) == -1  # RB_EINVAL
 
 
 @pytest.mark.parametrize("seed", range(8))

@@ -186,6 +186,35 @@ def test_deterministic_repeat(case):
             assert np.array_equal(t[k], t0[k]), k
 
 
+def test_async_host_pipelined():
+    """RB_ASYNC_HOST (ragb.h rb_index_wait): builds return after the device
+    stages and finish the host stage on a library thread; two pipelined builds
+    sharing one workspace (the second launched while the first's host stage
+    may still run) equal synchronous builds byte for byte, and also through
+    the host-buffer entry."""
+    cases = [generate(3000, 20, 30000, 91), generate(5000, 4, 2000, 17)]
+    ref = []
+    for w in cases:
+        idx, _ = dev_build(w.ids, flags=0)
+        ref.append((idx.linkage(), idx.order_contexts(), idx.tree()))
+    for w, (lk, oc_, tr) in zip(cases, ref):
+        t = torch.from_numpy(np.ascontiguousarray(w.ids).view(np.int32)).cuda()
+        a, ws = F.build_index(t, flags=F.RB_ASYNC_HOST)
+        b, ws = F.build_index(t, flags=F.RB_ASYNC_HOST, workspace=ws)  # a's host stage may still run
+        c, _ = F.build_index_host(w.ids, flags=F.RB_ASYNC_HOST, workspace=ws)
+        for idx in (b, a, c):  # b settles first: every accessor waits by itself
+            for x, y in zip(idx.linkage(), lk):
+                assert np.array_equal(x, y)
+            for x, y in zip(idx.order_contexts(), oc_):
+                assert np.array_equal(x, y)
+            tt = idx.tree()
+            for k in tr:
+                assert np.array_equal(tt[k], tr[k]), k
+            st = idx.wait().stats()
+            assert st["host_ms"] > 0 and st["total_ms"] >= st["linkage_ms"]
+        del a, b, c  # rb_index_free joins a pending host stage
+
+
 # ------------------------------------------------------------- full sizes
 def linkage_properties(a, b, h, s, N):
     """Properties of a complete-linkage merge order that hold at any size."""
