@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import argparse
 import json
+from concurrent.futures import ThreadPoolExecutor
 import os
 import statistics
 import subprocess
@@ -313,16 +314,16 @@ def run_ours(args, ws, rank, local):
     pipelined = not sharded and not os.environ.get("RAGB_BENCH_SEQUENTIAL")
 
     def run_pipelined(n, build_fn, finish_fn):
-        prev = None
-        for _ in range(n):
-            flush.zero_()
-            idx = build_fn()
-            if prev is not None:
-                finish_fn(prev)
-            prev = idx
-        if prev is not None:
-            finish_fn(prev)
-        return prev
+        # finish_fn (wait for the host stage, read the orders back, release
+        # the handle) runs on a helper thread while the next build's device
+        # stages run; all of them complete inside the caller's timed region
+        futs = []
+        with ThreadPoolExecutor(max_workers=1) as ex:
+            for _ in range(n):
+                flush.zero_()
+                futs.append(ex.submit(finish_fn, build_fn()))
+            for f in futs:
+                f.result()
 
     if pipelined:
         def build_async():
