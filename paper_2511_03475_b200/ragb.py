@@ -435,7 +435,11 @@ def build_index(ids, lens=None, *, alpha=(1, 200), flags=0, row0=0, nrows=-1, st
     """Build the context index from device ids (torch.int32/uint32 CUDA tensor [N, K]).
 
     Returns (Index, Workspace); workspace.rows holds the distance rows (unless
-    the linkage consumed them: pass flags |= RB_KEEP_ROWS to keep them)."""
+    the linkage consumed them: pass flags |= RB_KEEP_ROWS to keep them).
+    flags |= RB_ASYNC_HOST returns once the device stages are done (the
+    workspace is free for the next build) and finishes the tree / orders /
+    schedule on a library thread; Index methods wait for it (ragb.h
+    rb_index_wait)."""
     import torch
     if not ids.is_cuda:
         raise ValueError("build_index expects a CUDA tensor; use build_index_host for host arrays")
