@@ -2245,6 +2245,85 @@ __global__ void __launch_bounds__(NTH) k_inplace_rescan(const T *__restrict__ D,
   for (int k = tid; k < MW; k += NTH) smask[k] = amask[k] & ~(sb.T ? sb.dmask[k] : 0u);
   for (int k = tid; k < nt; k += NTH) scol[k] = sb.tcol[k];
   __syncthreads();
+#ifdef RAGB_RESCAN64
+  constexpr bool kKey32 = false;  // variant: the 64-bit keys for codes too (A/B)
+#else
+  constexpr bool kKey32 = true;
+#endif
+  if constexpr (sizeof(T) == 2 && kKey32) {
+    // 16-bit codes and M <= kInplaceMaxM < 2^16: a key (code, column) fits
+    // 32 bits as code << 16 | column (same order as the 64-bit key), and the
+    // two smallest are kept branch-free with min/max (~half the instructions
+    // of the 64-bit compare-and-swap per column)
+    for (int i = blockIdx.x; i < nres; i += gridDim.x) {
+      const int r = rlist[i];
+      unsigned b0 = ~0u, b1 = ~0u;
+      auto ins = [&](unsigned k) {
+        const unsigned hi = max(b0, k);
+        b0 = min(b0, k);
+        b1 = min(b1, hi);
+      };
+      const uint4 *src = reinterpret_cast<const uint4 *>(D + (int64_t)r * ld);
+      constexpr int UR = 4;
+      for (int q0 = tid; q0 < MV; q0 += NTH * UR) {
+        uint4 x[UR];
+#pragma unroll
+        for (int u = 0; u < UR; ++u) x[u] = q0 + u * NTH < MV ? __ldcs(src + q0 + u * NTH) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int u = 0; u < UR; ++u) {
+          const int q = q0 + u * NTH;
+          if (q >= MV) continue;
+          const int c0 = VW * q;
+          unsigned mb = (smask[c0 >> 5] >> (c0 & 31)) & 0xffu;
+          if (c0 + 8 > M) mb &= (1u << (M - c0)) - 1u;
+          if (r >= c0 && r < c0 + 8) mb &= ~(1u << (r - c0));
+          const unsigned xv[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const unsigned v = (k & 1) ? (xv[k >> 1] >> 16) : (xv[k >> 1] & 0xffffu);
+            ins(((mb >> k) & 1u) ? ((v << 16) | (unsigned)(c0 + k)) : ~0u);
+          }
+        }
+      }
+      if (nt > 0) {
+        const uint4 *trow4 = reinterpret_cast<const uint4 *>(sb.T + (int64_t)r * sb.cap);
+        for (int k8 = tid; 8 * k8 < nt; k8 += NTH) {
+          unsigned vs[8];
+          Elem<uint16_t>::unpack(trow4[k8], vs);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int k = 8 * k8 + u;
+            const int c = k < nt ? scol[k] : -1;
+            ins((c >= 0 && c != r) ? ((vs[u] << 16) | (unsigned)c) : ~0u);
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned y0 = __shfl_xor_sync(0xffffffffu, b0, o), y1 = __shfl_xor_sync(0xffffffffu, b1, o);
+        ins(y0);
+        ins(y1);
+      }
+      auto widen = [](unsigned k) -> u64 { return k == ~0u ? ~0ull : ((u64)(k >> 16) << 32) | (k & 0xffffu); };
+      if (lane == 0) {
+        wmin[w][0] = widen(b0);
+        wmin[w][1] = widen(b1);
+      }
+      __syncthreads();
+      if (tid == 0) {
+        u64 bb[2] = {wmin[0][0], wmin[0][1]};
+        for (int i2 = 1; i2 < NTH / 32; ++i2)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) top2_insert(bb, wmin[i2][q]);
+        key[r] = bb[0];
+        if (nc.key2) {
+          nc.key2[r] = bb[1];
+          nc.kround[r] = bb[1] != ~0ull ? nc.round : 0;
+        }
+      }
+      __syncthreads();
+    }
+  } else {
   for (int i = blockIdx.x; i < nres; i += gridDim.x) {
     const int r = rlist[i];
     u64 bt[2] = {~0ull, ~0ull};  // the row's two smallest keys (this thread)
@@ -2311,6 +2390,7 @@ __global__ void __launch_bounds__(NTH) k_inplace_rescan(const T *__restrict__ D,
       }
     }
     __syncthreads();
+  }
   }
 }
 
