@@ -17,6 +17,7 @@ typedef unsigned long long u64;
 constexpr int PT = 1024;  // threads of the single-CTA round-prep kernel
 constexpr u64 kDead = ~0ull;  // row key of a row merged away by an in-place round
 constexpr int kInplaceMaxM = 48 * 1024;  // in-place rounds keep a whole row in shared memory
+static_assert(kInplaceMaxM < (1 << 16), "in-place row minima use 32-bit (code << 16 | column) keys");
 
 // ---------------------------------------------------------------------------
 // Stored element of the linkage matrices.  float: the Eq. 1 value itself;
@@ -2024,7 +2025,9 @@ __global__ void __launch_bounds__(NTH, 2) k_inplace_rows_sb(PrepArgs a, uint16_t
     __syncthreads();
     if (tid == 0) row[L] = 0;
     __syncthreads();
-    u64 best = ~0ull;
+    // row minimum on 32-bit keys code << 16 | column (M <= kInplaceMaxM < 2^16:
+    // the 64-bit key's order; ~0u = none)
+    unsigned best = ~0u;
     uint4 *out = reinterpret_cast<uint4 *>(D + (int64_t)L * ld);
     for (int q = tid; q < MV; q += NTH) {
       const uint4 v = rowv[q];
@@ -2038,8 +2041,7 @@ __global__ void __launch_bounds__(NTH, 2) k_inplace_rows_sb(PrepArgs a, uint16_t
         const int c = c0 + k;
         // live, and clean or merged this round (its value is in the new row)
         const bool live = ((mb >> k) & 1u) && c < M && c != L && (!((db >> k) & 1u) || a.alive[c]);
-        const u64 kk = ((u64)vv[k] << 32) | (unsigned)c;
-        best = (live && kk < best) ? kk : best;
+        best = min(best, live ? (vv[k] << 16) | (unsigned)c : ~0u);
       }
     }
     uint4 *tout = reinterpret_cast<uint4 *>(sb.T + (int64_t)L * sb.cap);
@@ -2047,15 +2049,11 @@ __global__ void __launch_bounds__(NTH, 2) k_inplace_rows_sb(PrepArgs a, uint16_t
     for (int k = tid; k < nt; k += NTH) {
       const int c = sb.tcol[k];  // retired slots (incl. dead columns): -1
       if (c < 0 || c == L || a.alive[c]) continue;
-      const u64 kk = ((u64)trow[k] << 32) | (unsigned)c;
-      best = kk < best ? kk : best;
+      best = min(best, ((unsigned)trow[k] << 16) | (unsigned)c);
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const u64 y = __shfl_xor_sync(0xffffffffu, best, o);
-      best = y < best ? y : best;
-    }
-    if (lane == 0) wmin[w] = best;
+    for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if (lane == 0) wmin[w] = best == ~0u ? ~0ull : ((u64)(best >> 16) << 32) | (best & 0xffffu);
     __syncthreads();
     if (tid == 0) {
       u64 b = wmin[0];
