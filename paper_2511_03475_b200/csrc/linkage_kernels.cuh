@@ -381,14 +381,21 @@ __global__ void __launch_bounds__(256) k_level_adj_rows(PrepArgs a, uint32_t *__
         // dirty columns (side buffer) hold stale values here: taken from T below
         const uint32_t clean = sb.T ? ~(sb.dmask[c0 >> 5] >> (c0 & 31)) : ~0u;
         const int base = (int)lpre[c0 >> 5] + __popc(below);
+        // the vector's matches land in level positions [base, base + VW): at
+        // most two adjacency words, one shared atomic each (not one per match)
+        const int wj = base >> 5, sh = base & 31;
+        uint32_t lo = 0u, hi = 0u;
 #pragma unroll
         for (int k = 0; k < VW; ++k) {
           const int c = c0 + k;
           if (((mb & clean) >> k & 1u) && v[k] == hb && c != r) {
-            const int j = base + __popc(mb & ((1u << k) - 1u));
-            atomicOr(&wbits[j >> 5], 1u << (j & 31));
+            const int b = sh + __popc(mb & ((1u << k) - 1u));  // < 32 + VW
+            if (b < 32) lo |= 1u << b;
+            else hi |= 1u << (b - 32);
           }
         }
+        if (lo) atomicOr(&wbits[wj], lo);
+        if (hi) atomicOr(&wbits[wj + 1], hi);
       }
       if (sb.T) {  // dirty columns from the side buffer
         const int nt = *sb.nt;
