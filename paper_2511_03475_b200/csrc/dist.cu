@@ -627,7 +627,7 @@ rb_status build_index_dist(rb_dist *d, const uint32_t *ids_d, const uint8_t *len
       unsigned char *sc = d->scratch[r];
       k_adj_gather<<<sms * 4, 256, 0, st>>>(pa[l], at<uint32_t>(sc, L.adj),
                                             reinterpret_cast<const uint32_t *const *>(table(r, TADJ)), world, r, S);
-      const size_t m1 = std::min<size_t>((size_t)M, 1024);
+      const size_t m1 = std::min<size_t>((size_t)M, (size_t)std::min(1024, kWarpCliqueMaxN));  // staged only on the warp path
       const size_t smem = m1 * ((m1 + 31) / 32) * 4;  // the staged adjacency of levels <= 1024
       if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_level_cliques, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

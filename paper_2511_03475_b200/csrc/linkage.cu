@@ -418,7 +418,7 @@ cudaError_t run_linkage(float *rows, int64_t N, unsigned long long *nnkey, void 
       }
     }
     {
-      const size_t m1 = std::min<size_t>((size_t)M, 1024);
+      const size_t m1 = std::min<size_t>((size_t)M, (size_t)std::min(1024, kWarpCliqueMaxN));  // staged only on the warp path
       const size_t smem = m1 * ((m1 + 31) / 32) * 4;  // the staged adjacency of levels <= 1024
       if (smem > 48 * 1024)
         occupancy_cached(k_level_cliques, CT, smem);
