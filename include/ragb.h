@@ -84,10 +84,10 @@ enum rb_flags {
   RB_ALPHA_ANY = 1u << 1,     /* accept alpha outside the paper's band         */
   RB_KEEP_ROWS = 1u << 2,     /* linkage must not overwrite rows_dev           */
   RB_SKIP_LINKAGE = 1u << 3,  /* stop after distance rows + row NN (a1-a4)     */
-  RB_ASYNC_HOST = 1u << 4     /* return once the device stages (a1-a5) are done;
-                                 the host stage (a6-a7: tree, orders, schedule)
-                                 finishes on a library thread — see
-                                 rb_index_wait                                 */
+  RB_ASYNC_HOST = 1u << 4     /* rb_build_index / _host: return once the device
+                                 stages (a1-a5) are done; the host stage (a6-a7:
+                                 tree, orders, schedule) finishes on a library
+                                 thread — see rb_index_wait                    */
 };
 
 typedef struct rb_params {
