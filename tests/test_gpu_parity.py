@@ -215,6 +215,33 @@ def test_async_host_pipelined():
         del a, b, c  # rb_index_free joins a pending host stage
 
 
+def test_async_host_soak_C3():
+    """Eight pipelined C3 builds on one workspace, each read back on a helper
+    thread while the next build runs (the bench's pattern): every one equals
+    the synchronous build."""
+    from concurrent.futures import ThreadPoolExecutor
+    w = config("C3")
+    ref, _ = dev_build(w.ids, flags=0)
+    ra, ro = ref.linkage(), ref.order_contexts()
+    t = torch.from_numpy(np.ascontiguousarray(w.ids).view(np.int32)).cuda()
+    ws = None
+
+    def check(idx):
+        for x, y in zip(idx.linkage(), ra):
+            assert np.array_equal(x, y)
+        for x, y in zip(idx.order_contexts(), ro):
+            assert np.array_equal(x, y)
+        return True
+
+    with ThreadPoolExecutor(max_workers=1) as ex:
+        futs = []
+        for _ in range(8):
+            idx, ws = F.build_index(t, flags=F.RB_ASYNC_HOST, workspace=ws)
+            futs.append(ex.submit(check, idx))
+            del idx
+        assert all(f.result() for f in futs)
+
+
 # ------------------------------------------------------------- full sizes
 def linkage_properties(a, b, h, s, N):
     """Properties of a complete-linkage merge order that hold at any size."""
