@@ -589,7 +589,14 @@ static rb_status build_common(const uint32_t *ids_dev, const uint8_t *lens_dev, 
   if (linkage && (p->flags & RB_ASYNC_HOST)) {
     auto tb = std::make_shared<ragb::TreeBuild>(std::move(T));
     try {
-      idx->host = std::thread([idx, tb, host_stage]() mutable { idx->host_status = host_stage(*tb); });
+      idx->host = std::thread([idx, tb, host_stage]() mutable {
+        try {
+          idx->host_status = host_stage(*tb);
+        } catch (...) {  // (no exception may leave the library's thread)
+          idx->host_msg = "host stage: allocation failed";
+          idx->host_status = RB_ENOMEM;
+        }
+      });
     } catch (...) {
       return cleanup(fail(RB_ENOMEM, "host stage thread"));
     }
