@@ -73,6 +73,7 @@ void host_begin(HostIndex &H, TreeBuild &T) {
   const int32_t K = H.K;
   const bool uniform = H.lens.empty();
   const int nth = host_threads();
+  const auto hb0 = std::chrono::steady_clock::now();
   T.zk.clear();
   T.runs.clear();
   T.rpar.assign((size_t)(N + std::max<int64_t>(N - 1, 0)), -1);
@@ -89,7 +90,7 @@ void host_begin(HostIndex &H, TreeBuild &T) {
   {
     // (two cores fewer than the tail stages: the round-launching thread and
     // this replay worker must not be preempted while the device rounds run)
-    const int nt = std::max(1, std::min<int>(nth - 2, (int)(N / 4096) + 1));
+    const int nt = std::max(1, std::min<int>(nth - 2, (int)((int64_t)N * K / 81920) + 1));  // ~80K entries per thread
     std::vector<std::thread> pool;
     for (int w = 0; w < nt; ++w)
       pool.emplace_back([&, w] {
@@ -97,7 +98,12 @@ void host_begin(HostIndex &H, TreeBuild &T) {
           uint32_t *d = T.lset.data() + i * K;
           const uint32_t *src = H.ids.data() + i * K;
           const int L = uniform ? K : H.lens[i];
-          for (int k = 0; k < L; ++k) {  // insertion sort (K <= 255, typically 5-20)
+          if (L > 32) {  // long lists (C5: K up to 100): O(L log L)
+            std::copy(src, src + L, d);
+            std::sort(d, d + L);
+            continue;
+          }
+          for (int k = 0; k < L; ++k) {  // insertion sort (typically 5-20 entries)
             const uint32_t x = src[k];
             int q = k;
             while (q > 0 && d[q - 1] > x) {
@@ -113,6 +119,7 @@ void host_begin(HostIndex &H, TreeBuild &T) {
       });
     for (auto &t : pool) t.join();
   }
+  const auto hb1 = std::chrono::steady_clock::now();
   const int64_t nz = std::max<int64_t>(N - 1, 0);
   T.voff.assign(nz + 1, 0);
   T.vpool.clear();
@@ -123,6 +130,10 @@ void host_begin(HostIndex &H, TreeBuild &T) {
   T.csize.assign(N, 1);
   T.done = 0;
   T.ok = true;
+  if (H.trace)
+    std::fprintf(stderr, "[ragb host] begin: setup+sort %.3f ms, rest %.3f ms\n",
+                 std::chrono::duration<double, std::milli>(hb1 - hb0).count(),
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hb1).count());
 }
 
 // Replay merges [T.done, upto) of H.za/zb/zs: any order in which every merge
@@ -276,7 +287,7 @@ rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg) {
     *msg = T.err;
     return RB_EINVAL;
   }
-  const std::vector<uint32_t> &lset = T.lset;
+  const auto &lset = T.lset;
   const std::vector<int64_t> &voff = T.voff;
   const std::vector<uint32_t> &vpool = T.vpool;
   const std::vector<int32_t> &rchild = T.rchild;
@@ -468,8 +479,30 @@ rb_status host_finish(HostIndex &H, TreeBuild &T, std::string *msg) {
       const uint32_t *sp = p > 0 ? set_ptr(vraw[p - 1], &np) : nullptr;
       const uint32_t *row = H.ids.data() + i * K;
       const int L = len_of(i);
-      for (int k = 0; k < L; ++k)
-        if (!in_sorted(sp, np, row[k])) out[o++] = row[k];
+      if (np > 16) {
+        // long parent sets (C5: K up to 100): an open-addressing table of the
+        // parent's docs (0xFFFFFFFF, the reserved DocId, marks an empty slot)
+        // instead of a branchy binary search per entry
+        uint32_t tab[512];
+        int bits = 5;
+        while ((1 << bits) < 2 * np) ++bits;
+        const uint32_t msk = (1u << bits) - 1u;
+        std::fill(tab, tab + (1 << bits), 0xFFFFFFFFu);
+        for (int z = 0; z < np; ++z) {
+          uint32_t hsh = (sp[z] * 0x9E3779B1u) >> (32 - bits);
+          while (tab[hsh] != 0xFFFFFFFFu) hsh = (hsh + 1) & msk;
+          tab[hsh] = sp[z];
+        }
+        for (int k = 0; k < L; ++k) {
+          const uint32_t x = row[k];
+          uint32_t hsh = (x * 0x9E3779B1u) >> (32 - bits);
+          while (tab[hsh] != 0xFFFFFFFFu && tab[hsh] != x) hsh = (hsh + 1) & msk;
+          if (tab[hsh] != x) out[o++] = x;
+        }
+      } else {
+        for (int k = 0; k < L; ++k)
+          if (!in_sorted(sp, np, row[k])) out[o++] = row[k];
+      }
       for (int k = L; k < K; ++k) out[k] = row[k];  // padding slots of a shorter context
       H.prefix_len[i] = (uint8_t)(p1 - p0);
     }

@@ -261,7 +261,7 @@ struct TreeBuild {
   std::vector<int64_t> runs;    // boundaries of the sorted batches in zk
   std::vector<int64_t> rpar;    // [N + N-1] raw parent node of every node (-1: none yet)
   std::vector<uint8_t> keep;    // [N-1] raw merge t kept by the collapse (X11), set once its parent exists
-  std::vector<uint32_t> lset;   // [N][K] sorted leaf sets
+  std::vector<uint32_t, NoInitAlloc<uint32_t>> lset;  // [N][K] sorted leaf sets (written by the sort threads: no fill)
   std::vector<int64_t> voff;    // [N] offsets of merge t's intersection set
   std::vector<uint32_t> vpool;
   std::vector<int32_t> rchild;  // [2(N-1)] raw children of merge t

@@ -138,6 +138,18 @@ def test_host_index_random(seed):
     check_host_index(w.ids, w.lens)
 
 
+@pytest.mark.parametrize("seed", range(3))
+def test_host_index_long_lists(seed):
+    """K of 40-100 over a small pool: leaf sets longer than 32 (sorted with
+    std::sort) and parent sets above 16 docs (the hashed membership of the
+    leaves' ordered contexts), fixed and variable lengths."""
+    rng = np.random.default_rng(100 + seed)
+    K = int(rng.integers(40, 101))
+    N = int(rng.integers(20, 90))
+    w = generate(N, K, K + int(rng.integers(2, 30)), 100 + seed, len_min=(K - 10 if seed % 2 else None))
+    check_host_index(w.ids, w.lens)
+
+
 @pytest.mark.parametrize("kind", ["disjoint", "identical", "permutations"])
 def test_host_index_edges(kind):
     check_host_index(edge(kind, 17, 5).ids)
