@@ -105,7 +105,7 @@ typedef struct rb_params {
                              uniform K <= 32 (complete linkage); 0: fp32 matrices  */
   int32_t inplace;        /* -1 cost model; 0 never; 1 every round where allowed   */
   float inplace_weight;   /* cost-model weight of one merge, in row equivalents
-                             (0 = default 48)                                      */
+                             (0 = default 56)                                      */
   int32_t gather;         /* -1 auto; 0 window compaction only (no row gather)     */
   int32_t long_lists;     /* -1 auto; 0 the general distance kernel for 32<K<=128  */
   int32_t dist_grid;      /* 0 auto; > 0 caps the distance kernel's grid           */

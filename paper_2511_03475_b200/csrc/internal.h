@@ -49,7 +49,7 @@ struct ScratchLayout {
 struct Tuning {
   int value_codes = -1;         // -1 auto, 0 fp32 linkage matrices
   int inplace = -1;             // -1 cost model, 0 never, 1 wherever allowed
-  float inplace_weight = 48.f;  // cost-model weight of a merge (row equivalents; 48 measured best at C4)
+  float inplace_weight = 56.f;  // cost-model weight of a merge (row equivalents; measured after the 32-bit rescans: C4 flat 48-56, worse from 64; C3 11.0 -> 10.3 ms at 56)
   int gather = -1;              // -1 auto, 0 window compaction only
   int long_lists = -1;          // -1 auto, 0 general kernel for 32 < K <= 128
   int dist_grid = 0;            // 0 auto, > 0 grid cap of the distance kernel
